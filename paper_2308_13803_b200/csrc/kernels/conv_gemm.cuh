@@ -1,0 +1,57 @@
+// Host-facing description of one implicit-GEMM convolution launch (K1/K2/K5
+// in DESIGN.md). Shared by the runtime (which plans launches per layer and
+// batch size) and the kernel translation unit.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ds {
+
+constexpr int kConvBM = 128;       // UMMA M: output pixels per tile
+constexpr int kConvBK = 64;        // K elements per pipeline stage (one 128 B swizzle row)
+constexpr int kConvThreads = 192;  // 4 gather/epilogue warps + TMA warp + MMA warp
+constexpr int kConvMaxStages = 4;
+
+// One conv (or FC, as a 1x1 conv over a 1x1 image) as a GEMM
+//   Y[m, n] = act( sum_k A[m, k] * Wt[n, k] + bias[n] (+ R[m, n]) )
+// with m = (image, ho, wo), k = (r, s, c) flattened in that order (KRSC
+// weights), A gathered from the NHWC input on the fly.
+struct ConvGemmArgs {
+  CUtensorMap tmap_b;  // weights [Cout][Kpad] bf16, box {64, BN}, 128 B swizzle
+  CUtensorMap tmap_a;  // input viewed as [rows][C] (1x1 stride-1 convs only)
+  const __nv_bfloat16* x;
+  int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
+  int R, S, stride_h, stride_w, pad_h, pad_w;
+  int Ho, Wo;
+  int M;       // images * Ho * Wo
+  int num_kb;  // ceil(R*S*C / 64)
+  int taps;    // R*S
+  int Cout, BN, stages;
+  uint32_t tmem_cols;
+  const float* bias;
+  const __nv_bfloat16* residual;
+  int ld_res;
+  void* y;
+  int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
+  int out_f32, relu;
+};
+
+enum class ConvLoadMode : int {
+  kGather16 = 0,  // cp.async gather, 8 channels (16 B) per granule, C % 8 == 0
+  kGather8 = 1,   // cp.async gather, 4 channels (8 B) per granule, C == 4 (stem)
+  kTmaA = 2,      // 1x1 stride-1 conv: A is a plain 2D tile, loaded by TMA
+};
+
+// Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
+// elements) with a {64, box_rows} box and 128 B swizzle.
+bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         uint64_t row_stride_elems, uint32_t box_rows);
+
+size_t conv_gemm_smem_bytes(int BN, int stages);
+
+cudaError_t launch_conv_gemm(const ConvGemmArgs& args, ConvLoadMode mode, cudaStream_t stream);
+
+}  // namespace ds

@@ -1,0 +1,150 @@
+// Standalone bring-up check for the tcgen05 implicit-GEMM conv kernel:
+// random bf16 data, several conv geometries / load modes, compared against a
+// double-precision CPU loop over the same bf16 values. Dev tool only; the
+// parity gate proper lives in tests/ (through the C-ABI).
+#include "../paper_2308_13803_b200/csrc/kernels/conv_gemm.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+using namespace ds;
+
+static float bf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+struct Case {
+  const char* name;
+  int N, H, W, C, R, S, sh, sw, ph, pw, Cout, BN;
+  ConvLoadMode mode;
+  bool residual, f32, relu;
+  int ldy_extra, c_off;
+};
+
+static int run(const Case& cs) {
+  const int Ho = (cs.H + 2 * cs.ph - cs.R) / cs.sh + 1;
+  const int Wo = (cs.W + 2 * cs.pw - cs.S) / cs.sw + 1;
+  const int M = cs.N * Ho * Wo;
+  const int K = cs.R * cs.S * cs.C;
+  const int Kpad = (K + 63) / 64 * 64;
+  const int ldy = cs.Cout + cs.ldy_extra;
+  std::mt19937 rng(1234);
+  std::normal_distribution<float> nd(0.f, 1.f);
+  std::vector<__nv_bfloat16> hx((size_t)cs.N * cs.H * cs.W * cs.C), hw((size_t)cs.Cout * Kpad),
+      hr((size_t)M * cs.Cout);
+  std::vector<float> fx(hx.size()), fw(hw.size(), 0.f), fr(hr.size()), hb(cs.Cout);
+  for (size_t i = 0; i < hx.size(); ++i) { fx[i] = bf(nd(rng)); hx[i] = __float2bfloat16_rn(fx[i]); }
+  for (int n = 0; n < cs.Cout; ++n)
+    for (int k = 0; k < Kpad; ++k) {
+      float v = k < K ? bf(nd(rng) * 0.05f) : 0.f;
+      fw[(size_t)n * Kpad + k] = v;
+      hw[(size_t)n * Kpad + k] = __float2bfloat16_rn(v);
+    }
+  for (size_t i = 0; i < hr.size(); ++i) { fr[i] = bf(nd(rng)); hr[i] = __float2bfloat16_rn(fr[i]); }
+  for (int n = 0; n < cs.Cout; ++n) hb[n] = nd(rng) * 0.1f;
+
+  __nv_bfloat16 *dx, *dw, *dr;
+  float* db;
+  void* dy;
+  const size_t ybytes = (size_t)M * ldy * (cs.f32 ? 4 : 2);
+  cudaMalloc(&dx, hx.size() * 2 + 4096);
+  cudaMalloc(&dw, hw.size() * 2);
+  cudaMalloc(&dr, hr.size() * 2);
+  cudaMalloc(&db, hb.size() * 4);
+  cudaMalloc(&dy, ybytes);
+  cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(dr, hr.data(), hr.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dy, 0xFF, ybytes);  // NaN-fill so unwritten outputs are caught
+
+  ConvGemmArgs a{};
+  if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad, cs.BN)) {
+    printf("%s: tmap_b encode failed\n", cs.name);
+    return 1;
+  }
+  if (cs.mode == ConvLoadMode::kTmaA &&
+      !encode_tmap_2d_bf16(&a.tmap_a, dx, M, cs.C, cs.C, kConvBM)) {
+    printf("%s: tmap_a encode failed\n", cs.name);
+    return 1;
+  }
+  a.x = dx; a.H = cs.H; a.W = cs.W; a.C = cs.C; a.R = cs.R; a.S = cs.S;
+  a.stride_h = cs.sh; a.stride_w = cs.sw; a.pad_h = cs.ph; a.pad_w = cs.pw;
+  a.Ho = Ho; a.Wo = Wo; a.M = M; a.num_kb = Kpad / 64; a.taps = cs.R * cs.S;
+  a.Cout = cs.Cout; a.BN = cs.BN; a.stages = a.num_kb < 4 ? a.num_kb : 4;
+  a.tmem_cols = 32;
+  while ((int)a.tmem_cols < cs.BN) a.tmem_cols *= 2;
+  a.bias = db; a.residual = cs.residual ? dr : nullptr; a.ld_res = cs.Cout;
+  a.y = dy; a.ldy = ldy; a.c_off = cs.c_off; a.out_f32 = cs.f32; a.relu = cs.relu;
+  // channels [c_off, c_off+Cout) of an ldy-wide buffer; keep Cout+c_off <= ldy
+  cudaError_t e = launch_conv_gemm(a, cs.mode, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("%s: CUDA error %s\n", cs.name, cudaGetErrorString(e));
+    return 1;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 20; ++i) launch_conv_gemm(a, cs.mode, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= 20;
+
+  std::vector<uint8_t> hy(ybytes);
+  cudaMemcpy(hy.data(), dy, ybytes, cudaMemcpyDeviceToHost);
+  double max_err = 0, max_ref = 0;
+  long bad = 0;
+  for (int m = 0; m < M; ++m) {
+    const int n_img = m / (Ho * Wo), rem = m % (Ho * Wo), ho = rem / Wo, wo = rem % Wo;
+    for (int co = 0; co < cs.Cout; ++co) {
+      double acc = hb[co];
+      for (int r = 0; r < cs.R; ++r)
+        for (int s = 0; s < cs.S; ++s) {
+          const int hi = ho * cs.sh - cs.ph + r, wi = wo * cs.sw - cs.pw + s;
+          if (hi < 0 || hi >= cs.H || wi < 0 || wi >= cs.W) continue;
+          const float* xp = &fx[(((size_t)n_img * cs.H + hi) * cs.W + wi) * cs.C];
+          const float* wp = &fw[(size_t)co * Kpad + (r * cs.S + s) * cs.C];
+          for (int c = 0; c < cs.C; ++c) acc += (double)xp[c] * wp[c];
+        }
+      if (cs.residual) acc += fr[(size_t)m * cs.Cout + co];
+      if (cs.relu && acc < 0) acc = 0;
+      const size_t o = (size_t)m * ldy + cs.c_off + co;
+      double got = cs.f32 ? ((float*)hy.data())[o]
+                          : __bfloat162float(((__nv_bfloat16*)hy.data())[o]);
+      double err = std::fabs(got - acc);
+      if (!(err <= 0.02 + 0.01 * std::fabs(acc))) ++bad;
+      if (!(err <= max_err)) max_err = err;
+      if (std::fabs(acc) > max_ref) max_ref = std::fabs(acc);
+    }
+  }
+  const double flops = 2.0 * M * cs.Cout * K;
+  printf("%-28s M=%7d N=%5d K=%5d  max_err=%.4g (max|ref| %.3g) bad=%ld  %.3f us  %.1f TFLOP/s\n",
+         cs.name, M, cs.Cout, K, max_err, max_ref, bad, ms * 1e3, flops / (ms * 1e-3) / 1e12);
+  cudaFree(dx); cudaFree(dw); cudaFree(dr); cudaFree(db); cudaFree(dy);
+  return bad ? 1 : 0;
+}
+
+int main() {
+  const Case cases[] = {
+      {"1x1 s1 tmaA", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"1x1 s1 gather", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"3x3 s1 p1", 1, 28, 28, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"3x3 s2 p1 N96", 2, 28, 28, 64, 3, 3, 2, 2, 1, 1, 96, 96, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"7x7 s2 p3 C4 stem", 1, 64, 64, 4, 7, 7, 2, 2, 3, 3, 64, 64, ConvLoadMode::kGather8, false, false, true, 0, 0},
+      {"1x7 p(0,3) N160", 2, 17, 17, 128, 1, 7, 1, 1, 0, 3, 160, 160, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"fc 2048->1000 f32", 3, 1, 1, 2048, 1, 1, 1, 1, 0, 0, 1000, 256, ConvLoadMode::kTmaA, false, true, false, 0, 0},
+      {"1x1 residual+slice", 2, 7, 7, 512, 1, 1, 1, 1, 0, 0, 256, 128, ConvLoadMode::kTmaA, true, false, true, 64, 32},
+      {"3x3 C80 N192", 1, 20, 20, 80, 3, 3, 1, 1, 0, 0, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"1x1 7x7 2048 Mtail", 1, 7, 7, 512, 1, 1, 1, 1, 0, 0, 2048, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"fc 10 classes", 5, 1, 1, 128, 1, 1, 1, 1, 0, 0, 10, 16, ConvLoadMode::kTmaA, false, true, false, 0, 0},
+      {"big 1x1 s1", 64, 56, 56, 64, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"big 3x3 256", 32, 14, 14, 256, 3, 3, 1, 1, 1, 1, 256, 256, ConvLoadMode::kGather16, false, false, true, 0, 0},
+  };
+  int fails = 0;
+  for (const auto& c : cases) fails += run(c);
+  printf("%s (%d failing cases)\n", fails ? "FAIL" : "PASS", fails);
+  return fails ? 1 : 0;
+}
