@@ -1,0 +1,147 @@
+"""Python mirror of the reference device seam `dnnscaler::GpuSim`
+(reference proj/core/include/dnnscaler/gpu_sim.hpp:13-50) over the B200
+backend's C ABI. Same method names, argument meaning and error behaviour:
+the reference's std::invalid_argument surfaces as ValueError with the same
+message; CUDA failures raise DsError.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+MODELS = ("synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3")
+
+
+@dataclass(frozen=True)
+class Config:
+    """== GpuSim::Config (gpu_sim.hpp:15-18)."""
+
+    abs_max_bs: int = 128
+    max_mtl: int = 10
+
+
+@dataclass(frozen=True)
+class ModelInfo:
+    in_h: int
+    in_w: int
+    classes: int
+    n_ops: int
+    n_params: int
+    macs_per_image: float
+    weight_count: float
+    act_bytes_per_image: float
+
+
+def model_info(model_id: str) -> ModelInfo:
+    lib = _lib.load()
+    mi = _lib.DsModelInfo()
+    _lib.check(lib.ds_model_info_get(model_id.encode(), ctypes.byref(mi)))
+    return ModelInfo(mi.in_h, mi.in_w, mi.classes, mi.n_ops, mi.n_params, mi.macs_per_image,
+                     mi.weight_count, mi.act_bytes_per_image)
+
+
+def generate_images(model_id: str, first: int, count: int, seed: int = 42) -> np.ndarray:
+    """The synthetic inputs of DESIGN.md: u8 NHWC [count, h, w, 3]."""
+    info = model_info(model_id)
+    out = np.empty((count, info.in_h, info.in_w, 3), dtype=np.uint8)
+    _lib.check(_lib.load().ds_generate_images(info.in_h, info.in_w, seed, first, count,
+                                              out.ctypes.data))
+    return out
+
+
+class GpuBackend:
+    """One serving backend on one GPU (single-owner, not thread-safe)."""
+
+    def __init__(self, model_id: str, config: Config = Config(), seed: int = 42, device: int = 0):
+        lib = _lib.load()
+        self._lib = lib
+        self._h = ctypes.c_void_p()
+        _lib.check(lib.ds_backend_create(model_id.encode(),
+                                         _lib.DsConfig(config.abs_max_bs, config.max_mtl),
+                                         seed, device, ctypes.byref(self._h)))
+        self.model_id = model_id
+        self.info = model_info(model_id)
+        self._config = config
+
+    # ---- reference GpuSim method set -------------------------------------
+    def run_batch(self, bs: int) -> float:
+        lat = ctypes.c_double()
+        _lib.check(self._lib.ds_run_batch(self._h, bs, ctypes.byref(lat)))
+        return lat.value
+
+    def run_mt_request(self) -> float:
+        lat = ctypes.c_double()
+        _lib.check(self._lib.ds_run_mt_request(self._h, ctypes.byref(lat)))
+        return lat.value
+
+    def apply_instance_change(self, delta: int) -> float:
+        d = ctypes.c_double()
+        _lib.check(self._lib.ds_apply_instance_change(self._h, delta, ctypes.byref(d)))
+        return d.value
+
+    def set_mtl(self, target: int) -> float:
+        d = ctypes.c_double()
+        _lib.check(self._lib.ds_set_mtl(self._h, target, ctypes.byref(d)))
+        return d.value
+
+    def mtl(self) -> int:
+        return self._lib.ds_mtl(self._h)
+
+    def clock_ms(self) -> float:
+        return self._lib.ds_clock_ms(self._h)
+
+    def config(self) -> Config:
+        c = self._lib.ds_get_config(self._h)
+        return Config(c.abs_max_bs, c.max_mtl)
+
+    # ---- extensions --------------------------------------------------------
+    def run_batches(self, bs: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.float64)
+        _lib.check(self._lib.ds_run_batches(self._h, bs, count, out.ctypes.data))
+        return out
+
+    def run_mt_requests(self, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.float64)
+        _lib.check(self._lib.ds_run_mt_requests(self._h, count, out.ctypes.data))
+        return out
+
+    def forward(self, images: np.ndarray, probs: bool = False):
+        images = np.ascontiguousarray(images, dtype=np.uint8)
+        bs = images.shape[0]
+        logits = np.empty((bs, self.info.classes), dtype=np.float32)
+        p = np.empty_like(logits) if probs else None
+        _lib.check(self._lib.ds_forward(self._h, images.ctypes.data, bs, logits.ctypes.data,
+                                        p.ctypes.data if probs else None))
+        return (logits, p) if probs else logits
+
+    def set_host_io(self, enabled: bool) -> None:
+        _lib.check(self._lib.ds_set_host_io(self._h, 1 if enabled else 0))
+
+    def drain(self) -> None:
+        _lib.check(self._lib.ds_drain(self._h))
+
+    def stats(self) -> dict:
+        s = _lib.DsBackendStats()
+        _lib.check(self._lib.ds_backend_stats_get(self._h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.ds_backend_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -301,18 +301,6 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-template <int MODE>
-cudaError_t configure_once(size_t smem) {
-  // Raise the dynamic smem cap once per instantiation (max over calls).
-  static size_t configured = 0;
-  if (smem <= configured) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e == cudaSuccess) configured = smem;
-  return e;
-}
-
 }  // namespace
 
 bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -333,21 +321,35 @@ size_t conv_gemm_smem_bytes(int BN, int stages) {
   return smem_layout(BN, stages).total + 1024;  // + alignment slack
 }
 
+cudaError_t conv_gemm_init() {
+  // Opt every instantiation into the full 227 KiB of dynamic shared memory
+  // once, outside any stream capture.
+  static cudaError_t status = [] {
+    const int cap = 227 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
+    return e;
+  }();
+  return status;
+}
+
 cudaError_t launch_conv_gemm(const ConvGemmArgs& args, ConvLoadMode mode, cudaStream_t stream) {
   const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages);
   const dim3 grid((args.Cout + args.BN - 1) / args.BN, (args.M + kConvBM - 1) / kConvBM);
-  cudaError_t e;
   switch (mode) {
     case ConvLoadMode::kGather16:
-      if ((e = configure_once<0>(smem)) != cudaSuccess) return e;
       conv_gemm_kernel<0><<<grid, kConvThreads, smem, stream>>>(args);
       break;
     case ConvLoadMode::kGather8:
-      if ((e = configure_once<1>(smem)) != cudaSuccess) return e;
       conv_gemm_kernel<1><<<grid, kConvThreads, smem, stream>>>(args);
       break;
     case ConvLoadMode::kTmaA:
-      if ((e = configure_once<2>(smem)) != cudaSuccess) return e;
       conv_gemm_kernel<2><<<grid, kConvThreads, smem, stream>>>(args);
       break;
   }

@@ -52,6 +52,9 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint
 
 size_t conv_gemm_smem_bytes(int BN, int stages);
 
+// Must run once per device before the first launch (and before any capture).
+cudaError_t conv_gemm_init();
+
 cudaError_t launch_conv_gemm(const ConvGemmArgs& args, ConvLoadMode mode, cudaStream_t stream);
 
 }  // namespace ds

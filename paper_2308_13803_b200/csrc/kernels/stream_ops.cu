@@ -1,0 +1,211 @@
+// HBM-bound layers of the forward pass. Each thread owns one output pixel x
+// 8 channels (one 16 B vector), so consecutive threads in a warp touch
+// consecutive 16 B chunks of the NHWC row: fully coalesced 512 B per warp
+// access. Neighbouring taps of the stencils hit L1/L2, so DRAM traffic stays
+// close to one read of the input and one write of the output.
+#include "stream_ops.cuh"
+
+namespace ds {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  return make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
+}
+
+inline unsigned grid_for(long long work) {
+  return static_cast<unsigned>((work + kBlock - 1) / kBlock);
+}
+
+__global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __restrict__ out,
+                                   long long pixels) {
+  const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= pixels) return;
+  const uint8_t* s = img + 3 * p;
+  float v[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) v[c] = (static_cast<float>(s[c]) - 127.5f) / 63.75f;
+  out[p] = make_uint2(pack2(v[0], v[1]), pack2(v[2], 0.0f));
+}
+
+__global__ void dwconv3x3_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
+                                 const float4* __restrict__ bias, uint4* __restrict__ y, int h,
+                                 int wd, int cg, int ho, int wo, int stride, long long work) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= work) return;
+  const int g = static_cast<int>(i % cg);
+  long long pix = i / cg;
+  const int ox = static_cast<int>(pix % wo);
+  pix /= wo;
+  const int oy = static_cast<int>(pix % ho);
+  const int n = static_cast<int>(pix / ho);
+  float acc[8];
+  const float4 b0 = __ldg(bias + 2 * g), b1 = __ldg(bias + 2 * g + 1);
+  acc[0] = b0.x; acc[1] = b0.y; acc[2] = b0.z; acc[3] = b0.w;
+  acc[4] = b1.x; acc[5] = b1.y; acc[6] = b1.z; acc[7] = b1.w;
+  const int iy0 = oy * stride - 1, ix0 = ox * stride - 1;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int iy = iy0 + r;
+    if (iy < 0 || iy >= h) continue;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int ix = ix0 + s;
+      if (ix < 0 || ix >= wd) continue;
+      float xv[8], wv[8];
+      unpack8(__ldg(x + ((static_cast<long long>(n) * h + iy) * wd + ix) * cg + g), xv);
+      unpack8(__ldg(w + (r * 3 + s) * cg + g), wv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(xv[e], wv[e], acc[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.0f);
+  y[i] = pack8(acc);
+}
+
+__global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
+                               int cg, int ho, int wo, int stride, int pad, int is_max, int ldo_g,
+                               int coff_g, long long work) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= work) return;
+  const int g = static_cast<int>(i % cg);
+  long long pix = i / cg;
+  const int ox = static_cast<int>(pix % wo);
+  pix /= wo;
+  const int oy = static_cast<int>(pix % ho);
+  const int n = static_cast<int>(pix / ho);
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = is_max ? -INFINITY : 0.0f;
+  const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int iy = iy0 + r;
+    if (iy < 0 || iy >= h) continue;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int ix = ix0 + s;
+      if (ix < 0 || ix >= w) continue;
+      float xv[8];
+      unpack8(__ldg(x + ((static_cast<long long>(n) * h + iy) * w + ix) * cg + g), xv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = is_max ? fmaxf(acc[e], xv[e]) : acc[e] + xv[e];
+    }
+  }
+  if (!is_max) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = acc[e] / 9.0f;
+  }
+  const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox;
+  y[opix * ldo_g + coff_g + g] = pack8(acc);
+}
+
+__global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int hw,
+                                      int cg, long long work) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= work) return;
+  const int g = static_cast<int>(i % cg);
+  const long long n = i / cg;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint4* p = x + n * hw * cg + g;
+  for (int q = 0; q < hw; ++q) {
+    float xv[8];
+    unpack8(__ldg(p + static_cast<long long>(q) * cg), xv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += xv[e];
+  }
+  const float inv = static_cast<float>(hw);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = acc[e] / inv;
+  y[i] = pack8(acc);
+}
+
+__global__ void softmax_kernel(const float* __restrict__ logits, float* __restrict__ probs, int n,
+                               int classes) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* l = logits + static_cast<long long>(row) * classes;
+  float mx = -INFINITY;
+  for (int j = lane; j < classes; j += 32) mx = fmaxf(mx, l[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int j = lane; j < classes; j += 32) sum += expf(l[j] - mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = 1.0f / sum;
+  float* p = probs + static_cast<long long>(row) * classes;
+  for (int j = lane; j < classes; j += 32) p[j] = expf(l[j] - mx) * inv;
+}
+
+}  // namespace
+
+cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
+                               cudaStream_t stream) {
+  const long long pixels = static_cast<long long>(n) * h * w;
+  stage_input_kernel<<<grid_for(pixels), kBlock, 0, stream>>>(img, reinterpret_cast<uint2*>(out),
+                                                              pixels);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
+                             __nv_bfloat16* y, int n, int h, int wd, int c, int stride,
+                             cudaStream_t stream) {
+  const int ho = (h + 2 - 3) / stride + 1, wo = (wd + 2 - 3) / stride + 1;
+  const int cg = c / 8;
+  const long long work = static_cast<long long>(n) * ho * wo * cg;
+  dwconv3x3_kernel<<<grid_for(work), kBlock, 0, stream>>>(
+      reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
+      reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd, cg, ho, wo,
+      stride, work);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int h, int w, int c,
+                           int stride, int pad, bool is_max, int ldo, int c_off,
+                           cudaStream_t stream) {
+  const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
+  const int cg = c / 8;
+  const long long work = static_cast<long long>(n) * ho * wo * cg;
+  pool3x3_kernel<<<grid_for(work), kBlock, 0, stream>>>(
+      reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, stride,
+      pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,
+                                  cudaStream_t stream) {
+  const int cg = c / 8;
+  const long long work = static_cast<long long>(n) * cg;
+  global_avgpool_kernel<<<grid_for(work), kBlock, 0, stream>>>(
+      reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, work);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax(const float* logits, float* probs, int n, int classes,
+                           cudaStream_t stream) {
+  const int rows_per_block = kBlock / 32;
+  softmax_kernel<<<(n + rows_per_block - 1) / rows_per_block, kBlock, 0, stream>>>(logits, probs,
+                                                                                  n, classes);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

@@ -1,0 +1,36 @@
+// Launchers for the HBM-bound layers of the forward pass (K3/K4/K5b/K6 in
+// DESIGN.md). All tensors are NHWC bf16; every kernel moves 16 B (8 channels)
+// per thread per access, fp32 math inside, bf16 rounding on store.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ds {
+
+// u8 NHWC [n][h][w][3] images -> normalised bf16 NHWC [n][h][w][4] (channel 3
+// zero), x = (p - 127.5) / 63.75, the stem's 8-byte gather granule.
+cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
+                               cudaStream_t stream);
+
+// Depthwise 3x3, pad 1, stride 1|2, + bias, ReLU. w: [9][C] bf16 (tap-major).
+cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
+                             __nv_bfloat16* y, int n, int h, int wd, int c, int stride,
+                             cudaStream_t stream);
+
+// 3x3 max pool (stride, pad) or 3x3 average pool (count_include_pad, /9).
+// Output may be a channel slice of a wider buffer (ldo channels, c_off).
+cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int h, int w, int c,
+                           int stride, int pad, bool is_max, int ldo, int c_off,
+                           cudaStream_t stream);
+
+// Mean over all pixels: [n][hw][c] -> [n][c] bf16.
+cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,
+                                  cudaStream_t stream);
+
+// Row softmax over fp32 logits [n][classes] (one warp per row).
+cudaError_t launch_softmax(const float* logits, float* probs, int n, int classes,
+                           cudaStream_t stream);
+
+}  // namespace ds

@@ -1,0 +1,447 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "../kernels/stream_ops.cuh"
+
+namespace ds {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// N tile: one tile when Cout fits in 256 (UMMA N <= 256, multiple of 16),
+// otherwise the smallest even split.
+int choose_bn(int cout) {
+  if (cout <= 256) return round_up(cout, 16);
+  const int n = (cout + 255) / 256;
+  return round_up((cout + n - 1) / n, 16);
+}
+
+int choose_stages(int bn, int num_kb) {
+  const int per_stage = kConvBM * kConvBK * 2 + bn * kConvBK * 2;
+  int st = (200 * 1024) / per_stage;
+  st = std::min(st, kConvMaxStages);
+  st = std::min(st, num_kb);
+  return std::max(st, 1);
+}
+
+uint32_t tmem_cols_for(int bn) {
+  uint32_t c = 32;
+  while (static_cast<int>(c) < bn) c <<= 1;
+  return c;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Instance
+
+Instance::Instance(const ModelSpec& m, int max_bs, int device)
+    : m_(m), max_bs_(max_bs), device_(device) {
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  check_cuda(conv_gemm_init(), "conv_gemm_init");
+  check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  const HostParams& hp = params_for(m);
+
+  size_t off = 0;
+  auto take = [&off](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t w_off = take(hp.w.size() * sizeof(uint16_t));
+  const size_t b_off = take(hp.b.size() * sizeof(float));
+  const size_t img_off = take(static_cast<size_t>(max_bs) * m.in_h * m.in_w * 3);
+  std::vector<size_t> buf_off;
+  for (const auto& b : m.buffers)
+    buf_off.push_back(
+        take(static_cast<size_t>(max_bs) * b.h * b.w * b.c * (b.f32 ? sizeof(float) : 2)));
+  const size_t probs_off = take(static_cast<size_t>(max_bs) * m.classes * sizeof(float));
+  device_bytes_ = off;
+  check_cuda(cudaMalloc(&d_arena_, off), "cudaMalloc(instance arena)");
+  uint8_t* base = static_cast<uint8_t*>(d_arena_);
+  check_cuda(cudaMemsetAsync(d_arena_, 0, off, stream_), "cudaMemset");
+  d_w_ = reinterpret_cast<uint16_t*>(base + w_off);
+  d_b_ = reinterpret_cast<float*>(base + b_off);
+  d_images_ = base + img_off;
+  for (size_t o : buf_off) bufs_.push_back(base + o);
+  d_probs_ = reinterpret_cast<float*>(base + probs_off);
+  d_logits_ = static_cast<float*>(bufs_.at(m.logits));
+  check_cuda(cudaMemcpyAsync(d_w_, hp.w.data(), hp.w.size() * sizeof(uint16_t),
+                             cudaMemcpyHostToDevice, stream_),
+             "upload weights");
+  check_cuda(cudaMemcpyAsync(d_b_, hp.b.data(), hp.b.size() * sizeof(float),
+                             cudaMemcpyHostToDevice, stream_),
+             "upload biases");
+
+  plans_.resize(m.ops.size());
+  kernels_per_forward_ = 2;  // input staging + softmax
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    ++kernels_per_forward_;
+    if (op.kind != OpKind::kConv && op.kind != OpKind::kFc) continue;
+    const ParamSpec& p = m.params.at(op.param);
+    const BufferSpec& in = m.buffers.at(op.in);
+    const BufferSpec& out = m.buffers.at(op.out);
+    ConvPlan& pl = plans_[i];
+    ConvGemmArgs& a = pl.args;
+    std::memset(&a, 0, sizeof(a));
+    a.x = static_cast<const __nv_bfloat16*>(bufs_[op.in]);
+    a.H = in.h;
+    a.W = in.w;
+    a.C = in.c;
+    a.R = op.r;
+    a.S = op.s;
+    a.stride_h = op.sh;
+    a.stride_w = op.sw;
+    a.pad_h = op.ph;
+    a.pad_w = op.pw;
+    pl.ho = a.Ho = out.h;
+    pl.wo = a.Wo = out.w;
+    if (op.kind == OpKind::kFc) {
+      a.H = a.W = 1;
+      a.Ho = a.Wo = pl.ho = pl.wo = 1;
+    }
+    const int kpad = hp.kpad.at(op.param);
+    a.num_kb = kpad / kConvBK;
+    a.taps = op.r * op.s;
+    a.Cout = p.cout;
+    a.BN = choose_bn(p.cout);
+    a.stages = choose_stages(a.BN, a.num_kb);
+    a.tmem_cols = tmem_cols_for(a.BN);
+    a.bias = d_b_ + hp.b_off.at(op.param);
+    if (op.residual >= 0) {
+      a.residual = static_cast<const __nv_bfloat16*>(bufs_[op.residual]);
+      a.ld_res = m.buffers.at(op.residual).c;
+    }
+    a.y = bufs_[op.out];
+    a.ldy = out.c;
+    a.c_off = op.c_off;
+    a.out_f32 = out.f32 ? 1 : 0;
+    a.relu = op.relu ? 1 : 0;
+    if (in.c == 4) {
+      pl.mode = ConvLoadMode::kGather8;
+    } else if (in.c % 8 != 0) {
+      throw std::logic_error("conv input channels must be a multiple of 8");
+    } else if (op.r == 1 && op.s == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 && op.pw == 0 &&
+               in.c >= kConvBK) {
+      pl.mode = ConvLoadMode::kTmaA;
+    } else {
+      pl.mode = ConvLoadMode::kGather16;
+    }
+    if (!encode_tmap_2d_bf16(&a.tmap_b, d_w_ + hp.w_off.at(op.param), p.cout, kpad, kpad, a.BN))
+      throw CudaError("cuTensorMapEncodeTiled failed (weights)");
+    if (pl.mode == ConvLoadMode::kTmaA) {
+      const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
+      if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
+        throw CudaError("cuTensorMapEncodeTiled failed (activations)");
+    }
+  }
+  check_cuda(cudaStreamSynchronize(stream_), "instance setup");
+}
+
+Instance::~Instance() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+  if (d_arena_) cudaFree(d_arena_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Instance::enqueue_layers(int bs) {
+  const ModelSpec& m = m_;
+  const HostParams& hp = params_for(m);
+  check_cuda(launch_stage_input(d_images_, static_cast<__nv_bfloat16*>(bufs_[0]), bs, m.in_h,
+                                m.in_w, stream_),
+             "stage_input");
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    const BufferSpec& in = m.buffers[op.in];
+    const BufferSpec& out = m.buffers[op.out];
+    const auto* x = static_cast<const __nv_bfloat16*>(bufs_[op.in]);
+    auto* y = static_cast<__nv_bfloat16*>(bufs_[op.out]);
+    cudaError_t e = cudaSuccess;
+    switch (op.kind) {
+      case OpKind::kConv:
+      case OpKind::kFc: {
+        ConvGemmArgs a = plans_[i].args;
+        a.M = bs * plans_[i].ho * plans_[i].wo;
+        e = launch_conv_gemm(a, plans_[i].mode, stream_);
+        break;
+      }
+      case OpKind::kDwConv: {
+        const auto* w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off[op.param]);
+        e = launch_dwconv3x3(x, w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c, op.sh,
+                             stream_);
+        break;
+      }
+      case OpKind::kMaxPool:
+      case OpKind::kAvgPool:
+        e = launch_pool3x3(x, y, bs, in.h, in.w, in.c, op.sh, op.ph, op.kind == OpKind::kMaxPool,
+                           out.c, op.c_off, stream_);
+        break;
+      case OpKind::kGlobalAvgPool:
+        e = launch_global_avgpool(x, y, bs, in.h * in.w, in.c, stream_);
+        break;
+    }
+    check_cuda(e, "layer launch");
+  }
+  check_cuda(launch_softmax(d_logits_, d_probs_, bs, m.classes, stream_), "softmax");
+}
+
+void Instance::enqueue_forward(int bs) {
+  if (bs < 1 || bs > max_bs_) throw std::invalid_argument("invalid batch size");
+  auto it = graphs_.find(bs);
+  if (it == graphs_.end()) {
+    cudaGraph_t g = nullptr;
+    check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
+    try {
+      enqueue_layers(bs);
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    check_cuda(cudaStreamEndCapture(stream_, &g), "capture end");
+    cudaGraphExec_t exec = nullptr;
+    check_cuda(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    it = graphs_.emplace(bs, exec).first;
+  }
+  check_cuda(cudaGraphLaunch(it->second, stream_), "graph launch");
+}
+
+// ------------------------------------------------------------------ Backend
+
+Backend::Backend(const std::string& model_id, BackendConfig cfg, uint64_t seed, int device)
+    : model_(build_model(model_id)), cfg_(cfg), seed_(seed), device_(device) {
+  if (cfg_.abs_max_bs < 1 || cfg_.max_mtl < 1)
+    throw std::invalid_argument("invalid device limits");  // reference gpu_sim.cpp:9-10
+  check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+  params_for(model_);
+  pool_images_ = std::max(cfg_.abs_max_bs, cfg_.max_mtl);
+  const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
+  host_images_.resize(img_bytes * pool_images_);
+  generate_images(model_.in_h, model_.in_w, seed_, 0, pool_images_, host_images_.data());
+  inst_.resize(cfg_.max_mtl);
+  inflight_.resize(cfg_.max_mtl);
+  io_cursor_.assign(cfg_.max_mtl, 0);
+  pinned_logits_.assign(cfg_.max_mtl, nullptr);
+  instance(0);
+}
+
+Backend::~Backend() {
+  cudaSetDevice(device_);
+  try {
+    drain();
+  } catch (...) {
+  }
+  inst_.clear();
+  for (cudaEvent_t e : all_events_) cudaEventDestroy(e);
+  if (pinned_images_) cudaFreeHost(pinned_images_);
+  for (float* p : pinned_logits_)
+    if (p) cudaFreeHost(p);
+}
+
+Instance& Backend::instance(int i) {
+  if (!inst_.at(i)) {
+    const int max_bs = (i == 0) ? cfg_.abs_max_bs : 1;
+    inst_[i] = std::make_unique<Instance>(model_, max_bs, device_);
+    const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
+    const int first = (i == 0) ? 0 : (i % pool_images_);
+    check_cuda(cudaMemcpy(inst_[i]->images(), host_images_.data() + img_bytes * first,
+                          img_bytes * max_bs, cudaMemcpyHostToDevice),
+               "upload images");
+  }
+  return *inst_[i];
+}
+
+int Backend::instances_created() const {
+  int n = 0;
+  for (const auto& p : inst_) n += p ? 1 : 0;
+  return n;
+}
+
+size_t Backend::device_bytes() const {
+  size_t n = 0;
+  for (const auto& p : inst_)
+    if (p) n += p->device_bytes();
+  return n;
+}
+
+cudaStream_t Backend::batch_stream() const { return inst_[0]->stream(); }
+
+cudaEvent_t Backend::take_event() {
+  if (free_events_.empty()) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    all_events_.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = free_events_.back();
+  free_events_.pop_back();
+  return e;
+}
+
+void Backend::enqueue_request(int i, int bs) {
+  Instance& I = instance(i);
+  Inflight f{take_event(), take_event(), bs};
+  cudaStream_t s = I.stream();
+  check_cuda(cudaEventRecord(f.start, s), "event record");
+  const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
+  if (host_io_) {
+    int64_t& cur = io_cursor_[i];
+    if (cur + bs > pool_images_) cur = 0;
+    const uint8_t* src = pinned_images_ + img_bytes * static_cast<size_t>(cur);
+    cur = (i == 0) ? cur + bs : (cur + cfg_.max_mtl) % pool_images_;
+    check_cuda(cudaMemcpyAsync(I.images(), src, img_bytes * bs, cudaMemcpyHostToDevice, s),
+               "H2D images");
+    h2d_bytes_ += static_cast<int64_t>(img_bytes) * bs;
+  }
+  I.enqueue_forward(bs);
+  kernel_launches_ += I.kernels_per_forward();
+  if (host_io_) {
+    const size_t lb = static_cast<size_t>(bs) * model_.classes * sizeof(float);
+    check_cuda(cudaMemcpyAsync(pinned_logits_[i], I.logits(), lb, cudaMemcpyDeviceToHost, s),
+               "D2H logits");
+    d2h_bytes_ += static_cast<int64_t>(lb);
+  }
+  check_cuda(cudaEventRecord(f.end, s), "event record");
+  inflight_[i].push_back(f);
+}
+
+double Backend::complete_oldest(int i) {
+  Inflight f = inflight_[i].front();
+  inflight_[i].pop_front();
+  check_cuda(cudaEventSynchronize(f.end), "request");
+  float ms = 0.0f;
+  check_cuda(cudaEventElapsedTime(&ms, f.start, f.end), "cudaEventElapsedTime");
+  free_events_.push_back(f.start);
+  free_events_.push_back(f.end);
+  return static_cast<double>(ms);
+}
+
+void Backend::drain() {
+  for (size_t i = 0; i < inflight_.size(); ++i)
+    while (!inflight_[i].empty()) complete_oldest(static_cast<int>(i));
+  batch_bs_ = 0;
+  mt_active_ = false;
+  rr_ = 0;
+}
+
+void Backend::run_batches(int bs, int count, double* lat_out) {
+  if (bs < 1 || bs > cfg_.abs_max_bs) throw std::invalid_argument("invalid batch size");
+  if (mt_active_ || (batch_bs_ != 0 && batch_bs_ != bs)) drain();
+  batch_bs_ = bs;
+  for (int j = 0; j < count; ++j) {
+    while (static_cast<int>(inflight_[0].size()) < kDepth) enqueue_request(0, bs);
+    const double lat = complete_oldest(0);
+    clock_ms_ += lat;  // reference gpu_sim.cpp:16
+    lat_out[j] = lat;
+  }
+}
+
+void Backend::run_mt_requests(int count, double* lat_out) {
+  if (batch_bs_ != 0) drain();
+  mt_active_ = true;
+  for (int j = 0; j < count; ++j) {
+    for (int i = 0; i < mtl_; ++i)
+      while (static_cast<int>(inflight_[i].size()) < kDepth) enqueue_request(i, 1);
+    const double lat = complete_oldest(rr_);
+    rr_ = (rr_ + 1) % mtl_;
+    clock_ms_ += lat / static_cast<double>(mtl_);  // reference gpu_sim.cpp:22
+    lat_out[j] = lat;
+  }
+}
+
+double Backend::run_batch(int bs) {
+  double lat = 0.0;
+  run_batches(bs, 1, &lat);
+  return lat;
+}
+
+double Backend::run_mt_request() {
+  double lat = 0.0;
+  run_mt_requests(1, &lat);
+  return lat;
+}
+
+double Backend::apply_instance_change(int delta) {
+  // Validation and messages follow reference gpu_sim.cpp:26-37.
+  if (delta == 0) return 0.0;
+  if (delta != 1 && delta != -1) throw std::invalid_argument("instance changes are single steps");
+  const int target = mtl_ + delta;
+  if (target < 1) throw std::invalid_argument("cannot terminate last instance");
+  if (target > cfg_.max_mtl) throw std::invalid_argument("instance limit exceeded");
+  drain();
+  const auto t0 = std::chrono::steady_clock::now();
+  if (delta > 0) {
+    // Launch: weights, workspace and stream (first time), then one warm-up
+    // request, which also captures the instance's bs=1 graph.
+    Instance& I = instance(target - 1);
+    I.enqueue_forward(1);
+    check_cuda(cudaStreamSynchronize(I.stream()), "instance warm-up");
+  }
+  mtl_ = target;
+  const double delay =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  clock_ms_ += delay;
+  return delay;
+}
+
+double Backend::set_mtl(int target) {
+  // reference gpu_sim.cpp:39-46
+  if (target < 1) throw std::invalid_argument("cannot terminate last instance");
+  if (target > cfg_.max_mtl) throw std::invalid_argument("instance limit exceeded");
+  double total = 0.0;
+  while (mtl_ < target) total += apply_instance_change(1);
+  while (mtl_ > target) total += apply_instance_change(-1);
+  return total;
+}
+
+void Backend::forward(const uint8_t* host_images, int bs, float* host_logits, float* host_probs) {
+  if (bs < 1 || bs > cfg_.abs_max_bs) throw std::invalid_argument("invalid batch size");
+  drain();
+  Instance& I = instance(0);
+  cudaStream_t s = I.stream();
+  const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
+  check_cuda(cudaMemcpyAsync(I.images(), host_images, img_bytes * bs, cudaMemcpyHostToDevice, s),
+             "H2D images");
+  I.enqueue_forward(bs);
+  kernel_launches_ += I.kernels_per_forward();
+  const size_t lb = static_cast<size_t>(bs) * model_.classes * sizeof(float);
+  if (host_logits)
+    check_cuda(cudaMemcpyAsync(host_logits, I.logits(), lb, cudaMemcpyDeviceToHost, s), "D2H");
+  if (host_probs)
+    check_cuda(cudaMemcpyAsync(host_probs, I.probs(), lb, cudaMemcpyDeviceToHost, s), "D2H");
+  // Put the resident synthetic batch back for the serving paths.
+  check_cuda(cudaMemcpyAsync(I.images(), host_images_.data(), img_bytes * I.max_bs(),
+                             cudaMemcpyHostToDevice, s),
+             "restore images");
+  check_cuda(cudaStreamSynchronize(s), "forward");
+}
+
+void Backend::set_host_io(bool enabled) {
+  drain();
+  if (enabled && !pinned_images_) {
+    check_cuda(cudaMallocHost(&pinned_images_, host_images_.size()), "cudaMallocHost");
+    std::memcpy(pinned_images_, host_images_.data(), host_images_.size());
+    for (int i = 0; i < cfg_.max_mtl; ++i) {
+      const int mbs = (i == 0) ? cfg_.abs_max_bs : 1;
+      check_cuda(cudaMallocHost(&pinned_logits_[i],
+                                static_cast<size_t>(mbs) * model_.classes * sizeof(float)),
+                 "cudaMallocHost");
+    }
+  }
+  host_io_ = enabled;
+}
+
+}  // namespace ds

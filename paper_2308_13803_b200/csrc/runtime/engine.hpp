@@ -1,0 +1,156 @@
+// The B200 serving backend: the device-side replacement of the reference's
+// `GpuSim` (reference gpu_sim.hpp:13-50, gpu_sim.cpp:7-46).
+//
+//   Instance  one co-located model replica: its own weights, activation
+//             workspace, stream, and a CUDA graph per batch size.
+//   Backend   GpuSim's method set over real forward passes. run_batch serves
+//             one batch on instance 0; run_mt_request serves one bs=1 request
+//             while every active instance keeps requests in flight on its own
+//             stream; latencies are cudaEvent pairs around each request. The
+//             virtual clock keeps the reference's arithmetic (clock += lat,
+//             += lat/mtl, += instance-change delay) so a recorded tape replays
+//             bit-exactly through the reference control plane.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <deque>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../kernels/conv_gemm.cuh"
+#include "model.hpp"
+#include "synth.hpp"
+
+namespace ds {
+
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+class Instance {
+ public:
+  Instance(const ModelSpec& m, int max_bs, int device);
+  ~Instance();
+  Instance(const Instance&) = delete;
+  Instance& operator=(const Instance&) = delete;
+
+  // Enqueues one forward over the first bs images of images() (graph per bs).
+  void enqueue_forward(int bs);
+  // Same sequence without a graph (used for capture and first launch).
+  void enqueue_layers(int bs);
+
+  cudaStream_t stream() const { return stream_; }
+  uint8_t* images() const { return d_images_; }
+  float* logits() const { return d_logits_; }
+  float* probs() const { return d_probs_; }
+  int max_bs() const { return max_bs_; }
+  int kernels_per_forward() const { return kernels_per_forward_; }
+  size_t device_bytes() const { return device_bytes_; }
+
+ private:
+  struct ConvPlan {
+    ConvGemmArgs args;
+    ConvLoadMode mode;
+    int ho, wo;
+  };
+  const ModelSpec& m_;
+  int max_bs_;
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  void* d_arena_ = nullptr;
+  size_t device_bytes_ = 0;
+  uint16_t* d_w_ = nullptr;
+  float* d_b_ = nullptr;
+  uint8_t* d_images_ = nullptr;
+  float* d_logits_ = nullptr;
+  float* d_probs_ = nullptr;
+  std::vector<void*> bufs_;
+  std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
+  std::map<int, cudaGraphExec_t> graphs_;
+  int kernels_per_forward_ = 0;
+};
+
+struct BackendConfig {
+  int abs_max_bs = 128;  // reference gpu_sim.hpp:16
+  int max_mtl = 10;      // reference gpu_sim.hpp:17
+};
+
+class Backend {
+ public:
+  Backend(const std::string& model_id, BackendConfig cfg, uint64_t seed, int device);
+  ~Backend();
+  Backend(const Backend&) = delete;
+  Backend& operator=(const Backend&) = delete;
+
+  // --- reference GpuSim method set (gpu_sim.hpp:23-40) ---
+  double run_batch(int bs);
+  double run_mt_request();
+  double apply_instance_change(int delta);
+  double set_mtl(int target);
+  int mtl() const { return mtl_; }
+  double clock_ms() const { return clock_ms_; }
+  const BackendConfig& config() const { return cfg_; }
+
+  // --- extensions ---
+  // One control window: `count` consecutive seam calls at a fixed knob.
+  void run_batches(int bs, int count, double* lat_out);
+  void run_mt_requests(int count, double* lat_out);
+  // Parity path: host u8 NHWC images in, fp32 logits (and probs) out.
+  void forward(const uint8_t* host_images, int bs, float* host_logits, float* host_probs);
+  // End-to-end mode: every request copies its images from a pinned host pool
+  // and reads its logits back inside the timed event pair.
+  void set_host_io(bool enabled);
+  bool host_io() const { return host_io_; }
+  // Drains every in-flight request (device idle on return).
+  void drain();
+
+  const ModelSpec& model() const { return model_; }
+  int64_t kernel_launches() const { return kernel_launches_; }
+  int64_t h2d_bytes() const { return h2d_bytes_; }
+  int64_t d2h_bytes() const { return d2h_bytes_; }
+  int instances_created() const;
+  size_t device_bytes() const;
+  cudaStream_t batch_stream() const;
+
+ private:
+  struct Inflight {
+    cudaEvent_t start, end;
+    int bs;
+  };
+  Instance& instance(int i);
+  void enqueue_request(int i, int bs);
+  double complete_oldest(int i);
+  cudaEvent_t take_event();
+
+  ModelSpec model_;
+  BackendConfig cfg_;
+  uint64_t seed_;
+  int device_;
+  std::vector<std::unique_ptr<Instance>> inst_;
+  std::vector<std::deque<Inflight>> inflight_;
+  std::vector<cudaEvent_t> free_events_;
+  std::vector<cudaEvent_t> all_events_;
+  std::vector<uint8_t> host_images_;  // synthetic image pool (pageable master copy)
+  uint8_t* pinned_images_ = nullptr;  // pinned copy for host-I/O mode
+  std::vector<float*> pinned_logits_;
+  std::vector<int64_t> io_cursor_;
+  int pool_images_ = 0;
+  bool host_io_ = false;
+  int batch_bs_ = 0;  // bs of batches in flight on instance 0 (0: none)
+  bool mt_active_ = false;
+  int rr_ = 0;
+  int mtl_ = 1;
+  double clock_ms_ = 0.0;
+  int64_t kernel_launches_ = 0;
+  int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  static constexpr int kDepth = 2;  // requests kept in flight per stream
+};
+
+}  // namespace ds

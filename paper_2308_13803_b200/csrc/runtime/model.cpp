@@ -1,0 +1,326 @@
+// Architecture definitions (see model.hpp). Parameter layers are numbered in
+// the order the builder emits them; that index seeds each layer's weights
+// (mix_seed(42, 1000 + index), reference random.hpp:10-15), so the order here
+// is part of the model definition and is restated independently in
+// oracle/fwd_oracle.c.
+#include "model.hpp"
+
+#include <stdexcept>
+
+namespace ds {
+
+namespace {
+
+class Builder {
+ public:
+  explicit Builder(ModelSpec& m) : m_(m) {}
+
+  int buffer(int h, int w, int c, bool f32 = false) {
+    m_.buffers.push_back(BufferSpec{h, w, c, f32});
+    return static_cast<int>(m_.buffers.size()) - 1;
+  }
+
+  const BufferSpec& buf(int id) const { return m_.buffers.at(id); }
+
+  // Dense conv; writes channels [c_off, c_off + cout) of `out` (a new buffer
+  // when out < 0). Returns the output buffer.
+  int conv(int in, int cout, int r, int s, int sh, int sw, int ph, int pw, int out = -1,
+           int c_off = 0, int residual = -1, bool relu = true, float gain = 1.0f) {
+    const BufferSpec ib = buf(in);
+    const int ho = (ib.h + 2 * ph - r) / sh + 1;
+    const int wo = (ib.w + 2 * pw - s) / sw + 1;
+    if (out < 0) out = buffer(ho, wo, cout);
+    const BufferSpec ob = buf(out);
+    if (ob.h != ho || ob.w != wo || c_off + cout > ob.c)
+      throw std::logic_error("conv output shape mismatch in " + m_.id);
+    ParamSpec p;
+    p.kind = OpKind::kConv;
+    p.cout = cout;
+    p.r = r;
+    p.s = s;
+    p.cin_stored = ib.c;
+    p.cin = (in == 0) ? 3 : ib.c;
+    p.gain = gain;
+    m_.params.push_back(p);
+    OpSpec op;
+    op.kind = OpKind::kConv;
+    op.in = in;
+    op.out = out;
+    op.c_off = c_off;
+    op.residual = residual;
+    op.r = r;
+    op.s = s;
+    op.sh = sh;
+    op.sw = sw;
+    op.ph = ph;
+    op.pw = pw;
+    op.relu = relu;
+    op.param = static_cast<int>(m_.params.size()) - 1;
+    m_.ops.push_back(op);
+    m_.macs_per_image += static_cast<double>(ho) * wo * cout * r * s * p.cin;
+    return out;
+  }
+
+  int conv_sq(int in, int cout, int k, int stride, int pad, int out = -1, int c_off = 0) {
+    return conv(in, cout, k, k, stride, stride, pad, pad, out, c_off);
+  }
+
+  int dw(int in, int stride) {
+    const BufferSpec ib = buf(in);
+    const int ho = (ib.h + 2 - 3) / stride + 1, wo = (ib.w + 2 - 3) / stride + 1;
+    const int out = buffer(ho, wo, ib.c);
+    ParamSpec p;
+    p.kind = OpKind::kDwConv;
+    p.cout = ib.c;
+    p.r = p.s = 3;
+    p.cin = p.cin_stored = 1;
+    m_.params.push_back(p);
+    OpSpec op;
+    op.kind = OpKind::kDwConv;
+    op.in = in;
+    op.out = out;
+    op.r = op.s = 3;
+    op.sh = op.sw = stride;
+    op.ph = op.pw = 1;
+    op.param = static_cast<int>(m_.params.size()) - 1;
+    m_.ops.push_back(op);
+    m_.macs_per_image += static_cast<double>(ho) * wo * ib.c * 9;
+    return out;
+  }
+
+  int pool(int in, bool is_max, int stride, int pad, int out = -1, int c_off = 0) {
+    const BufferSpec ib = buf(in);
+    const int ho = (ib.h + 2 * pad - 3) / stride + 1, wo = (ib.w + 2 * pad - 3) / stride + 1;
+    if (out < 0) out = buffer(ho, wo, ib.c);
+    const BufferSpec ob = buf(out);
+    if (ob.h != ho || ob.w != wo || c_off + ib.c > ob.c)
+      throw std::logic_error("pool output shape mismatch in " + m_.id);
+    OpSpec op;
+    op.kind = is_max ? OpKind::kMaxPool : OpKind::kAvgPool;
+    op.in = in;
+    op.out = out;
+    op.c_off = c_off;
+    op.r = op.s = 3;
+    op.sh = op.sw = stride;
+    op.ph = op.pw = pad;
+    op.relu = false;
+    m_.ops.push_back(op);
+    return out;
+  }
+
+  int gap(int in) {
+    const BufferSpec ib = buf(in);
+    const int out = buffer(1, 1, ib.c);
+    OpSpec op;
+    op.kind = OpKind::kGlobalAvgPool;
+    op.in = in;
+    op.out = out;
+    op.relu = false;
+    m_.ops.push_back(op);
+    return out;
+  }
+
+  int fc(int in, int classes) {
+    const BufferSpec ib = buf(in);
+    const int out = buffer(1, 1, classes, true);
+    ParamSpec p;
+    p.kind = OpKind::kFc;
+    p.cout = classes;
+    p.cin = p.cin_stored = ib.c;
+    p.fc = true;
+    m_.params.push_back(p);
+    OpSpec op;
+    op.kind = OpKind::kFc;
+    op.in = in;
+    op.out = out;
+    op.relu = false;
+    op.param = static_cast<int>(m_.params.size()) - 1;
+    m_.ops.push_back(op);
+    m_.macs_per_image += static_cast<double>(classes) * ib.c;
+    m_.logits = out;
+    m_.classes = classes;
+    return out;
+  }
+
+ private:
+  ModelSpec& m_;
+};
+
+ModelSpec synthetic_cnn() {
+  // Config 1: 3x32x32 -> conv3x3 32 -> conv3x3 s2 64 -> conv3x3 s2 128 -> GAP -> FC 10.
+  ModelSpec m;
+  m.id = "synthetic_cnn";
+  m.in_h = m.in_w = 32;
+  Builder b(m);
+  int x = b.buffer(32, 32, 4);
+  x = b.conv_sq(x, 32, 3, 1, 1);
+  x = b.conv_sq(x, 64, 3, 2, 1);
+  x = b.conv_sq(x, 128, 3, 2, 1);
+  b.fc(b.gap(x), 10);
+  return m;
+}
+
+ModelSpec mobilenet_v1() {
+  // Howard et al. 2017, width 1.0, 224x224 (Table 1): stem + 13 dw/pw pairs.
+  ModelSpec m;
+  m.id = "mobilenet_v1";
+  m.in_h = m.in_w = 224;
+  Builder b(m);
+  int x = b.buffer(224, 224, 4);
+  x = b.conv_sq(x, 32, 3, 2, 1);
+  const int cfg[13][2] = {{64, 1},  {128, 2}, {128, 1}, {256, 2}, {256, 1},
+                          {512, 2}, {512, 1}, {512, 1}, {512, 1}, {512, 1},
+                          {512, 1}, {1024, 2}, {1024, 1}};
+  for (const auto& c : cfg) {
+    x = b.dw(x, c[1]);
+    x = b.conv_sq(x, c[0], 1, 1, 0);
+  }
+  b.fc(b.gap(x), 1000);
+  return m;
+}
+
+ModelSpec resnet50_v1() {
+  // He et al. 2016, original v1: the stride of a down-sampling bottleneck
+  // sits on its first 1x1 conv (and on the projection shortcut).
+  ModelSpec m;
+  m.id = "resnet50_v1";
+  m.in_h = m.in_w = 224;
+  Builder b(m);
+  int x = b.buffer(224, 224, 4);
+  x = b.conv_sq(x, 64, 7, 2, 3);
+  x = b.pool(x, true, 2, 1);
+  const int blocks[4] = {3, 4, 6, 3};
+  const int width[4] = {64, 128, 256, 512};
+  for (int st = 0; st < 4; ++st) {
+    for (int i = 0; i < blocks[st]; ++i) {
+      const int stride = (i == 0 && st > 0) ? 2 : 1;
+      const int w = width[st];
+      const int in = x;
+      int y = b.conv(in, w, 1, 1, stride, stride, 0, 0);
+      y = b.conv_sq(y, w, 3, 1, 1);
+      int shortcut = in;
+      if (i == 0) shortcut = b.conv(in, 4 * w, 1, 1, stride, stride, 0, 0, -1, 0, -1, false);
+      x = b.conv(y, 4 * w, 1, 1, 1, 1, 0, 0, -1, 0, shortcut, true, 0.5f);
+    }
+  }
+  b.fc(b.gap(x), 1000);
+  return m;
+}
+
+// Inception-v3 (Szegedy et al. 2016), torchvision layout without the aux head.
+int inception_a(Builder& b, int x, int pool_features) {
+  const auto in = b.buf(x);
+  const int out = b.buffer(in.h, in.w, 64 + 64 + 96 + pool_features);
+  b.conv_sq(x, 64, 1, 1, 0, out, 0);
+  int t = b.conv_sq(x, 48, 1, 1, 0);
+  b.conv_sq(t, 64, 5, 1, 2, out, 64);
+  t = b.conv_sq(x, 64, 1, 1, 0);
+  t = b.conv_sq(t, 96, 3, 1, 1);
+  b.conv_sq(t, 96, 3, 1, 1, out, 128);
+  t = b.pool(x, false, 1, 1);
+  b.conv_sq(t, pool_features, 1, 1, 0, out, 224);
+  return out;
+}
+
+int inception_b(Builder& b, int x) {
+  const auto in = b.buf(x);
+  const int ho = (in.h - 3) / 2 + 1, wo = (in.w - 3) / 2 + 1;
+  const int out = b.buffer(ho, wo, 384 + 96 + in.c);
+  b.conv_sq(x, 384, 3, 2, 0, out, 0);
+  int t = b.conv_sq(x, 64, 1, 1, 0);
+  t = b.conv_sq(t, 96, 3, 1, 1);
+  b.conv_sq(t, 96, 3, 2, 0, out, 384);
+  b.pool(x, true, 2, 0, out, 480);
+  return out;
+}
+
+int inception_c(Builder& b, int x, int c7) {
+  const auto in = b.buf(x);
+  const int out = b.buffer(in.h, in.w, 768);
+  b.conv_sq(x, 192, 1, 1, 0, out, 0);
+  int t = b.conv_sq(x, c7, 1, 1, 0);
+  t = b.conv(t, c7, 1, 7, 1, 1, 0, 3);
+  b.conv(t, 192, 7, 1, 1, 1, 3, 0, out, 192);
+  t = b.conv_sq(x, c7, 1, 1, 0);
+  t = b.conv(t, c7, 7, 1, 1, 1, 3, 0);
+  t = b.conv(t, c7, 1, 7, 1, 1, 0, 3);
+  t = b.conv(t, c7, 7, 1, 1, 1, 3, 0);
+  b.conv(t, 192, 1, 7, 1, 1, 0, 3, out, 384);
+  t = b.pool(x, false, 1, 1);
+  b.conv_sq(t, 192, 1, 1, 0, out, 576);
+  return out;
+}
+
+int inception_d(Builder& b, int x) {
+  const auto in = b.buf(x);
+  const int ho = (in.h - 3) / 2 + 1, wo = (in.w - 3) / 2 + 1;
+  const int out = b.buffer(ho, wo, 320 + 192 + in.c);
+  int t = b.conv_sq(x, 192, 1, 1, 0);
+  b.conv_sq(t, 320, 3, 2, 0, out, 0);
+  t = b.conv_sq(x, 192, 1, 1, 0);
+  t = b.conv(t, 192, 1, 7, 1, 1, 0, 3);
+  t = b.conv(t, 192, 7, 1, 1, 1, 3, 0);
+  b.conv_sq(t, 192, 3, 2, 0, out, 320);
+  b.pool(x, true, 2, 0, out, 512);
+  return out;
+}
+
+int inception_e(Builder& b, int x) {
+  const auto in = b.buf(x);
+  const int out = b.buffer(in.h, in.w, 2048);
+  b.conv_sq(x, 320, 1, 1, 0, out, 0);
+  int t = b.conv_sq(x, 384, 1, 1, 0);
+  b.conv(t, 384, 1, 3, 1, 1, 0, 1, out, 320);
+  b.conv(t, 384, 3, 1, 1, 1, 1, 0, out, 704);
+  t = b.conv_sq(x, 448, 1, 1, 0);
+  t = b.conv_sq(t, 384, 3, 1, 1);
+  b.conv(t, 384, 1, 3, 1, 1, 0, 1, out, 1088);
+  b.conv(t, 384, 3, 1, 1, 1, 1, 0, out, 1472);
+  t = b.pool(x, false, 1, 1);
+  b.conv_sq(t, 192, 1, 1, 0, out, 1856);
+  return out;
+}
+
+ModelSpec inception_v3() {
+  ModelSpec m;
+  m.id = "inception_v3";
+  m.in_h = m.in_w = 299;
+  Builder b(m);
+  int x = b.buffer(299, 299, 4);
+  x = b.conv_sq(x, 32, 3, 2, 0);
+  x = b.conv_sq(x, 32, 3, 1, 0);
+  x = b.conv_sq(x, 64, 3, 1, 1);
+  x = b.pool(x, true, 2, 0);
+  x = b.conv_sq(x, 80, 1, 1, 0);
+  x = b.conv_sq(x, 192, 3, 1, 0);
+  x = b.pool(x, true, 2, 0);
+  x = inception_a(b, x, 32);
+  x = inception_a(b, x, 64);
+  x = inception_a(b, x, 64);
+  x = inception_b(b, x);
+  x = inception_c(b, x, 128);
+  x = inception_c(b, x, 160);
+  x = inception_c(b, x, 160);
+  x = inception_c(b, x, 192);
+  x = inception_d(b, x);
+  x = inception_e(b, x);
+  x = inception_e(b, x);
+  b.fc(b.gap(x), 1000);
+  return m;
+}
+
+}  // namespace
+
+std::vector<std::string> model_ids() {
+  return {"synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"};
+}
+
+ModelSpec build_model(const std::string& id) {
+  if (id == "synthetic_cnn") return synthetic_cnn();
+  if (id == "mobilenet_v1") return mobilenet_v1();
+  if (id == "resnet50_v1") return resnet50_v1();
+  if (id == "inception_v3") return inception_v3();
+  throw std::invalid_argument("unknown model: " + id);
+}
+
+}  // namespace ds

@@ -1,0 +1,58 @@
+// Network IR for the served models. The reference has no model code at all
+// (its "forward pass" is the analytic latency of perf_model.cpp:70-86); these
+// are the canonical architectures named by BASELINE.json's configs, laid out
+// for the B200 kernels: NHWC bf16 activations, KRSC bf16 weights with folded
+// batch-norm (bias only), fp32 logits.
+#pragma once
+
+#include <string>
+#include <vector>
+
+namespace ds {
+
+enum class OpKind { kConv, kDwConv, kMaxPool, kAvgPool, kGlobalAvgPool, kFc };
+
+// Per-image activation buffer shape (NHWC). Buffer 0 is always the staged
+// input (C = 4: RGB + one zero channel).
+struct BufferSpec {
+  int h = 1, w = 1, c = 1;
+  bool f32 = false;
+};
+
+// A parameterised layer, in canonical generation order.
+struct ParamSpec {
+  OpKind kind = OpKind::kConv;
+  int cout = 0, r = 1, s = 1;
+  int cin = 0;         // real input channels (3 for stems)
+  int cin_stored = 0;  // channels in the device layout (4 for stems)
+  float gain = 1.0f;   // multiplies the He std (residual-branch ends use 0.5)
+  bool fc = false;     // FC: std sqrt(1/fan_in), zero bias
+};
+
+struct OpSpec {
+  OpKind kind = OpKind::kConv;
+  int in = 0;
+  int out = 0;
+  int c_off = 0;      // channel offset inside `out` (concat slices)
+  int residual = -1;  // buffer added in the epilogue before ReLU
+  int r = 1, s = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+  bool relu = true;
+  int param = -1;
+};
+
+struct ModelSpec {
+  std::string id;
+  int in_h = 0, in_w = 0;
+  int classes = 0;
+  std::vector<BufferSpec> buffers;
+  std::vector<ParamSpec> params;
+  std::vector<OpSpec> ops;
+  int logits = -1;  // fp32 [classes] buffer
+  double macs_per_image = 0.0;  // algorithmic multiply-accumulates (real channels)
+};
+
+// "synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3".
+ModelSpec build_model(const std::string& id);
+std::vector<std::string> model_ids();
+
+}  // namespace ds

@@ -78,6 +78,7 @@ static int run(const Case& cs) {
   a.bias = db; a.residual = cs.residual ? dr : nullptr; a.ld_res = cs.Cout;
   a.y = dy; a.ldy = ldy; a.c_off = cs.c_off; a.out_f32 = cs.f32; a.relu = cs.relu;
   // channels [c_off, c_off+Cout) of an ldy-wide buffer; keep Cout+c_off <= ldy
+  conv_gemm_init();
   cudaError_t e = launch_conv_gemm(a, cs.mode, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
