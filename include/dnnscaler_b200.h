@@ -124,6 +124,161 @@ ds_status ds_generate_images(int h, int w, uint64_t seed, int64_t first, int cou
 ds_status ds_model_param(const char* model_id, int layer, uint16_t* w, size_t w_cap,
                          size_t* w_len, float* b, size_t b_cap, size_t* b_len, int* kpad);
 
+/* ======================================================================
+ * Control plane (the reference's Profiler / Scaler / harness over a seam).
+ * Replaces reference harness.hpp:54-80 (run_job / run_scenario),
+ * profiler.hpp:34-38, scaler.hpp:13-70, matrix_completion.hpp:39-49.
+ * ====================================================================== */
+
+typedef struct {
+  int kind; /* 0 batching, 1 multi-tenancy (reference KnobKind) */
+  int value;
+} ds_knob;
+
+typedef struct {
+  double at_s;
+  double slo_ms;
+} ds_slo_step;
+
+/* == JobSpec (reference domain.hpp:41-48). */
+typedef struct {
+  int job_id;
+  const char* dnn_id; /* catalog id; for the device seam also the model id */
+  double slo_ms;
+  double duration_s;
+  int n_slo_steps;
+  const ds_slo_step* slo_steps;
+} ds_job_spec;
+
+/* == DnnProfile (reference domain.hpp:26-34): (x, items/s) points. */
+typedef struct {
+  const char* id;
+  int n_batching;
+  const int* batching_x;
+  const double* batching_tput;
+  int n_mt;
+  const int* mt_x;
+  const double* mt_tput;
+  int has_sigma;
+  double sigma;
+  int has_u1;
+  double u1;
+} ds_dnn_profile;
+
+/* == Scenario (reference scenario.hpp:17-30), catalog passed separately. */
+typedef struct {
+  int controller; /* 0 dnnscaler, 1 clipper, 2 static */
+  ds_knob static_knob;
+  uint64_t seed;
+  double alpha;
+  int m, n, abs_max_bs, max_mtl, window;
+  double sigma;
+} ds_scenario;
+
+typedef enum {
+  DS_SEAM_ANALYTIC = 0, /* the reference's simulated GpuSim (perf model) */
+  DS_SEAM_DEVICE = 1,   /* the B200 backend */
+  DS_SEAM_REPLAY = 2    /* a recorded tape */
+} ds_seam_kind;
+
+typedef struct {
+  int kind;
+  ds_backend* backend; /* DEVICE: existing handle to serve on, or NULL to create one
+                          per job (model = dnn_id, seed = mix_seed(seed, job_id)) */
+  int device;          /* DEVICE with backend == NULL: CUDA ordinal */
+  int host_io;         /* DEVICE with backend == NULL: end-to-end copies */
+  const double* tape;  /* REPLAY */
+  size_t tape_len;
+} ds_seam_spec;
+
+typedef struct {
+  double time_s;
+  int job_id;
+  ds_knob knob;
+  double p95_ms, mean_ms, throughput, power_w, slo_ms;
+  int violated;
+} ds_metrics_record;
+
+/* == ProfileReport (reference profiler.hpp:11-29). */
+typedef struct {
+  double tput_base, tput_batching, tput_mt, ti_batching, ti_mt;
+  double base_latency_ms, probe_latency_batching_ms, probe_latency_mt_ms;
+  int m, n, batches_per_point;
+  double base_elapsed_ms, batching_elapsed_ms, mt_elapsed_ms, transition_ms;
+  double profiling_cost_ms, items_served;
+} ds_profile_report;
+
+/* == JobSummary (reference harness.hpp:19-43) minus strings. */
+typedef struct {
+  int job_id;
+  int approach_kind; /* knob kind actually controlled */
+  int profiled;
+  double ti_batching, ti_mt, profiling_cost_ms;
+  ds_knob steady_knob;
+  int converged, knob_changes, settle_period, periods;
+  double duration_s, total_items, avg_throughput, steady_throughput, p95_overall_ms;
+  double slo_compliance, avg_power_w, power_efficiency, final_slo_ms;
+  int n_readaptations;
+  int failed; /* run_scenario semantics: error captured, see ds_job_result_error */
+} ds_job_summary;
+
+typedef struct ds_job_result ds_job_result;
+
+/* run_job (reference harness.cpp:329-333) on the given seam. A job that
+ * throws yields a result with failed = 1 and its message (run_scenario
+ * semantics, harness.cpp:341-351); the call itself returns DS_OK. */
+ds_status ds_job_run(const ds_scenario* scenario, const ds_job_spec* job,
+                     const ds_dnn_profile* catalog, int n_catalog, const ds_seam_spec* seam,
+                     ds_job_result** out);
+
+/* Incremental form: start (profile + seed the knob), then one control period
+ * per ds_job_step, then ds_job_finish for the summary. */
+typedef struct ds_job_session ds_job_session;
+ds_status ds_job_start(const ds_scenario* scenario, const ds_job_spec* job,
+                       const ds_dnn_profile* catalog, int n_catalog, const ds_seam_spec* seam,
+                       ds_job_session** out);
+ds_status ds_job_step(ds_job_session* s, ds_metrics_record* record, int* done);
+ds_status ds_job_knob(const ds_job_session* s, ds_knob* knob);
+ds_status ds_job_finish(ds_job_session* s, ds_job_result** out);
+void ds_job_session_free(ds_job_session* s);
+
+size_t ds_job_result_records(const ds_job_result* r, ds_metrics_record* out, size_t cap);
+ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* out);
+ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* out);
+size_t ds_job_result_tape(const ds_job_result* r, double* out, size_t cap);
+size_t ds_job_result_latencies(const ds_job_result* r, double* out, size_t cap);
+size_t ds_job_result_readaptations(const ds_job_result* r, double* at_s, int* periods, size_t cap);
+const char* ds_job_result_error(const ds_job_result* r);
+void ds_job_result_free(ds_job_result* r);
+
+/* Single controller steps, for unit parity with the reference goldens. */
+ds_status ds_percentile(const double* samples, size_t n, double q, double* out);
+ds_status ds_band_verdict(double p95_ms, double slo_ms, double alpha, int* verdict /*0 below,1 in,2 above*/);
+
+typedef struct {
+  int min_bs, max_bs, current_bs, abs_max_bs, infeasible;
+} ds_batch_scaler;
+ds_status ds_batch_step(ds_batch_scaler* st, double p95_ms, double slo_ms, double alpha,
+                        int* changed);
+
+typedef struct {
+  int mtl, max_mtl, last_action /*0 hold,1 add,2 remove*/, damped;
+} ds_mt_scaler;
+ds_status ds_mt_step(ds_mt_scaler* st, double p95_ms, double slo_ms, double alpha, int* action,
+                     int* infeasible);
+
+ds_status ds_mt_init(double lat1_ms, double latn_ms, int n_probe, const double* rows,
+                     int n_rows, int row_len, double slo_ms, int max_mtl, uint64_t seed,
+                     int* out);
+ds_status ds_estimate_row(const double* rows, int n_rows, int row_len, const int* levels,
+                          const double* values, int n_obs, int width, uint64_t seed,
+                          double* out);
+ds_status ds_decide(const ds_profile_report* r, double eps, int* approach /*0 B, 1 MT*/);
+ds_status ds_calibrate_batching(const int* x, const double* tput, int n, double* a_ms,
+                                double* b_ms);
+ds_status ds_calibrate_mt(const int* x, const double* tput, int n, double* l1_ms,
+                          double* capacity);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,15 +6,17 @@
 #include <stdexcept>
 #include <string>
 
-#include "engine.hpp"
-
-struct ds_backend {
-  ds::Backend* impl;
-};
+#include "abi_internal.hpp"
 
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+void ds_internal_set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
 
 template <typename F>
 ds_status guard(F&& f) {
