@@ -92,6 +92,11 @@ ds_status ds_set_host_io(ds_backend* b, int enabled);
 /* Waits for all in-flight requests (the device is idle on return). */
 ds_status ds_drain(ds_backend* b);
 
+/* Device timer around a region of serving calls (drain + cudaEvent at both
+ * ends, so every request issued in between on any instance is inside). */
+ds_status ds_timer_start(ds_backend* b);
+ds_status ds_timer_stop(ds_backend* b, double* elapsed_ms);
+
 typedef struct {
   int in_h, in_w, classes;
   int n_ops, n_params;
@@ -112,6 +117,24 @@ typedef struct {
 } ds_backend_stats;
 
 ds_status ds_backend_stats_get(const ds_backend* b, ds_backend_stats* out);
+
+/* Algorithmic cost of each kernel of one forward, launch order: input
+ * staging, one per layer, softmax. kind: 0 staging, 1 conv/FC implicit GEMM,
+ * 2 depthwise, 3 pool, 4 global-avg-pool, 5 softmax. A launch at batch B
+ * moves B*bytes_per_image + fixed_bytes and computes B*flops_per_image. */
+typedef struct {
+  int kind;
+  double flops_per_image;
+  double bytes_per_image;
+  double fixed_bytes;
+} ds_kernel_cost;
+
+ds_status ds_model_kernels(const char* model_id, ds_kernel_cost* out, int cap, int* n);
+
+/* Device time (ms) of every kernel of one bs-forward, from cudaEvent nodes
+ * captured between the kernels of a graph on the batching instance's
+ * stream, averaged over reps launches. ms_out has ds_model_kernels() slots. */
+ds_status ds_profile_kernels(ds_backend* b, int bs, int reps, double* ms_out, int cap);
 
 /* The synthetic inputs: image i = RandomStream(mix_seed(seed, 1000000 + i)),
  * one byte per (h, w, c) draw (next_u64() >> 56). */

@@ -51,6 +51,11 @@ class DsBackendStats(ctypes.Structure):
     ]
 
 
+class DsKernelCost(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("flops_per_image", ctypes.c_double),
+                ("bytes_per_image", ctypes.c_double), ("fixed_bytes", ctypes.c_double)]
+
+
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 _vp = ctypes.c_void_p
 
@@ -74,8 +79,15 @@ SIGNATURES = {
     "ds_forward": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
     "ds_set_host_io": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ds_drain": (ctypes.c_int, [_vp]),
+    "ds_timer_start": (ctypes.c_int, [_vp]),
+    "ds_timer_stop": (ctypes.c_int, [_vp, _c_double_p]),
     "ds_model_info_get": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(DsModelInfo)]),
     "ds_backend_stats_get": (ctypes.c_int, [_vp, ctypes.POINTER(DsBackendStats)]),
+    "ds_model_kernels": (
+        ctypes.c_int,
+        [ctypes.c_char_p, ctypes.POINTER(DsKernelCost), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+    ),
+    "ds_profile_kernels": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int]),
     "ds_generate_images": (
         ctypes.c_int,
         [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, _vp],

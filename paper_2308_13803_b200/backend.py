@@ -44,6 +44,20 @@ def model_info(model_id: str) -> ModelInfo:
                      mi.weight_count, mi.act_bytes_per_image)
 
 
+KERNEL_KINDS = ("stage", "conv_gemm", "dwconv", "pool", "gap", "softmax")
+
+
+def kernel_costs(model_id: str) -> list:
+    """Per-kernel algorithmic cost of one forward (launch order)."""
+    lib = _lib.load()
+    n = ctypes.c_int()
+    _lib.check(lib.ds_model_kernels(model_id.encode(), None, 0, ctypes.byref(n)))
+    arr = (_lib.DsKernelCost * n.value)()
+    _lib.check(lib.ds_model_kernels(model_id.encode(), arr, n.value, ctypes.byref(n)))
+    return [dict(kind=KERNEL_KINDS[c.kind], flops_per_image=c.flops_per_image,
+                 bytes_per_image=c.bytes_per_image, fixed_bytes=c.fixed_bytes) for c in arr]
+
+
 def generate_images(model_id: str, first: int, count: int, seed: int = 42) -> np.ndarray:
     """The synthetic inputs of DESIGN.md: u8 NHWC [count, h, w, 3]."""
     info = model_info(model_id)
@@ -123,6 +137,21 @@ class GpuBackend:
 
     def drain(self) -> None:
         _lib.check(self._lib.ds_drain(self._h))
+
+    def timer_start(self) -> None:
+        _lib.check(self._lib.ds_timer_start(self._h))
+
+    def timer_stop(self) -> float:
+        ms = ctypes.c_double()
+        _lib.check(self._lib.ds_timer_stop(self._h, ctypes.byref(ms)))
+        return ms.value
+
+    def profile_kernels(self, bs: int, reps: int = 10) -> np.ndarray:
+        """Device ms of every kernel of one bs-forward (event nodes in a graph)."""
+        n = len(kernel_costs(self.model_id))
+        out = np.empty(n, dtype=np.float64)
+        _lib.check(self._lib.ds_profile_kernels(self._h, bs, reps, out.ctypes.data, n))
+        return out
 
     def stats(self) -> dict:
         s = _lib.DsBackendStats()

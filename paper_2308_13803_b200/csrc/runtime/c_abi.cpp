@@ -148,6 +148,16 @@ ds_status ds_drain(ds_backend* b) {
   return guard([&] { b->impl->drain(); });
 }
 
+ds_status ds_timer_start(ds_backend* b) {
+  if (!b) return null_handle();
+  return guard([&] { b->impl->timer_start(); });
+}
+
+ds_status ds_timer_stop(ds_backend* b, double* elapsed_ms) {
+  if (!b || !elapsed_ms) return null_handle();
+  return guard([&] { *elapsed_ms = b->impl->timer_stop(); });
+}
+
 ds_status ds_model_info_get(const char* model_id, ds_model_info* out) {
   if (!model_id || !out) return null_handle();
   return guard([&] {
@@ -183,6 +193,26 @@ ds_status ds_backend_stats_get(const ds_backend* b, ds_backend_stats* out) {
     const ds::ModelSpec& m = b->impl->model();
     out->kernels_per_forward = static_cast<int>(m.ops.size()) + 2;
     out->device_bytes = static_cast<double>(b->impl->device_bytes());
+  });
+}
+
+ds_status ds_model_kernels(const char* model_id, ds_kernel_cost* out, int cap, int* n) {
+  if (!model_id || !n) return null_handle();
+  return guard([&] {
+    const auto costs = ds::kernel_costs(ds::build_model(model_id));
+    *n = static_cast<int>(costs.size());
+    for (int i = 0; out && i < cap && i < *n; ++i)
+      out[i] = ds_kernel_cost{static_cast<int>(costs[i].kind), costs[i].flops_per_image,
+                              costs[i].bytes_per_image, costs[i].fixed_bytes};
+  });
+}
+
+ds_status ds_profile_kernels(ds_backend* b, int bs, int reps, double* ms_out, int cap) {
+  if (!b || !ms_out) return null_handle();
+  return guard([&] {
+    const auto ms = b->impl->profile_kernels(bs, reps < 1 ? 1 : reps);
+    if (static_cast<int>(ms.size()) > cap) throw std::invalid_argument("output too small");
+    for (size_t i = 0; i < ms.size(); ++i) ms_out[i] = ms[i];
   });
 }
 

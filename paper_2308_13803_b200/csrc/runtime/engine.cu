@@ -156,12 +156,20 @@ Instance::~Instance() {
   if (stream_) cudaStreamDestroy(stream_);
 }
 
-void Instance::enqueue_layers(int bs) {
+void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks) {
   const ModelSpec& m = m_;
   const HostParams& hp = params_for(m);
+  size_t mark = 0;
+  auto record_mark = [&] {
+    if (marks)
+      check_cuda(cudaEventRecordWithFlags((*marks)[mark++], stream_, cudaEventRecordExternal),
+                 "mark");
+  };
+  record_mark();
   check_cuda(launch_stage_input(d_images_, static_cast<__nv_bfloat16*>(bufs_[0]), bs, m.in_h,
                                 m.in_w, stream_),
              "stage_input");
+  record_mark();
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
     const BufferSpec& in = m.buffers[op.in];
@@ -193,8 +201,51 @@ void Instance::enqueue_layers(int bs) {
         break;
     }
     check_cuda(e, "layer launch");
+    record_mark();
   }
   check_cuda(launch_softmax(d_logits_, d_probs_, bs, m.classes, stream_), "softmax");
+  record_mark();
+}
+
+std::vector<double> Instance::profile_kernels(int bs, int reps) {
+  if (bs < 1 || bs > max_bs_) throw std::invalid_argument("invalid batch size");
+  const int nk = kernels_per_forward_;
+  std::vector<cudaEvent_t> marks(nk + 1);
+  for (auto& e : marks) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<double> acc(nk, 0.0);
+  try {
+    check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+      enqueue_layers(bs, &marks);
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &g);
+      throw;
+    }
+    check_cuda(cudaStreamEndCapture(stream_, &g), "capture end");
+    check_cuda(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+    for (int r = 0; r < reps + 1; ++r) {  // first launch is a warm-up
+      check_cuda(cudaGraphLaunch(exec, stream_), "launch");
+      check_cuda(cudaStreamSynchronize(stream_), "profile");
+      if (r == 0) continue;
+      for (int k = 0; k < nk; ++k) {
+        float ms = 0.0f;
+        check_cuda(cudaEventElapsedTime(&ms, marks[k], marks[k + 1]), "elapsed");
+        acc[k] += ms;
+      }
+    }
+  } catch (...) {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (g) cudaGraphDestroy(g);
+    for (auto& e : marks) cudaEventDestroy(e);
+    throw;
+  }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(g);
+  for (auto& e : marks) cudaEventDestroy(e);
+  for (auto& v : acc) v /= reps;
+  return acc;
 }
 
 void Instance::enqueue_forward(int bs) {
@@ -246,6 +297,8 @@ Backend::~Backend() {
   }
   inst_.clear();
   for (cudaEvent_t e : all_events_) cudaEventDestroy(e);
+  for (cudaEvent_t e : timer_)
+    if (e) cudaEventDestroy(e);
   if (pinned_images_) cudaFreeHost(pinned_images_);
   for (float* p : pinned_logits_)
     if (p) cudaFreeHost(p);
@@ -427,6 +480,24 @@ void Backend::forward(const uint8_t* host_images, int bs, float* host_logits, fl
                              cudaMemcpyHostToDevice, s),
              "restore images");
   check_cuda(cudaStreamSynchronize(s), "forward");
+}
+
+void Backend::timer_start() {
+  drain();
+  for (auto& e : timer_)
+    if (!e) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+  check_cuda(cudaDeviceSynchronize(), "timer sync");
+  check_cuda(cudaEventRecord(timer_[0], inst_[0]->stream()), "timer start");
+}
+
+double Backend::timer_stop() {
+  drain();
+  check_cuda(cudaDeviceSynchronize(), "timer sync");
+  check_cuda(cudaEventRecord(timer_[1], inst_[0]->stream()), "timer stop");
+  check_cuda(cudaEventSynchronize(timer_[1]), "timer stop");
+  float ms = 0.0f;
+  check_cuda(cudaEventElapsedTime(&ms, timer_[0], timer_[1]), "timer elapsed");
+  return static_cast<double>(ms);
 }
 
 void Backend::set_host_io(bool enabled) {

@@ -43,8 +43,13 @@ class Instance {
 
   // Enqueues one forward over the first bs images of images() (graph per bs).
   void enqueue_forward(int bs);
-  // Same sequence without a graph (used for capture and first launch).
-  void enqueue_layers(int bs);
+  // Same sequence without a graph (used for capture and first launch). When
+  // `marks` is given (kernels_per_forward()+1 events), an externally visible
+  // event is recorded before the first and after every kernel.
+  void enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks = nullptr);
+  // Device time of every kernel of one forward (staging, ops..., softmax),
+  // averaged over `reps` launches of a graph with event nodes between kernels.
+  std::vector<double> profile_kernels(int bs, int reps);
 
   cudaStream_t stream() const { return stream_; }
   uint8_t* images() const { return d_images_; }
@@ -110,6 +115,16 @@ class Backend {
   bool host_io() const { return host_io_; }
   // Drains every in-flight request (device idle on return).
   void drain();
+  // Device timer over a region of serving calls: both ends drain all
+  // in-flight work and record a cudaEvent, so the elapsed time covers every
+  // request issued in between on every instance stream.
+  void timer_start();
+  double timer_stop();
+  // Per-kernel device time of one bs-forward on the batching instance.
+  std::vector<double> profile_kernels(int bs, int reps) {
+    drain();
+    return instance(0).profile_kernels(bs, reps);
+  }
 
   const ModelSpec& model() const { return model_; }
   int64_t kernel_launches() const { return kernel_launches_; }
@@ -150,6 +165,7 @@ class Backend {
   double clock_ms_ = 0.0;
   int64_t kernel_launches_ = 0;
   int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  cudaEvent_t timer_[2] = {nullptr, nullptr};
   static constexpr int kDepth = 2;  // requests kept in flight per stream
 };
 

@@ -311,6 +311,51 @@ ModelSpec inception_v3() {
 
 }  // namespace
 
+std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
+  std::vector<KernelCost> out;
+  const double px = static_cast<double>(m.in_h) * m.in_w;
+  out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
+  for (const auto& op : m.ops) {
+    const BufferSpec& in = m.buffers[op.in];
+    const BufferSpec& out_b = m.buffers[op.out];
+    const double in_elems = static_cast<double>(in.h) * in.w * in.c;
+    const double hw_out = static_cast<double>(out_b.h) * out_b.w;
+    KernelCost k{KernelKind::kPool, 0.0, 0.0, 0.0};
+    switch (op.kind) {
+      case OpKind::kConv:
+      case OpKind::kFc: {
+        const ParamSpec& p = m.params[op.param];
+        const double out_elems = hw_out * p.cout;
+        k.kind = KernelKind::kConvGemm;
+        k.flops_per_image = 2.0 * out_elems * p.r * p.s * p.cin;
+        k.bytes_per_image = in_elems * 2 + out_elems * (out_b.f32 ? 4 : 2) +
+                            (op.residual >= 0 ? out_elems * 2 : 0.0);
+        k.fixed_bytes = static_cast<double>(p.cout) * p.r * p.s * p.cin * 2 + p.cout * 4.0;
+        break;
+      }
+      case OpKind::kDwConv: {
+        k.kind = KernelKind::kDwConv;
+        k.flops_per_image = 2.0 * hw_out * in.c * 9;
+        k.bytes_per_image = in_elems * 2 + hw_out * in.c * 2;
+        k.fixed_bytes = in.c * 9.0 * 2 + in.c * 4.0;
+        break;
+      }
+      case OpKind::kMaxPool:
+      case OpKind::kAvgPool:
+        k.kind = KernelKind::kPool;
+        k.bytes_per_image = in_elems * 2 + hw_out * in.c * 2;
+        break;
+      case OpKind::kGlobalAvgPool:
+        k.kind = KernelKind::kGap;
+        k.bytes_per_image = in_elems * 2 + in.c * 2.0;
+        break;
+    }
+    out.push_back(k);
+  }
+  out.push_back({KernelKind::kSoftmax, 0.0, m.classes * 8.0, 0.0});
+  return out;
+}
+
 std::vector<std::string> model_ids() {
   return {"synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"};
 }

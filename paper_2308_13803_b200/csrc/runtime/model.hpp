@@ -53,6 +53,19 @@ struct ModelSpec {
 
 // "synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3".
 ModelSpec build_model(const std::string& id);
+
+// Algorithmic cost of every kernel of one forward, in launch order:
+// input staging, one entry per op, softmax. Bytes are the minimum DRAM
+// traffic (each input, output, residual and weight tensor moved once, bf16
+// activations, fp32 logits); FLOPs are 2 x real multiply-accumulates.
+enum class KernelKind { kStage = 0, kConvGemm = 1, kDwConv = 2, kPool = 3, kGap = 4, kSoftmax = 5 };
+struct KernelCost {
+  KernelKind kind;
+  double flops_per_image = 0.0;
+  double bytes_per_image = 0.0;
+  double fixed_bytes = 0.0;  // weights + bias, once per launch
+};
+std::vector<KernelCost> kernel_costs(const ModelSpec& m);
 std::vector<std::string> model_ids();
 
 }  // namespace ds
