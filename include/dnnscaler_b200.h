@@ -92,6 +92,11 @@ ds_status ds_set_host_io(ds_backend* b, int enabled);
 /* Waits for all in-flight requests (the device is idle on return). */
 ds_status ds_drain(ds_backend* b);
 
+/* NVTX range markers (header-only NVTX v3; no-ops without a tool attached),
+ * used to scope ncu captures to a bench's timed region. */
+void ds_nvtx_push(const char* name);
+void ds_nvtx_pop(void);
+
 /* Device timer around a region of serving calls (drain + cudaEvent at both
  * ends, so every request issued in between on any instance is inside). */
 ds_status ds_timer_start(ds_backend* b);
@@ -135,6 +140,12 @@ ds_status ds_model_kernels(const char* model_id, ds_kernel_cost* out, int cap, i
  * captured between the kernels of a graph on the batching instance's
  * stream, averaged over reps launches. ms_out has ds_model_kernels() slots. */
 ds_status ds_profile_kernels(ds_backend* b, int bs, int reps, double* ms_out, int cap);
+
+/* Debug/parity aid: activation buffer `buffer` of the last forward on the
+ * batching instance (first bs images; NHWC bf16 bits, or fp32 for logits).
+ * Buffer ids follow the model IR (0 = staged input); out_len in bytes. */
+ds_status ds_debug_read_buffer(ds_backend* b, int buffer, int bs, void* out, size_t cap,
+                               size_t* out_len);
 
 /* The synthetic inputs: image i = RandomStream(mix_seed(seed, 1000000 + i)),
  * one byte per (h, w, c) draw (next_u64() >> 56). */

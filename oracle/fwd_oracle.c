@@ -568,6 +568,8 @@ static void run_pool(const net* n, const op* o, float** B, int st) {
 
 static float* g_feat_out = NULL; /* debug: pooled features of a single-image call */
 void oracle_debug_features(float* out) { g_feat_out = out; }
+static int g_dbg_buf = -1;       /* debug: capture this activation buffer ... */
+static float* g_dbg_out = NULL;  /* ... into this array (single-image calls only) */
 
 static void forward_one(const net* n, const uint8_t* img, int st, float* logits) {
   float* B[160];
@@ -612,10 +614,31 @@ static void forward_one(const net* n, const uint8_t* img, int st, float* logits)
   }
   memcpy(logits, B[n->logits], sizeof(float) * n->classes);
   if (g_feat_out) memcpy(g_feat_out, B[n->ops[n->nops - 1].in], sizeof(float) * n->ops[n->nops - 1].cin);
+  if (g_dbg_out && g_dbg_buf >= 0 && g_dbg_buf < n->nb)
+    memcpy(g_dbg_out, B[g_dbg_buf],
+           sizeof(float) * n->buf[g_dbg_buf].h * n->buf[g_dbg_buf].w * n->buf[g_dbg_buf].c);
   for (int b = 0; b < n->nb; ++b) free(B[b]);
 }
 
 /* ----------------------------------------------------------- C API */
+/* Debug: one image through the net, activation buffer `buf` (NHWC fp32) out;
+ * returns its element count, or -1. Buffer ids follow emission order. */
+long oracle_debug_buffer(const char* id, const uint8_t* img, int bf16_storage, int buf,
+                         float* out) {
+  net* n = get_net(id);
+  if (!n || buf < 0 || buf >= n->nb) return -1;
+  long count = (long)n->buf[buf].h * n->buf[buf].w * n->buf[buf].c;
+  if (out) {
+    float* logits = (float*)malloc(sizeof(float) * n->classes);
+    g_dbg_buf = buf;
+    g_dbg_out = out;
+    forward_one(n, img, bf16_storage, logits);
+    g_dbg_out = NULL;
+    g_dbg_buf = -1;
+    free(logits);
+  }
+  return count;
+}
 int oracle_model_info(const char* id, int* in_h, int* in_w, int* classes, int* n_params,
                       double* macs) {
   net* n = get_net(id);

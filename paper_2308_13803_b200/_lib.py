@@ -79,6 +79,8 @@ SIGNATURES = {
     "ds_forward": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
     "ds_set_host_io": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ds_drain": (ctypes.c_int, [_vp]),
+    "ds_nvtx_push": (None, [ctypes.c_char_p]),
+    "ds_nvtx_pop": (None, []),
     "ds_timer_start": (ctypes.c_int, [_vp]),
     "ds_timer_stop": (ctypes.c_int, [_vp, _c_double_p]),
     "ds_model_info_get": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(DsModelInfo)]),

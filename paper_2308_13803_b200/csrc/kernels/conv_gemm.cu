@@ -5,23 +5,30 @@
 // behind GpuSim::run_batch / run_mt_request (reference gpu_sim.cpp:13-24):
 // every dense conv, 1x1 conv and FC layer of the served networks runs here.
 //
-// CTA = 6 warps, one 128 x BN output tile:
-//   warps 0-3  A producers: gather the im2col rows of the tile straight from
+// Persistent CTA (one per SM) walking 128 x BN output tiles, N-tile fastest
+// so the CTAs sharing an A row-block run together and A is read from DRAM
+// once. Eighteen warps, three pipelines (operand ring, two TMEM
+// accumulators, tile loop):
+//   warps 0-7  epilogue (two per TMEM lane quarter, alternating 128 B column
+//              groups): TMEM -> registers (tcgen05.ld), + bias (+ residual),
+//              ReLU, packed into 128 B-swizzled smem rows and written by TMA
+//              bulk tensor stores into the (possibly channel-sliced) NHWC
+//              output; releases the accumulator buffer to the MMA warp, so
+//              tile i's epilogue overlaps tile i+1's main loop.
+//   warps 8-15 A producers: gather the im2col rows of each tile straight from
 //              the NHWC input with zero-filling cp.async (padding, K tail and
 //              M tail become zeros), written in the 128 B-swizzled K-major
-//              layout the UMMA descriptor expects; completion is signalled to
-//              the stage's full barrier by cp.async.mbarrier.arrive.
-//              For 1x1 stride-1 layers the A tile is a plain 2D box and the
-//              TMA warp loads it instead (kTmaA).
-//              After the main loop the same 4 warps are the epilogue: TMEM ->
-//              registers (tcgen05.ld), + bias (+ residual), ReLU, bf16/fp32
-//              stores into the (possibly channel-sliced) NHWC output.
-//   warp 4     TMA producer for the weight tile (and A in kTmaA); owns TMEM.
-//   warp 5     one elected thread issues tcgen05.mma (M=128, N=BN, K=16) into
-//              an fp32 TMEM accumulator and commits stage releases.
+//              layout the UMMA descriptor expects; completion reaches the
+//              stage's full barrier via cp.async.mbarrier.arrive.noinc.
+//              For 1x1 stride-1 layers the A tile is a plain 2D box loaded by
+//              the TMA warp instead (kTmaA) and these warps idle.
+//   warp 16    TMA producer for the weight tile (and A in kTmaA); owns TMEM.
+//   warp 17    one thread issues tcgen05.mma (M=128, N=BN, K=16) into the
+//              current fp32 TMEM accumulator and commits stage releases.
 #include "conv_gemm.cuh"
 #include "sm100_ptx.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 
@@ -31,73 +38,101 @@ namespace {
 
 constexpr int kABytes = kConvBM * kConvBK * 2;  // 16 KiB per stage
 
+// Output staging for the TMA-store epilogue: per epilogue warp two buffers
+// of 32 rows x 128 B (64 bf16 or 32 fp32 columns, 128 B-swizzled).
+constexpr int kYStageBytes = 32 * 128;
+
+// Warp roles (kConvThreads = 18 warps).
+constexpr int kEpiWarps = 8;      // warps 0-7: epilogue, two per TMEM lane quarter
+constexpr int kGatherWarp0 = 8;   // warps 8-15: A gather
+constexpr int kGatherWarps = 8;
+constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
+constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
+
 struct SmemLayout {
-  uint32_t a_off, b_off, bar_off, total;
+  uint32_t a_off, b_off, y_off, bar_off, bias_off, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int BN, int stages) {
+__host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * kABytes;
-  L.bar_off = L.b_off + static_cast<uint32_t>(stages) * BN * 128;
-  // full[stages], empty[stages], tmem_full, tmem slot
-  L.total = L.bar_off + (2 * stages + 2) * 8;
+  L.y_off = L.b_off + static_cast<uint32_t>(stages) * BN * 128;
+  L.bar_off = L.y_off + kEpiWarps * 2 * kYStageBytes;
+  // full[stages], empty[stages], tmem_full[2], tmem_empty[2], tmem slot
+  L.bias_off = L.bar_off + ((2 * stages + 5) * 8 + 15) / 16 * 16;
+  // bias padded so a 32-column epilogue slice never reads past it
+  L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
 }
 
+// Gathers the A tiles of one output tile (128 im2col rows) for every K
+// block into the stage ring. `it` is the CTA-wide pipeline iteration counter
+// (continues across tiles), so stage/phase follow the global sequence.
 template <int G>
-__device__ __forceinline__ void gather_a_tiles(const ConvGemmArgs& a, uint8_t* smem,
-                                               uint64_t* full, uint64_t* empty, int m0) {
-  constexpr int GPR = 64 / G;        // granules per 128 B row
-  constexpr int RPP = 128 / GPR;     // rows covered per pass of 128 threads
-  constexpr int PASSES = 128 / RPP;  // passes per tile
+__device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* smem,
+                                              uint64_t* full, uint64_t* empty, int m0,
+                                              uint32_t& it) {
+  constexpr int GPR = 64 / G;                   // granules per 128 B row
+  constexpr int RPP = kGatherWarps * 32 / GPR;  // rows covered per pass of the gather warps
+  constexpr int PASSES = kConvBM / RPP;         // passes per tile
   constexpr int GB = G * 2;          // granule bytes
-  const int t = threadIdx.x;
+  const int t = threadIdx.x - kGatherWarp0 * 32;
   const int gi = t % GPR;
   const int r0 = t / GPR;
-  const int HoWo = a.Ho * a.Wo;
 
+  // Output coordinates of this thread's rows m0+r0+p*RPP, by one division
+  // for the first row and carries after that (rows are consecutive pixels).
   int pix[PASSES], hi0[PASSES], wi0[PASSES];
+  {
+    const int HoWo = a.Ho * a.Wo;
+    const int m_first = m0 + r0;
+    int n = m_first / HoWo;
+    const int rem = m_first - n * HoWo;
+    int ho = rem / a.Wo;
+    int wo = rem - ho * a.Wo;
 #pragma unroll
-  for (int p = 0; p < PASSES; ++p) {
-    const int m = m0 + r0 + p * RPP;
-    if (m < a.M) {
-      const int n = m / HoWo;
-      const int rem = m - n * HoWo;
-      const int ho = rem / a.Wo;
-      const int wo = rem - ho * a.Wo;
+    for (int p = 0; p < PASSES; ++p) {
+      const bool live = m_first + p * RPP < a.M;
       pix[p] = n * a.H * a.W;
-      hi0[p] = ho * a.stride_h - a.pad_h;
+      hi0[p] = live ? ho * a.stride_h - a.pad_h : -(1 << 28);  // dead rows read zeros
       wi0[p] = wo * a.stride_w - a.pad_w;
-    } else {
-      pix[p] = 0;
-      hi0[p] = -(1 << 28);  // never inside the image: whole row zero-filled
-      wi0[p] = 0;
+      wo += RPP;
+      while (wo >= a.Wo) {
+        wo -= a.Wo;
+        if (++ho == a.Ho) {
+          ho = 0;
+          ++n;
+        }
+      }
     }
   }
 
   const uint32_t smem_base = ptx::smem_u32(smem);
   const int col_bytes = gi * GB;
-  for (int kb = 0; kb < a.num_kb; ++kb) {
-    const int s = kb % a.stages;
-    if (kb >= a.stages) ptx::mbar_wait(&empty[s], ((kb / a.stages) - 1) & 1);
+  // Rows of one thread differ by multiples of 8, so the 128 B swizzle phase
+  // (row & 7) is fixed per thread.
+  const uint32_t lane_off = static_cast<uint32_t>(r0) * 128 +
+                            ((((col_bytes >> 4) ^ (r0 & 7)) << 4) | (col_bytes & 15));
+  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
+    const uint32_t s = it % a.stages;
+    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
     const int k = kb * kConvBK + gi * G;
     const int tap = k / a.C;
     const int c = k - tap * a.C;
     const int r = tap / a.S;
     const int sx = tap - r * a.S;
     const bool kvalid = tap < a.taps;
-    const uint32_t sbase = smem_base + s * kABytes;
+    const uint32_t sbase = smem_base + s * kABytes + lane_off;
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
-      const int row = r0 + p * RPP;
       const int hi = hi0[p] + r;
       const int wi = wi0[p] + sx;
-      const bool v = kvalid && hi >= 0 && hi < a.H && wi >= 0 && wi < a.W;
+      const bool v = kvalid && static_cast<unsigned>(hi) < static_cast<unsigned>(a.H) &&
+                     static_cast<unsigned>(wi) < static_cast<unsigned>(a.W);
       const __nv_bfloat16* src =
           v ? a.x + (static_cast<size_t>(pix[p] + hi * a.W + wi) * a.C + c) : a.x;
-      const uint32_t off =
-          row * 128 + ((((col_bytes >> 4) ^ (row & 7)) << 4) | (col_bytes & 15));
+      const uint32_t off = static_cast<uint32_t>(p * RPP * 128);
       if constexpr (GB == 16) {
         ptx::cp_async_16(sbase + off, src, v ? 16u : 0u);
       } else {
@@ -116,16 +151,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, int m, int n,
-                                               const uint32_t (&raw)[16]) {
+// bias_s: the layer's bias staged in shared memory (indexed by channel).
+__device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const float* bias_s, int m,
+                                               int n, const uint32_t (&raw)[16]) {
   float v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
   if (n + 16 <= a.Cout) {
-    const float4* b4 = reinterpret_cast<const float4*>(a.bias + n);
+    const float4* b4 = reinterpret_cast<const float4*>(bias_s + n);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 b = __ldg(b4 + q);
+      const float4 b = b4[q];
       v[4 * q + 0] += b.x;
       v[4 * q + 1] += b.y;
       v[4 * q + 2] += b.z;
@@ -167,7 +203,7 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, int m, int
     }
   } else {
     for (int j = 0; j < 16 && n + j < a.Cout; ++j) {
-      float x = v[j] + a.bias[n + j];
+      float x = v[j] + bias_s[n + j];
       if (a.residual) x += __bfloat162float(a.residual[static_cast<size_t>(m) * a.ld_res + n + j]);
       if (a.relu) x = fmaxf(x, 0.0f);
       const size_t o = static_cast<size_t>(m) * a.ldy + a.c_off + n + j;
@@ -179,35 +215,94 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, int m, int
   }
 }
 
+// TMA-store epilogue for one 32-column slice of the warp's 32 rows: TMEM ->
+// registers, + bias (+ residual), ReLU, packed into the 128 B-swizzled
+// staging rows (lane = row, conflict-free 16 B stores). `col` is the slice's
+// offset inside its staging group.
+__device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const float* bias_s, int m,
+                                                   int n, const uint32_t (&raw)[32], uint8_t* group,
+                                                   int col, int lane) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) + bias_s[n + j];
+  if (a.residual && m < a.M) {
+    const __nv_bfloat16* rrow = a.residual + static_cast<size_t>(m) * a.ld_res + n;
+    if (n + 32 <= a.Cout) {
+      const uint4* rp = reinterpret_cast<const uint4*>(rrow);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 rr = __ldg(rp + q);
+        const uint32_t w[4] = {rr.x, rr.y, rr.z, rr.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[8 * q + 2 * e] += bf16_lo(w[e]);
+          v[8 * q + 2 * e + 1] += bf16_hi(w[e]);
+        }
+      }
+    } else {
+      for (int j = 0; j < 32 && n + j < a.Cout; ++j) v[j] += __bfloat162float(rrow[j]);
+    }
+  }
+  if (a.relu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+  }
+  uint8_t* row = group + lane * 128;
+  const int sw = lane & 7;  // 128 B swizzle: 16 B chunk c lives at c ^ (row & 7)
+  if (a.out_f32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)  // 32 fp32 = the whole 128 B row
+      *reinterpret_cast<float4*>(row + ((q ^ sw) << 4)) =
+          make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+    const int c16 = col >> 3;  // 8 bf16 per 16 B chunk
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(row + (((c16 + q) ^ sw) << 4)) =
+          make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_gemm_kernel(const __grid_constant__ ConvGemmArgs args) {
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const SmemLayout L = smem_layout(args.BN, args.stages);
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout);
+  float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
+  const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
+  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x)
+    bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
+  if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + args.stages;
-  uint64_t* tmem_full = empty + args.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + args.stages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * args.BN;
-  const int m0 = blockIdx.y * kConvBM;
+  const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
+  const int tiles = n_tiles * ((args.M + kConvBM - 1) / kConvBM);
+  const uint32_t acc_stride = args.tmem_cols / 2;  // two accumulator buffers
 
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     if (lane == 0) {
-      const uint32_t a_arrivals = (MODE == static_cast<int>(ConvLoadMode::kTmaA)) ? 0u : 128u;
       for (int s = 0; s < args.stages; ++s) {
-        ptx::mbar_init(&full[s], a_arrivals + 1);
+        ptx::mbar_init(&full[s], (kTmaA ? 0u : kGatherWarps * 32u) + 1u);
         ptx::mbar_init(&empty[s], 1);
       }
-      ptx::mbar_init(tmem_full, 1);
+      for (int b = 0; b < 2; ++b) {
+        ptx::mbar_init(&tmem_full[b], 1);
+        ptx::mbar_init(&tmem_empty[b], kEpiWarps);  // one arrival per epilogue warp
+      }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
-      if (MODE == static_cast<int>(ConvLoadMode::kTmaA)) ptx::tma_prefetch_desc(&args.tmap_a);
+      if (kTmaA) ptx::tma_prefetch_desc(&args.tmap_a);
     }
     __syncwarp();
     ptx::tmem_alloc(tmem_slot, args.tmem_cols);
@@ -216,69 +311,130 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < 4) {
-    if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather16)) {
-      gather_a_tiles<8>(args, smem + L.a_off, full, empty, m0);
-    } else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8)) {
-      gather_a_tiles<4>(args, smem + L.a_off, full, empty, m0);
+  if (warp < kEpiWarps) {
+    // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31)
+    // and takes every other 128 B column group (w/4 picks which).
+    const int quarter = warp & 3;
+    const int half = warp >> 2;
+    uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;
+    const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
+    uint32_t j = 0, groups = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+      const int m0 = (tile / n_tiles) * kConvBM;
+      const int n0 = (tile % n_tiles) * args.BN;
+      const uint32_t acc = j & 1;
+      ptx::mbar_wait(&tmem_full[acc], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int m = m0 + quarter * 32 + lane;
+      const uint32_t t_row =
+          tmem_base + acc * acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
+      if (args.debug_flags & 1) {
+        // release only
+      } else if (args.y_tma) {
+        for (int g0 = half * group_cols; g0 < args.BN && n0 + g0 < args.Cout; g0 += 2 * group_cols) {
+          uint8_t* group = ystage + (groups & 1) * kYStageBytes;
+          if (groups >= 2) {  // the store issued two groups ago must have read `group`
+            if (lane == 0) ptx::bulk_wait_read<1>();
+            __syncwarp();
+          }
+          for (int c = 0; c < group_cols && g0 + c < args.BN; c += 32) {
+            uint32_t raw[32];
+            ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
+            ptx::tmem_ld_wait();
+            epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane);
+          }
+          ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+            ptx::bulk_commit();
+          }
+          ++groups;
+        }
+      } else {
+        for (int c0 = half * 16; c0 < args.BN && n0 + c0 < args.Cout; c0 += 32) {
+          uint32_t raw[16];
+          ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
+          ptx::tmem_ld_wait();
+          if (m < args.M) epilogue_chunk(args, bias_s, m, n0 + c0, raw);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
     }
-    // Epilogue: this warp owns TMEM lanes [32*warp, 32*warp + 32).
-    ptx::mbar_wait(tmem_full, 0);
-    ptx::tc_fence_after();
-    const int m = m0 + threadIdx.x;
-    const uint32_t t_row = tmem_d + (static_cast<uint32_t>(warp * 32) << 16);
-    for (int c0 = 0; c0 < args.BN; c0 += 16) {
-      uint32_t raw[16];
-      ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
-      ptx::tmem_ld_wait();
-      if (m < args.M && n0 + c0 < args.Cout) epilogue_chunk(args, m, n0 + c0, raw);
+    if (lane == 0) ptx::bulk_wait<0>();
+  } else if (warp < kGatherWarp0 + kGatherWarps) {
+    if constexpr (!kTmaA) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles) * kConvBM;
+        if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather16))
+          gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, it);
+        else
+          gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, it);
+      }
     }
-  } else if (warp == 4) {
+  } else if (warp == kTmaWarp) {
     if (lane == 0) {
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      const uint32_t tx = b_bytes + (MODE == static_cast<int>(ConvLoadMode::kTmaA) ? kABytes : 0);
-      for (int kb = 0; kb < args.num_kb; ++kb) {
-        const int s = kb % args.stages;
-        if (kb >= args.stages) ptx::mbar_wait(&empty[s], ((kb / args.stages) - 1) & 1);
-        ptx::mbar_arrive_expect_tx(&full[s], tx);
-        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
-                         kb * kConvBK, n0);
-        if constexpr (MODE == static_cast<int>(ConvLoadMode::kTmaA)) {
-          ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * kABytes), &args.tmap_a, &full[s],
-                           kb * kConvBK, m0);
+      const uint32_t tx = b_bytes + (kTmaA ? kABytes : 0);
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles) * kConvBM;
+        const int n0 = (tile % n_tiles) * args.BN;
+        for (int kb = 0; kb < args.num_kb; ++kb, ++it) {
+          const uint32_t s = it % args.stages;
+          if (it >= static_cast<uint32_t>(args.stages))
+            ptx::mbar_wait(&empty[s], ((it / args.stages) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&full[s], tx);
+          ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
+                           kb * kConvBK, n0);
+          if constexpr (kTmaA)
+            ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * kABytes), &args.tmap_a, &full[s],
+                             kb * kConvBK, m0);
         }
       }
     }
-  } else {  // warp 5: MMA issuer
+  } else {  // kMmaWarp: MMA issuer
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      for (int kb = 0; kb < args.num_kb; ++kb) {
-        const int s = kb % args.stages;
-        ptx::mbar_wait(&full[s], (kb / args.stages) & 1);
+      uint32_t it = 0, j = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        const uint32_t acc = j & 1;
+        if (j >= 2) ptx::mbar_wait(&tmem_empty[acc], ((j >> 1) - 1) & 1);
         ptx::tc_fence_after();
-        if constexpr (MODE != static_cast<int>(ConvLoadMode::kTmaA)) ptx::fence_proxy_async_smem();
-        const uint64_t da = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.a_off + s * kABytes));
-        const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + s * b_bytes));
+        const uint32_t d = tmem_base + acc * acc_stride;
+        for (int kb = 0; kb < args.num_kb; ++kb, ++it) {
+          const uint32_t s = it % args.stages;
+          ptx::mbar_wait(&full[s], (it / args.stages) & 1);
+          ptx::tc_fence_after();
+          if constexpr (!kTmaA) ptx::fence_proxy_async_smem();
+          const uint64_t da =
+              ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.a_off + s * kABytes));
+          const uint64_t db =
+              ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + s * b_bytes));
 #pragma unroll
-        for (int k = 0; k < kConvBK / 16; ++k) {
-          // +32 B along K inside the swizzle row = +2 in the >>4 start field.
-          ptx::umma_bf16(tmem_d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < kConvBK / 16; ++k) {
+            // +32 B along K inside the swizzle row = +2 in the >>4 start field.
+            ptx::umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
+          ptx::umma_commit(&empty[s]);
         }
-        ptx::umma_commit(&empty[s]);
+        ptx::umma_commit(&tmem_full[acc]);
       }
-      ptx::umma_commit(tmem_full);
     }
     __syncwarp();
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_d, args.tmem_cols);
+    ptx::tmem_dealloc(tmem_base, args.tmem_cols);
   }
 }
 
@@ -317,8 +473,37 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t conv_gemm_smem_bytes(int BN, int stages) {
-  return smem_layout(BN, stages).total + 1024;  // + alignment slack
+bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
+                     uint64_t row_stride_elems, bool f32) {
+  EncodeTiledFn fn = get_encode_fn();
+  const uint64_t esz = f32 ? 4 : 2;
+  if (!fn || (row_stride_elems * esz) % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0)
+    return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {row_stride_elems * esz};
+  const cuuint32_t box[2] = {f32 ? 32u : 64u, 32};  // one 128 B row per output row
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base,
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+uint32_t conv_gemm_tmem_cols(int BN) {
+  uint32_t c = 32;
+  while (static_cast<int>(c) < 2 * BN) c <<= 1;  // two fp32 accumulators
+  return c;
+}
+
+int conv_gemm_stages(int BN, int cout) {
+  const int ctas = 1;  // 18 warps: one CTA per SM
+  const int per_stage = kABytes + BN * kConvBK * 2;
+  const int fixed = static_cast<int>(smem_layout(BN, 0, cout).total) + 64 * 8 + 1024;
+  const int budget = (227 * 1024) / ctas - fixed;
+  return std::max(1, std::min(kConvMaxStages, budget / per_stage));
+}
+
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout) {
+  return smem_layout(BN, stages, cout).total + 1024;  // + alignment slack
 }
 
 cudaError_t conv_gemm_init() {
@@ -339,9 +524,28 @@ cudaError_t conv_gemm_init() {
   return status;
 }
 
-cudaError_t launch_conv_gemm(const ConvGemmArgs& args, ConvLoadMode mode, cudaStream_t stream) {
-  const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages);
-  const dim3 grid((args.Cout + args.BN - 1) / args.BN, (args.M + kConvBM - 1) / kConvBM);
+int conv_gemm_sm_count() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
+
+cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cudaStream_t stream) {
+  // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
+  ConvGemmArgs args = in_args;
+  const int group_cols = args.out_f32 ? 32 : 64;
+  if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
+  const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages, args.Cout);
+  const int tiles = ((args.Cout + args.BN - 1) / args.BN) * ((args.M + kConvBM - 1) / kConvBM);
+  // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
+  const int by_smem = static_cast<int>((227 * 1024) / smem);
+  const int by_tmem = static_cast<int>(512 / args.tmem_cols);
+  const int per_sm = std::max(1, std::min(by_smem, by_tmem));
+  const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
   switch (mode) {
     case ConvLoadMode::kGather16:
       conv_gemm_kernel<0><<<grid, kConvThreads, smem, stream>>>(args);

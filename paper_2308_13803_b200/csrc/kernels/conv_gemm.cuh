@@ -12,8 +12,11 @@ namespace ds {
 
 constexpr int kConvBM = 128;       // UMMA M: output pixels per tile
 constexpr int kConvBK = 64;        // K elements per pipeline stage (one 128 B swizzle row)
-constexpr int kConvThreads = 192;  // 4 gather/epilogue warps + TMA warp + MMA warp
-constexpr int kConvMaxStages = 4;
+// Persistent CTA (one per SM): 8 epilogue warps, 8 gather warps, 1 TMA
+// warp, 1 MMA warp.
+constexpr int kConvThreads = 576;
+constexpr int kConvMaxStages = 8;
+constexpr int kConvSmemBudget = 200 * 1024;  // operand ring budget per CTA (1 CTA / SM)
 
 // One conv (or FC, as a 1x1 conv over a 1x1 image) as a GEMM
 //   Y[m, n] = act( sum_k A[m, k] * Wt[n, k] + bias[n] (+ R[m, n]) )
@@ -22,6 +25,8 @@ constexpr int kConvMaxStages = 4;
 struct ConvGemmArgs {
   CUtensorMap tmap_b;  // weights [Cout][Kpad] bf16, box {64, BN}, 128 B swizzle
   CUtensorMap tmap_a;  // input viewed as [rows][C] (1x1 stride-1 convs only)
+  CUtensorMap tmap_y;  // output slice [rows][Cout] at y + c_off, 128 B x 32-row boxes (y_tma)
+  int y_tma;           // epilogue stores through smem + TMA (else direct stores)
   const __nv_bfloat16* x;
   int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
   int R, S, stride_h, stride_w, pad_h, pad_w;
@@ -37,6 +42,7 @@ struct ConvGemmArgs {
   void* y;
   int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
   int out_f32, relu;
+  int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
 };
 
 enum class ConvLoadMode : int {
@@ -50,7 +56,20 @@ enum class ConvLoadMode : int {
 bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                          uint64_t row_stride_elems, uint32_t box_rows);
 
-size_t conv_gemm_smem_bytes(int BN, int stages);
+// Output map for the TMA-store epilogue: [rows][cols] bf16 or fp32 starting
+// at `base` (the channel slice), row stride in elements, boxes of 32 rows x
+// 128 B (64 bf16 / 32 fp32 columns) with 128 B swizzle. False when TMA
+// cannot address it (row stride or base not 16 B aligned).
+bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
+                     uint64_t row_stride_elems, bool f32);
+
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout);
+
+// Operand-ring depth for an N tile: as deep as kConvMaxStages allows within
+// the per-CTA budget, where two CTAs share an SM whenever their TMEM
+// (2 x BN accumulator columns each) fits.
+int conv_gemm_stages(int BN, int cout);
+uint32_t conv_gemm_tmem_cols(int BN);
 
 // Must run once per device before the first launch (and before any capture).
 cudaError_t conv_gemm_init();

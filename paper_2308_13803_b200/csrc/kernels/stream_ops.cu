@@ -1,8 +1,8 @@
-// HBM-bound layers of the forward pass. Each thread owns one output pixel x
-// 8 channels (one 16 B vector), so consecutive threads in a warp touch
-// consecutive 16 B chunks of the NHWC row: fully coalesced 512 B per warp
-// access. Neighbouring taps of the stencils hit L1/L2, so DRAM traffic stays
-// close to one read of the input and one write of the output.
+// HBM-bound layers of the forward pass. Threads own 8 channels (one 16 B
+// vector) of one or more output pixels, so consecutive threads in a warp
+// touch consecutive 16 B chunks of the NHWC row: fully coalesced 512 B per
+// warp access. Neighbouring taps of the stencils hit L1/L2, so DRAM traffic
+// stays close to one read of the input and one write of the output.
 #include "stream_ops.cuh"
 
 namespace ds {
@@ -44,7 +44,77 @@ __global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __res
   out[p] = make_uint2(pack2(v[0], v[1]), pack2(v[2], 0.0f));
 }
 
-__global__ void dwconv3x3_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
+// Depthwise 3x3, register-blocked: a thread owns 8 channels (one 16 B
+// vector) x kDwCols consecutive output columns of one output row, so each
+// loaded input vector feeds up to 3 outputs from registers; consecutive
+// threads take consecutive channel groups (coalesced 16 B loads/stores along
+// C). Weights come through the read-only path (L1-resident per block).
+constexpr int kDwCols = 4;
+
+template <int STRIDE>
+__global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
+    const uint4* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const float* __restrict__ bias, uint4* __restrict__ y, int h, int wd, int c, int ho, int wo,
+    int cg_log2, int xq_per_row, long long work) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= work) return;
+  const int cg = 1 << cg_log2;
+  const int g = static_cast<int>(i & (cg - 1));
+  const long long rest = i >> cg_log2;
+  const int xq = static_cast<int>(rest % xq_per_row);
+  const long long row = rest / xq_per_row;  // n * ho + oy
+  const int oy = static_cast<int>(row % ho);
+  const int n = static_cast<int>(row / ho);
+  const int ox0 = xq * kDwCols;
+  constexpr int IN_COLS = (kDwCols - 1) * STRIDE + 3;
+  const int ix0 = ox0 * STRIDE - 1;
+
+  float acc[kDwCols][8];
+  const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * g);
+  const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * g + 1);
+  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+  for (int q = 0; q < kDwCols; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[q][e] = bv[e];
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int iy = oy * STRIDE - 1 + r;
+    if (iy < 0 || iy >= h) continue;
+    const uint4* xrow = x + (static_cast<long long>(n) * h + iy) * wd * cg + g;
+    float wr[3][8];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) unpack8(__ldg(wv + (r * 3 + s) * cg + g), wr[s]);
+#pragma unroll
+    for (int col = 0; col < IN_COLS; ++col) {
+      const int ix = ix0 + col;
+      if (ix < 0 || ix >= wd) continue;
+      float xv[8];
+      unpack8(__ldg(xrow + static_cast<long long>(ix) * cg), xv);
+#pragma unroll
+      for (int q = 0; q < kDwCols; ++q) {
+        const int s = col - q * STRIDE;  // tap of output q that reads this column
+        if (s < 0 || s > 2) continue;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[q][e] = fmaf(xv[e], wr[s][e], acc[q][e]);
+      }
+    }
+  }
+  uint4* yrow = y + (static_cast<long long>(n) * ho + oy) * wo * cg + g;
+#pragma unroll
+  for (int q = 0; q < kDwCols; ++q) {
+    if (ox0 + q >= wo) break;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[q][e] = fmaxf(acc[q][e], 0.0f);
+    yrow[static_cast<long long>(ox0 + q) * cg] = pack8(acc[q]);
+  }
+}
+
+// One output pixel x 8 channels per thread (stride-2 layers, where a
+// column is shared by at most two outputs and blocking does not pay).
+__global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
                                  const float4* __restrict__ bias, uint4* __restrict__ y, int h,
                                  int wd, int cg, int ho, int wo, int stride, long long work) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -171,11 +241,22 @@ cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, con
                              cudaStream_t stream) {
   const int ho = (h + 2 - 3) / stride + 1, wo = (wd + 2 - 3) / stride + 1;
   const int cg = c / 8;
-  const long long work = static_cast<long long>(n) * ho * wo * cg;
-  dwconv3x3_kernel<<<grid_for(work), kBlock, 0, stream>>>(
-      reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
-      reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd, cg, ho, wo,
-      stride, work);
+  int cg_log2 = 0;
+  while ((1 << cg_log2) < cg) ++cg_log2;
+  if ((1 << cg_log2) != cg) return cudaErrorInvalidValue;  // channel groups must be a power of 2
+  const int xq = (wo + kDwCols - 1) / kDwCols;
+  const long long work = static_cast<long long>(n) * ho * xq * cg;
+  if (stride == 1)
+    dwconv3x3_kernel<1><<<grid_for(work), kBlock, 0, stream>>>(
+        reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h, wd, c, ho, wo,
+        cg_log2, xq, work);
+  else {
+    const long long pw = static_cast<long long>(n) * ho * wo * cg;
+    dwconv3x3_px_kernel<<<grid_for(pw), kBlock, 0, stream>>>(
+        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
+        reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd, cg, ho, wo,
+        stride, pw);
+  }
   return cudaGetLastError();
 }
 

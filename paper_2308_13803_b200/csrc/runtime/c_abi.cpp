@@ -6,6 +6,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "abi_internal.hpp"
 
 namespace {
@@ -148,6 +150,10 @@ ds_status ds_drain(ds_backend* b) {
   return guard([&] { b->impl->drain(); });
 }
 
+void ds_nvtx_push(const char* name) { nvtxRangePushA(name ? name : ""); }
+
+void ds_nvtx_pop(void) { nvtxRangePop(); }
+
 ds_status ds_timer_start(ds_backend* b) {
   if (!b) return null_handle();
   return guard([&] { b->impl->timer_start(); });
@@ -213,6 +219,20 @@ ds_status ds_profile_kernels(ds_backend* b, int bs, int reps, double* ms_out, in
     const auto ms = b->impl->profile_kernels(bs, reps < 1 ? 1 : reps);
     if (static_cast<int>(ms.size()) > cap) throw std::invalid_argument("output too small");
     for (size_t i = 0; i < ms.size(); ++i) ms_out[i] = ms[i];
+  });
+}
+
+ds_status ds_debug_read_buffer(ds_backend* b, int buffer, int bs, void* out, size_t cap,
+                               size_t* out_len) {
+  if (!b || !out_len) return null_handle();
+  return guard([&] {
+    const ds::ModelSpec& m = b->impl->model();
+    if (buffer < 0 || buffer >= static_cast<int>(m.buffers.size()))
+      throw std::invalid_argument("invalid buffer");
+    if (bs < 1 || bs > b->impl->config().abs_max_bs) throw std::invalid_argument("invalid batch size");
+    const ds::BufferSpec& s = m.buffers[buffer];
+    *out_len = static_cast<size_t>(bs) * s.h * s.w * s.c * (s.f32 ? 4 : 2);
+    if (out && cap >= *out_len) b->impl->read_buffer(buffer, bs, out);
   });
 }
 

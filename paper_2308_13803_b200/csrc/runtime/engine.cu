@@ -19,26 +19,19 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
 // N tile: one tile when Cout fits in 256 (UMMA N <= 256, multiple of 16),
-// otherwise the smallest even split.
+// otherwise the smallest even split in multiples of 64, so the epilogue's
+// 64-column TMA store boxes never cross into the neighbouring N tile.
 int choose_bn(int cout) {
   if (cout <= 256) return round_up(cout, 16);
   const int n = (cout + 255) / 256;
-  return round_up((cout + n - 1) / n, 16);
+  return round_up((cout + n - 1) / n, 64);
 }
 
-int choose_stages(int bn, int num_kb) {
-  const int per_stage = kConvBM * kConvBK * 2 + bn * kConvBK * 2;
-  int st = (200 * 1024) / per_stage;
-  st = std::min(st, kConvMaxStages);
-  st = std::min(st, num_kb);
-  return std::max(st, 1);
-}
+// The operand ring spans tiles (persistent kernel), so it is sized by the
+// shared-memory budget, not by the layer's K.
+int choose_stages(int bn, int cout) { return conv_gemm_stages(bn, cout); }
 
-uint32_t tmem_cols_for(int bn) {
-  uint32_t c = 32;
-  while (static_cast<int>(c) < bn) c <<= 1;
-  return c;
-}
+uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 
 }  // namespace
 
@@ -115,7 +108,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.taps = op.r * op.s;
     a.Cout = p.cout;
     a.BN = choose_bn(p.cout);
-    a.stages = choose_stages(a.BN, a.num_kb);
+    a.stages = choose_stages(a.BN, p.cout);
     a.tmem_cols = tmem_cols_for(a.BN);
     a.bias = d_b_ + hp.b_off.at(op.param);
     if (op.residual >= 0) {
@@ -131,8 +124,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
-    } else if (op.r == 1 && op.s == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 && op.pw == 0 &&
-               in.c >= kConvBK) {
+    } else if (op.r == 1 && op.s == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 && op.pw == 0) {
+      // A is a plain [pixels][C] matrix; for C < 64 the TMA box runs past
+      // the row and the out-of-bounds columns arrive as zeros.
       pl.mode = ConvLoadMode::kTmaA;
     } else {
       pl.mode = ConvLoadMode::kGather16;
@@ -143,6 +137,14 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
       if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
         throw CudaError("cuTensorMapEncodeTiled failed (activations)");
+    }
+    // TMA-store epilogue over the output channel slice (falls back to direct
+    // stores when TMA cannot address it, e.g. a 10-class fp32 head).
+    {
+      const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
+      const size_t esz = out.f32 ? 4 : 2;
+      void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
+      a.y_tma = encode_tmap_out(&a.tmap_y, base, rows, p.cout, out.c, out.f32) ? 1 : 0;
     }
   }
   check_cuda(cudaStreamSynchronize(stream_), "instance setup");
@@ -246,6 +248,13 @@ std::vector<double> Instance::profile_kernels(int bs, int reps) {
   for (auto& e : marks) cudaEventDestroy(e);
   for (auto& v : acc) v /= reps;
   return acc;
+}
+
+void Instance::read_buffer(int id, int bs, void* host) const {
+  const BufferSpec& b = m_.buffers.at(id);
+  const size_t bytes = static_cast<size_t>(bs) * b.h * b.w * b.c * (b.f32 ? 4 : 2);
+  check_cuda(cudaStreamSynchronize(stream_), "read_buffer");
+  check_cuda(cudaMemcpy(host, bufs_.at(id), bytes, cudaMemcpyDeviceToHost), "read_buffer");
 }
 
 void Instance::enqueue_forward(int bs) {

@@ -52,6 +52,8 @@ class Instance {
   std::vector<double> profile_kernels(int bs, int reps);
 
   cudaStream_t stream() const { return stream_; }
+  // Debug: copies activation buffer `id` (first bs images) to host, raw bytes.
+  void read_buffer(int id, int bs, void* host) const;
   uint8_t* images() const { return d_images_; }
   float* logits() const { return d_logits_; }
   float* probs() const { return d_probs_; }
@@ -127,6 +129,7 @@ class Backend {
   }
 
   const ModelSpec& model() const { return model_; }
+  void read_buffer(int id, int bs, void* host) { instance(0).read_buffer(id, bs, host); }
   int64_t kernel_launches() const { return kernel_launches_; }
   int64_t h2d_bytes() const { return h2d_bytes_; }
   int64_t d2h_bytes() const { return d2h_bytes_; }

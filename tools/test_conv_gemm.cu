@@ -4,9 +4,11 @@
 // parity gate proper lives in tests/ (through the C-ABI).
 #include "../paper_2308_13803_b200/csrc/kernels/conv_gemm.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <random>
 #include <vector>
 
@@ -72,9 +74,15 @@ static int run(const Case& cs) {
   a.x = dx; a.H = cs.H; a.W = cs.W; a.C = cs.C; a.R = cs.R; a.S = cs.S;
   a.stride_h = cs.sh; a.stride_w = cs.sw; a.pad_h = cs.ph; a.pad_w = cs.pw;
   a.Ho = Ho; a.Wo = Wo; a.M = M; a.num_kb = Kpad / 64; a.taps = cs.R * cs.S;
-  a.Cout = cs.Cout; a.BN = cs.BN; a.stages = a.num_kb < 4 ? a.num_kb : 4;
-  a.tmem_cols = 32;
-  while ((int)a.tmem_cols < cs.BN) a.tmem_cols *= 2;
+  a.Cout = cs.Cout; a.BN = cs.BN;
+  a.stages = conv_gemm_stages(cs.BN, cs.Cout);
+  a.tmem_cols = conv_gemm_tmem_cols(cs.BN);
+  a.y_tma = encode_tmap_out(&a.tmap_y, static_cast<uint8_t*>(dy) + cs.c_off * (cs.f32 ? 4 : 2), M,
+                            cs.Cout, ldy, cs.f32) ? 1 : 0;
+  if (getenv("NO_TMA_STORE")) a.y_tma = 0;
+  if (getenv("STAGES")) a.stages = atoi(getenv("STAGES"));
+  if (getenv("DEBUG_FLAGS")) a.debug_flags = atoi(getenv("DEBUG_FLAGS"));
+  if (getenv("TMEM_COLS")) a.tmem_cols = atoi(getenv("TMEM_COLS"));  // 512 forces 1 CTA/SM
   a.bias = db; a.residual = cs.residual ? dr : nullptr; a.ld_res = cs.Cout;
   a.y = dy; a.ldy = ldy; a.c_off = cs.c_off; a.out_f32 = cs.f32; a.relu = cs.relu;
   // channels [c_off, c_off+Cout) of an ldy-wide buffer; keep Cout+c_off <= ldy
@@ -128,7 +136,7 @@ static int run(const Case& cs) {
   return bad ? 1 : 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
   const Case cases[] = {
       {"1x1 s1 tmaA", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"1x1 s1 gather", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
@@ -143,9 +151,18 @@ int main() {
       {"fc 10 classes", 5, 1, 1, 128, 1, 1, 1, 1, 0, 0, 10, 16, ConvLoadMode::kTmaA, false, true, false, 0, 0},
       {"big 1x1 s1", 64, 56, 56, 64, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"big 3x3 256", 32, 14, 14, 256, 3, 3, 1, 1, 1, 1, 256, 256, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"mbv1 stem bs128", 128, 224, 224, 4, 3, 3, 2, 2, 1, 1, 32, 32, ConvLoadMode::kGather8, false, false, true, 0, 0},
+      {"mbv1 pw1 bs128", 128, 112, 112, 32, 1, 1, 1, 1, 0, 0, 64, 64, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 pw1g bs128", 128, 112, 112, 32, 1, 1, 1, 1, 0, 0, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"tmaA C32 small", 3, 5, 7, 32, 1, 1, 1, 1, 0, 0, 48, 48, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 pw2 bs128", 128, 56, 56, 64, 1, 1, 1, 1, 0, 0, 128, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 pw7 bs128", 128, 14, 14, 512, 1, 1, 1, 1, 0, 0, 512, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
   };
+  // Optional filter: substring of the case name; "--no-check" skips the CPU reference.
+  const char* only = argc > 1 ? argv[1] : nullptr;
   int fails = 0;
-  for (const auto& c : cases) fails += run(c);
+  for (const auto& c : cases)
+    if (!only || std::strstr(c.name, only)) fails += run(c);
   printf("%s (%d failing cases)\n", fails ? "FAIL" : "PASS", fails);
   return fails ? 1 : 0;
 }
