@@ -69,7 +69,7 @@ def run_job(scenario_path: str, job_index: int = 0, mode: str = "stock", tape=No
             max_periods: int = 1_000_000, max_tape: int = 50_000_000):
     """Reference run_job on the tape seam. mode: stock | record | replay."""
     l = lib()
-    m = {"stock": 0, "record": 1, "replay": 2}[mode]
+    m = {"stock": 0, "record": 1, "replay": 2, "callback": 3}[mode]
     t = np.ascontiguousarray(tape if tape is not None else np.zeros(0), dtype=np.float64)
     n_rec, tape_n, n_ra, consumed = (ctypes.c_size_t() for _ in range(4))
     # first call sizes the outputs

@@ -25,8 +25,9 @@ void set_err(char* err, size_t cap, const std::string& msg) {
 
 void set_mode(int mode, const double* tape, size_t tape_len) {
   auto& s = refseam::state();
-  s.mode = mode == 2 ? refseam::Mode::kReplay
-                     : (mode == 1 ? refseam::Mode::kRecord : refseam::Mode::kStock);
+  s.mode = mode == 3   ? refseam::Mode::kCallback
+           : mode == 2 ? refseam::Mode::kReplay
+                       : (mode == 1 ? refseam::Mode::kRecord : refseam::Mode::kStock);
   s.tape.clear();
   s.pos = 0;
   if (mode == 2) s.tape.assign(tape, tape + tape_len);
@@ -68,6 +69,14 @@ void pack_summary(const JobSummary& s, double* o) {
 extern "C" {
 
 int ref_record_width(void) { return kRecordWidth; }
+
+// Callback seam (mode 3 of ref_run_job): latencies come from host functions.
+void ref_set_callbacks(refseam::BatchFn batch, refseam::MtFn mt, refseam::ChangeFn change) {
+  auto& s = refseam::state();
+  s.batch_fn = batch;
+  s.mt_fn = mt;
+  s.change_fn = change;
+}
 int ref_summary_width(void) { return kSummaryWidth; }
 
 // Runs job `job_index` of a scenario file through reference run_job.
