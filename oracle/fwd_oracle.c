@@ -745,3 +745,66 @@ int oracle_param_device_layout(const char* id, int layer, uint16_t* w, size_t w_
   }
   return 2;
 }
+
+/* ---- IR export for the independent torch cross-check (tests/golden) ---- */
+int oracle_num_ops(const char* id) {
+  net* n = get_net(id);
+  return n ? n->nops : -1;
+}
+
+int oracle_num_buffers(const char* id) {
+  net* n = get_net(id);
+  return n ? n->nb : -1;
+}
+
+int oracle_buffer_shape(const char* id, int b, int* h, int* w, int* c) {
+  net* n = get_net(id);
+  if (!n || b < 0 || b >= n->nb) return 1;
+  *h = n->buf[b].h;
+  *w = n->buf[b].w;
+  *c = n->buf[b].c;
+  return 0;
+}
+
+/* f[14] = kind, in, out, c_off, res, kh, kw, sh, sw, ph, pw, relu, cin, cout */
+int oracle_op(const char* id, int i, int* f) {
+  net* n = get_net(id);
+  if (!n || i < 0 || i >= n->nops) return 1;
+  const op* o = &n->ops[i];
+  int v[14] = {o->kind, o->in, o->out, o->c_off, o->res, o->kh, o->kw,
+               o->sh,   o->sw, o->ph,  o->pw,    o->relu, o->cin, o->cout};
+  memcpy(f, v, sizeof(v));
+  return 0;
+}
+
+/* Canonical fp32 (bf16-valued) weights of op i: conv/fc [cout][kh][kw][cin],
+ * depthwise [9][C]; bias [cout]. Returns the weight count, or -1. */
+long oracle_op_params(const char* id, int i, float* w, float* b) {
+  net* n = get_net(id);
+  if (!n || i < 0 || i >= n->nops) return -1;
+  const op* o = &n->ops[i];
+  if (!has_params(o)) return 0;
+  if (o->kind == K_DW) {
+    if (w) memcpy(w, o->wt, sizeof(float) * 9 * o->cout);
+    if (b) memcpy(b, o->bias, sizeof(float) * o->cout);
+    return 9L * o->cout;
+  }
+  const long kk = (long)o->kh * o->kw * o->cin;
+  if (w)
+    for (int co = 0; co < o->cout; ++co)
+      for (long k = 0; k < kk; ++k) w[(long)co * kk + k] = o->wt[k * o->cout + co];
+  if (b) memcpy(b, o->bias, sizeof(float) * o->cout);
+  return kk * o->cout;
+}
+
+/* The oracle's restated generator, same contract as ref_random(). */
+void oracle_random(uint64_t seed, int n, uint64_t* u64_out, double* gauss_out, uint64_t* mix_out) {
+  rstream a, b;
+  rs_init(&a, seed);
+  rs_init(&b, seed);
+  for (int i = 0; i < n; ++i) {
+    u64_out[i] = mt64_next(&a.g);
+    gauss_out[i] = rs_gaussian(&b);
+    mix_out[i] = mix_seed(seed, (uint64_t)i);
+  }
+}

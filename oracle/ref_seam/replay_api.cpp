@@ -189,3 +189,16 @@ int ref_render_scenario(const char* scenario_path, char* csv, size_t csv_cap, si
 }
 
 }  // extern "C"
+
+// The reference's generator (random.hpp:10-47), for pinning the oracles'
+// restatements: n raw 64-bit draws of RandomStream(seed) (next_u64), then n
+// gaussians of a fresh RandomStream(seed), and mix_seed(seed, 0..n-1).
+extern "C" void ref_random(uint64_t seed, int n, uint64_t* u64_out, double* gauss_out,
+                           uint64_t* mix_out) {
+  dnnscaler::RandomStream a(seed), b(seed);
+  for (int i = 0; i < n; ++i) {
+    u64_out[i] = a.next_u64();
+    gauss_out[i] = b.gaussian();
+    mix_out[i] = dnnscaler::mix_seed(seed, static_cast<uint64_t>(i));
+  }
+}

@@ -1,0 +1,69 @@
+"""The C ABI library (CPU only): it loads, exports every function
+include/dnnscaler_b200.h declares, and its device-free entry points work;
+device entry points fail loudly (no CPU fallback) when there is no GPU.
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2308_13803_b200 import _lib
+from paper_2308_13803_b200.backend import kernel_costs, model_info
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dnnscaler_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ds_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported():
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) > 40
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r"\bT (ds_[a-z0-9_]+)", out))
+    assert set(names) <= exported
+
+
+def test_library_is_native_sm100a():
+    out = subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_device_free_entry_points():
+    mi = model_info("mobilenet_v1")
+    assert (mi.in_h, mi.in_w, mi.classes) == (224, 224, 1000)
+    ks = kernel_costs("resnet50_v1")
+    assert ks[0]["kind"] == "stage" and ks[-1]["kind"] == "softmax"
+    assert abs(sum(k["flops_per_image"] for k in ks) - 2 * model_info("resnet50_v1").macs_per_image) < 1
+    with pytest.raises(ValueError, match="unknown model"):
+        model_info("vgg16")
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    st = lib.ds_backend_create(b"synthetic_cnn", _lib.DsConfig(8, 2), 42, 0, ctypes.byref(h))
+    assert st == _lib.DS_ECUDA and not h
+    assert "cuda" in _lib.last_error().lower() or "CUDA" in _lib.last_error()
+
+
+def test_null_handles_are_errors():
+    lib = _lib.load()
+    lat = ctypes.c_double()
+    assert lib.ds_run_batch(None, 1, ctypes.byref(lat)) == _lib.DS_EINVAL
+    assert lib.ds_mtl(None) == 0
