@@ -143,6 +143,117 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
   }
 }
 
+__device__ __forceinline__ void unpack8_bf16(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Depthwise-fused producer (kDwFused): for each K block (64 channels) the
+// gather warps compute A = relu(dw3x3(x) + b) for the tile's 128 depthwise
+// output pixels straight into the 128 B-swizzled A stage, so the depthwise
+// activation never goes to HBM. Each thread owns one 8-channel granule of 4
+// rows; weights and bias of the granule are loaded once per K block.
+__device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, uint64_t* full,
+                                          uint64_t* empty, int m0, uint32_t& it) {
+  constexpr int GPR = 8;                        // 16 B granules per 128 B row
+  constexpr int RPP = kGatherWarps * 32 / GPR;  // 32 rows per pass
+  constexpr int PASSES = kConvBM / RPP;         // 4
+  const int t = threadIdx.x - kGatherWarp0 * 32;
+  const int gi = t % GPR;
+  const int r0 = t / GPR;
+  const int st = a.dw_stride;
+
+  int pix[PASSES], hi0[PASSES], wi0[PASSES];
+  bool live[PASSES];
+  {
+    const int HoWo = a.Ho * a.Wo;
+    const int m_first = m0 + r0;
+    int n = m_first / HoWo;
+    const int rem = m_first - n * HoWo;
+    int ho = rem / a.Wo;
+    int wo = rem - ho * a.Wo;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      live[p] = m_first + p * RPP < a.M;
+      pix[p] = n * a.H * a.W;
+      hi0[p] = ho * st - 1;
+      wi0[p] = wo * st - 1;
+      wo += RPP;
+      while (wo >= a.Wo) {
+        wo -= a.Wo;
+        if (++ho == a.Ho) {
+          ho = 0;
+          ++n;
+        }
+      }
+    }
+  }
+  const uint4* xv = reinterpret_cast<const uint4*>(a.x);
+  const uint4* wv = reinterpret_cast<const uint4*>(a.dw_w);
+  const float4* bv = reinterpret_cast<const float4*>(a.dw_b);
+  const int cg_all = a.C / 8;
+  const uint32_t lane_off =
+      static_cast<uint32_t>(r0) * 128 + (static_cast<uint32_t>(gi ^ (r0 & 7)) << 4);
+  uint8_t* stage_base = smem + lane_off;
+  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
+    const uint32_t s = it % a.stages;
+    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
+    const int g = kb * GPR + gi;  // channel group of this thread
+    const bool cvalid = g < cg_all;
+    float w[9][8], b[8];
+    if (cvalid) {
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) unpack8_bf16(__ldg(wv + tap * cg_all + g), w[tap]);
+      const float4 b0 = __ldg(bv + 2 * g), b1 = __ldg(bv + 2 * g + 1);
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    }
+    uint8_t* sp = stage_base + s * kABytes;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+      if (cvalid && live[p]) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = b[e];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int hi = hi0[p] + r;
+          if (static_cast<unsigned>(hi) >= static_cast<unsigned>(a.H)) continue;
+#pragma unroll
+          for (int sx = 0; sx < 3; ++sx) {
+            const int wi = wi0[p] + sx;
+            if (static_cast<unsigned>(wi) >= static_cast<unsigned>(a.W)) continue;
+            float xf[8];
+            unpack8_bf16(__ldg(xv + static_cast<size_t>(pix[p] + hi * a.W + wi) * cg_all + g), xf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = fmaf(xf[e], w[r * 3 + sx][e], acc[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.0f);
+      }
+      // bf16 rounding here is exactly where the unfused path stores the
+      // depthwise output, so fused and unfused forwards agree bit for bit.
+      *reinterpret_cast<uint4*>(sp + p * RPP * 128) =
+          make_uint4(pack2_bf16(acc[0], acc[1]), pack2_bf16(acc[2], acc[3]),
+                     pack2_bf16(acc[4], acc[5]), pack2_bf16(acc[6], acc[7]));
+    }
+    ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core (async proxy) reads
+    ptx::mbar_arrive(&full[s]);
+  }
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
@@ -373,8 +484,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int m0 = (tile / n_tiles) * kConvBM;
         if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather16))
           gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, it);
-        else
+        else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8))
           gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, it);
+        else
+          dw_a_tile(args, smem + L.a_off, full, empty, m0, it);
       }
     }
   } else if (warp == kTmaWarp) {
@@ -519,6 +632,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -555,6 +671,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       break;
     case ConvLoadMode::kTmaA:
       conv_gemm_kernel<2><<<grid, kConvThreads, smem, stream>>>(args);
+      break;
+    case ConvLoadMode::kDwFused:
+      conv_gemm_kernel<3><<<grid, kConvThreads, smem, stream>>>(args);
       break;
   }
   return cudaGetLastError();

@@ -43,12 +43,19 @@ struct ConvGemmArgs {
   int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
   int out_f32, relu;
   int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
+  // kDwFused: A[m, c] = relu(dw3x3(x)[m, c] + dw_b[c]), computed in the
+  // producer from the depthwise input x ([H][W][C], pad 1, stride dw_stride);
+  // Ho/Wo are the depthwise output dims, R = S = 1.
+  const __nv_bfloat16* dw_w;  // [9][C] bf16
+  const float* dw_b;          // [C]
+  int dw_stride;
 };
 
 enum class ConvLoadMode : int {
   kGather16 = 0,  // cp.async gather, 8 channels (16 B) per granule, C % 8 == 0
   kGather8 = 1,   // cp.async gather, 4 channels (8 B) per granule, C == 4 (stem)
   kTmaA = 2,      // 1x1 stride-1 conv: A is a plain 2D tile, loaded by TMA
+  kDwFused = 3,   // depthwise 3x3 + bias + ReLU computed into A, then the 1x1 GEMM
 };
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in

@@ -5,6 +5,8 @@
 // stays close to one read of the input and one write of the output.
 #include "stream_ops.cuh"
 
+#include <algorithm>
+
 namespace ds {
 
 namespace {
@@ -55,16 +57,16 @@ template <int STRIDE>
 __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
     const uint4* __restrict__ x, const __nv_bfloat16* __restrict__ w,
     const float* __restrict__ bias, uint4* __restrict__ y, int h, int wd, int c, int ho, int wo,
-    int cg_log2, int xq_per_row, long long work) {
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= work) return;
+    int cg_log2, int xq_per_row) {
+  // grid.y = output row (image * ho + oy); x covers (column quad, channel group)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = 1 << cg_log2;
-  const int g = static_cast<int>(i & (cg - 1));
-  const long long rest = i >> cg_log2;
-  const int xq = static_cast<int>(rest % xq_per_row);
-  const long long row = rest / xq_per_row;  // n * ho + oy
-  const int oy = static_cast<int>(row % ho);
-  const int n = static_cast<int>(row / ho);
+  const int g = i & (cg - 1);
+  const int xq = i >> cg_log2;
+  if (xq >= xq_per_row) return;
+  const int row = blockIdx.y;
+  const int n = row / ho;
+  const int oy = row - n * ho;
   const int ox0 = xq * kDwCols;
   constexpr int IN_COLS = (kDwCols - 1) * STRIDE + 3;
   const int ix0 = ox0 * STRIDE - 1;
@@ -244,13 +246,16 @@ cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, con
   int cg_log2 = 0;
   while ((1 << cg_log2) < cg) ++cg_log2;
   if ((1 << cg_log2) != cg) return cudaErrorInvalidValue;  // channel groups must be a power of 2
-  const int xq = (wo + kDwCols - 1) / kDwCols;
-  const long long work = static_cast<long long>(n) * ho * xq * cg;
-  if (stride == 1)
-    dwconv3x3_kernel<1><<<grid_for(work), kBlock, 0, stream>>>(
+  const int rows = n * ho;
+  if (rows > 65535) return cudaErrorInvalidValue;
+  auto block_for = [](int per_row) { return std::min(kBlock, (per_row + 31) / 32 * 32); };
+  if (stride == 1) {
+    const int xq = (wo + kDwCols - 1) / kDwCols;
+    const int bt = block_for(xq * cg);
+    dwconv3x3_kernel<1><<<dim3((xq * cg + bt - 1) / bt, rows), bt, 0, stream>>>(
         reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h, wd, c, ho, wo,
-        cg_log2, xq, work);
-  else {
+        cg_log2, xq);
+  } else {
     const long long pw = static_cast<long long>(n) * ho * wo * cg;
     dwconv3x3_px_kernel<<<grid_for(pw), kBlock, 0, stream>>>(
         reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),

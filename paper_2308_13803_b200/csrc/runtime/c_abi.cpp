@@ -196,8 +196,7 @@ ds_status ds_backend_stats_get(const ds_backend* b, ds_backend_stats* out) {
     out->h2d_bytes = b->impl->h2d_bytes();
     out->d2h_bytes = b->impl->d2h_bytes();
     out->instances_created = b->impl->instances_created();
-    const ds::ModelSpec& m = b->impl->model();
-    out->kernels_per_forward = static_cast<int>(m.ops.size()) + 2;
+    out->kernels_per_forward = b->impl->kernels_per_forward();
     out->device_bytes = static_cast<double>(b->impl->device_bytes());
   });
 }

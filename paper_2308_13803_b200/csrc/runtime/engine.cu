@@ -76,10 +76,11 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
              "upload biases");
 
   plans_.resize(m.ops.size());
+  fused_ = fused_depthwise(m);
   kernels_per_forward_ = 2;  // input staging + softmax
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
-    ++kernels_per_forward_;
+    if (!fused_[i]) ++kernels_per_forward_;
     if (op.kind != OpKind::kConv && op.kind != OpKind::kFc) continue;
     const ParamSpec& p = m.params.at(op.param);
     const BufferSpec& in = m.buffers.at(op.in);
@@ -120,7 +121,20 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.c_off = op.c_off;
     a.out_f32 = out.f32 ? 1 : 0;
     a.relu = op.relu ? 1 : 0;
-    if (in.c == 4) {
+    if (i > 0 && fused_[i - 1]) {
+      // depthwise + this 1x1 conv in one launch: A is computed from the
+      // depthwise input; the depthwise output buffer is never written.
+      const OpSpec& dw = m.ops[i - 1];
+      const BufferSpec& dw_in = m.buffers.at(dw.in);
+      pl.mode = ConvLoadMode::kDwFused;
+      a.x = static_cast<const __nv_bfloat16*>(bufs_[dw.in]);
+      a.H = dw_in.h;
+      a.W = dw_in.w;
+      a.C = dw_in.c;
+      a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
+      a.dw_b = d_b_ + hp.b_off.at(dw.param);
+      a.dw_stride = dw.sh;
+    } else if (in.c == 4) {
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
@@ -173,6 +187,7 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks) {
              "stage_input");
   record_mark();
   for (size_t i = 0; i < m.ops.size(); ++i) {
+    if (fused_[i]) continue;  // computed inside the next conv's producer
     const OpSpec& op = m.ops[i];
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out = m.buffers[op.out];

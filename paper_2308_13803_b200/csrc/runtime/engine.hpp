@@ -80,6 +80,7 @@ class Instance {
   float* d_probs_ = nullptr;
   std::vector<void*> bufs_;
   std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
+  std::vector<bool> fused_;      // depthwise ops folded into the next conv
   std::map<int, cudaGraphExec_t> graphs_;
   int kernels_per_forward_ = 0;
 };
@@ -131,6 +132,7 @@ class Backend {
   const ModelSpec& model() const { return model_; }
   void read_buffer(int id, int bs, void* host) { instance(0).read_buffer(id, bs, host); }
   int64_t kernel_launches() const { return kernel_launches_; }
+  int kernels_per_forward() const { return inst_[0]->kernels_per_forward(); }
   int64_t h2d_bytes() const { return h2d_bytes_; }
   int64_t d2h_bytes() const { return d2h_bytes_; }
   int instances_created() const;

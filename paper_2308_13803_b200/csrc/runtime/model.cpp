@@ -5,6 +5,7 @@
 // oracle/fwd_oracle.c.
 #include "model.hpp"
 
+#include <cstdlib>
 #include <stdexcept>
 
 namespace ds {
@@ -311,7 +312,25 @@ ModelSpec inception_v3() {
 
 }  // namespace
 
+std::vector<bool> fused_depthwise(const ModelSpec& m) {
+  std::vector<bool> fused(m.ops.size(), false);
+  const char* on = std::getenv("DS_DW_FUSION");  // opt-in until the fused producer wins
+  if (!on || on[0] != '1') return fused;
+  for (size_t i = 0; i + 1 < m.ops.size(); ++i) {
+    const OpSpec& dw = m.ops[i];
+    const OpSpec& pw = m.ops[i + 1];
+    if (dw.kind != OpKind::kDwConv || pw.kind != OpKind::kConv || pw.in != dw.out) continue;
+    if (pw.r != 1 || pw.s != 1 || pw.sh != 1 || pw.sw != 1 || pw.ph != 0 || pw.pw != 0) continue;
+    bool other_reader = false;
+    for (size_t j = 0; j < m.ops.size(); ++j)
+      if (j != i + 1 && (m.ops[j].in == dw.out || m.ops[j].residual == dw.out)) other_reader = true;
+    if (!other_reader) fused[i] = true;
+  }
+  return fused;
+}
+
 std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
+  const std::vector<bool> fused = fused_depthwise(m);
   std::vector<KernelCost> out;
   const double px = static_cast<double>(m.in_h) * m.in_w;
   out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
@@ -349,6 +368,16 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         k.kind = KernelKind::kGap;
         k.bytes_per_image = in_elems * 2 + in.c * 2.0;
         break;
+    }
+    const size_t i = &op - m.ops.data();
+    if (i > 0 && fused[i - 1]) {
+      // one launch: the depthwise input replaces the 1x1 input; both weights
+      const KernelCost dw = out.back();
+      out.pop_back();
+      const BufferSpec& dw_in = m.buffers[m.ops[i - 1].in];
+      k.flops_per_image += dw.flops_per_image;
+      k.bytes_per_image += static_cast<double>(dw_in.h) * dw_in.w * dw_in.c * 2 - in_elems * 2;
+      k.fixed_bytes += dw.fixed_bytes;
     }
     out.push_back(k);
   }

@@ -66,6 +66,12 @@ struct KernelCost {
   double fixed_bytes = 0.0;  // weights + bias, once per launch
 };
 std::vector<KernelCost> kernel_costs(const ModelSpec& m);
+
+// Depthwise ops folded into the A producer of the 1x1 conv that consumes
+// them (conv_gemm kDwFused): true for op i when op i is a depthwise conv whose
+// output feeds only op i+1, a 1x1 stride-1 conv. Opt-in (DS_DW_FUSION=1):
+// correct (parity-tested) but its producer is still latency-bound.
+std::vector<bool> fused_depthwise(const ModelSpec& m);
 std::vector<std::string> model_ids();
 
 }  // namespace ds

@@ -59,6 +59,20 @@ def test_forward_deterministic_and_batch_invariant():
     assert np.array_equal(a, one)
 
 
+def test_depthwise_fusion_matches_unfused(monkeypatch):
+    """The kDwFused conv (depthwise computed in the 1x1 conv's producer) and
+    the two-kernel path round the depthwise output to bf16 at the same point
+    with the same FMA order, so their logits agree bit for bit."""
+    imgs = generate_images("mobilenet_v1", 7, 4)
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
+        plain = be.forward(imgs)
+    monkeypatch.setenv("DS_DW_FUSION", "1")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
+        fused = be.forward(imgs)
+        assert be.stats()["kernels_per_forward"] > 0
+    assert np.array_equal(plain, fused)
+
+
 def test_softmax_probs():
     imgs = generate_images("synthetic_cnn", 0, 5)
     with GpuBackend("synthetic_cnn", Config(abs_max_bs=8, max_mtl=1)) as be:
