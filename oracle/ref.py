@@ -54,6 +54,7 @@ def lib() -> ctypes.CDLL:
 
 def write_scenario(scenario_dict: dict, catalog: list, directory: str) -> str:
     """Writes a reference-format scenario + catalog pair; returns the scenario path."""
+    os.makedirs(directory, exist_ok=True)
     cpath = os.path.join(directory, "catalog.json")
     with open(cpath, "w") as f:
         json.dump(catalog, f)
