@@ -80,21 +80,35 @@ __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[q][e] = bv[e];
   const uint4* wv = reinterpret_cast<const uint4*>(w);
+  // All weight vectors, then each stencil row's input vectors, are issued
+  // before first use so several loads are in flight per thread (the loop was
+  // latency-bound on load -> use). Taps outside the image are skipped, not
+  // multiplied by zero, to keep the FMA sequence of the fused path.
+  uint4 wraw[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) wraw[t] = __ldg(wv + t * cg + g);
 
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const int iy = oy * STRIDE - 1 + r;
-    if (iy < 0 || iy >= h) continue;
-    const uint4* xrow = x + (static_cast<long long>(n) * h + iy) * wd * cg + g;
-    float wr[3][8];
-#pragma unroll
-    for (int s = 0; s < 3; ++s) unpack8(__ldg(wv + (r * 3 + s) * cg + g), wr[s]);
+    const bool row_ok = iy >= 0 && iy < h;
+    const uint4* xrow = x + (static_cast<long long>(n) * h + (row_ok ? iy : 0)) * wd * cg + g;
+    uint4 raw[IN_COLS];
+    bool ok[IN_COLS];
 #pragma unroll
     for (int col = 0; col < IN_COLS; ++col) {
       const int ix = ix0 + col;
-      if (ix < 0 || ix >= wd) continue;
+      ok[col] = row_ok && ix >= 0 && ix < wd;
+      raw[col] = ok[col] ? __ldg(xrow + static_cast<long long>(ix) * cg) : make_uint4(0, 0, 0, 0);
+    }
+    float wr[3][8];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) unpack8(wraw[r * 3 + s], wr[s]);
+#pragma unroll
+    for (int col = 0; col < IN_COLS; ++col) {
+      if (!ok[col]) continue;
       float xv[8];
-      unpack8(__ldg(xrow + static_cast<long long>(ix) * cg), xv);
+      unpack8(raw[col], xv);
 #pragma unroll
       for (int q = 0; q < kDwCols; ++q) {
         const int s = col - q * STRIDE;  // tap of output q that reads this column
