@@ -70,6 +70,12 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint
 bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
                      uint64_t row_stride_elems, bool f32);
 
+// NHWC bf16 activation as a 4-D map {C, W, H, N} with a {box_c, box_w,
+// box_h, 1} box, no swizzle (used by the depthwise halo loads). Negative or
+// past-the-edge box coordinates read zeros (the convolution's padding).
+bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
+                      int box_w, int box_h);
+
 size_t conv_gemm_smem_bytes(int BN, int stages, int cout);
 
 // Operand-ring depth for an N tile: as deep as kConvMaxStages allows within

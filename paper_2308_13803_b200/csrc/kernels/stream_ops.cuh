@@ -3,6 +3,7 @@
 // per thread per access, fp32 math inside, bf16 rounding on store.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -18,6 +19,16 @@ cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, in
 cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
                              __nv_bfloat16* y, int n, int h, int wd, int c, int stride,
                              cudaStream_t stream);
+
+// Depthwise 3x3 streamed by TMA halo boxes (dwconv_tma.cu); C must be a
+// power of two >= 8. The input map comes from dwconv_tma_input_map over the
+// (max-batch) input buffer.
+bool dwconv_tma_supported(int c);
+bool dwconv_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w, int c,
+                          int stride);
+cudaError_t launch_dwconv3x3_tma(const CUtensorMap& in_map, const __nv_bfloat16* w,
+                                 const float* bias, __nv_bfloat16* y, int n, int h, int wd, int c,
+                                 int stride, cudaStream_t stream);
 
 // 3x3 max pool (stride, pad) or 3x3 average pool (count_include_pad, /9).
 // Output may be a channel slice of a wider buffer (ldo channels, c_off).

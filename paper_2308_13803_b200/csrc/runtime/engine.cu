@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "../kernels/stream_ops.cuh"
@@ -81,6 +82,18 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
     if (!fused_[i]) ++kernels_per_forward_;
+    if (op.kind == OpKind::kDwConv && !fused_[i]) {
+      const BufferSpec& din = m.buffers.at(op.in);
+      dw_maps_.resize(m.ops.size());
+      dw_tma_.resize(m.ops.size(), false);
+      const char* legacy = std::getenv("DS_DW_LEGACY");
+      // TMA halo tiles pay from 14-wide outputs up; the 7x7 tail keeps the
+      // register-blocked kernel (a 16x16 tile would be mostly empty).
+      const int dout_w = m.buffers.at(op.out).w;
+      dw_tma_[i] = !(legacy && legacy[0] == '1') && dout_w >= 14 && dwconv_tma_supported(din.c) &&
+                   dwconv_tma_input_map(&dw_maps_[i], bufs_[op.in], max_bs, din.h, din.w, din.c,
+                                        op.sh);
+    }
     if (op.kind != OpKind::kConv && op.kind != OpKind::kFc) continue;
     const ParamSpec& p = m.params.at(op.param);
     const BufferSpec& in = m.buffers.at(op.in);
@@ -204,8 +217,12 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks) {
       }
       case OpKind::kDwConv: {
         const auto* w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off[op.param]);
-        e = launch_dwconv3x3(x, w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c, op.sh,
-                             stream_);
+        if (i < dw_tma_.size() && dw_tma_[i])
+          e = launch_dwconv3x3_tma(dw_maps_[i], w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w,
+                                   in.c, op.sh, stream_);
+        else
+          e = launch_dwconv3x3(x, w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c, op.sh,
+                               stream_);
         break;
       }
       case OpKind::kMaxPool:

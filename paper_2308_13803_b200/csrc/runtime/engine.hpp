@@ -81,6 +81,8 @@ class Instance {
   std::vector<void*> bufs_;
   std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
   std::vector<bool> fused_;      // depthwise ops folded into the next conv
+  std::vector<CUtensorMap> dw_maps_;  // TMA halo maps of depthwise inputs (by op)
+  std::vector<bool> dw_tma_;          // depthwise op uses the TMA kernel
   std::map<int, cudaGraphExec_t> graphs_;
   int kernels_per_forward_ = 0;
 };
