@@ -54,6 +54,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   const size_t w_off = take(hp.w.size() * sizeof(uint16_t));
   const size_t b_off = take(hp.b.size() * sizeof(float));
   const size_t img_off = take(static_cast<size_t>(max_bs) * m.in_h * m.in_w * 3);
+  const size_t img2_off = take(static_cast<size_t>(max_bs) * m.in_h * m.in_w * 3);
   std::vector<size_t> buf_off;
   for (const auto& b : m.buffers)
     buf_off.push_back(
@@ -65,7 +66,13 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   check_cuda(cudaMemsetAsync(d_arena_, 0, off, stream_), "cudaMemset");
   d_w_ = reinterpret_cast<uint16_t*>(base + w_off);
   d_b_ = reinterpret_cast<float*>(base + b_off);
-  d_images_ = base + img_off;
+  d_images_[0] = base + img_off;
+  d_images_[1] = base + img2_off;
+  check_cuda(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (int s = 0; s < 2; ++s) {
+    check_cuda(cudaEventCreateWithFlags(&slot_free_[s], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreateWithFlags(&h2d_done_[s], cudaEventDisableTiming), "event");
+  }
   for (size_t o : buf_off) bufs_.push_back(base + o);
   d_probs_ = reinterpret_cast<float*>(base + probs_off);
   d_logits_ = static_cast<float*>(bufs_.at(m.logits));
@@ -181,11 +188,17 @@ Instance::~Instance() {
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+  if (copy_stream_) cudaStreamSynchronize(copy_stream_);
   if (d_arena_) cudaFree(d_arena_);
+  for (int s = 0; s < 2; ++s) {
+    if (slot_free_[s]) cudaEventDestroy(slot_free_[s]);
+    if (h2d_done_[s]) cudaEventDestroy(h2d_done_[s]);
+  }
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
-void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks) {
+void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int slot) {
   const ModelSpec& m = m_;
   const HostParams& hp = params_for(m);
   size_t mark = 0;
@@ -195,7 +208,7 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks) {
                  "mark");
   };
   record_mark();
-  check_cuda(launch_stage_input(d_images_, static_cast<__nv_bfloat16*>(bufs_[0]), bs, m.in_h,
+  check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs, m.in_h,
                                 m.in_w, stream_),
              "stage_input");
   record_mark();
@@ -289,14 +302,15 @@ void Instance::read_buffer(int id, int bs, void* host) const {
   check_cuda(cudaMemcpy(host, bufs_.at(id), bytes, cudaMemcpyDeviceToHost), "read_buffer");
 }
 
-void Instance::enqueue_forward(int bs) {
+void Instance::enqueue_forward(int bs, int slot) {
   if (bs < 1 || bs > max_bs_) throw std::invalid_argument("invalid batch size");
-  auto it = graphs_.find(bs);
+  const int key = bs * 2 + slot;
+  auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
     check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
     try {
-      enqueue_layers(bs);
+      enqueue_layers(bs, nullptr, slot);
     } catch (...) {
       cudaStreamEndCapture(stream_, &g);
       if (g) cudaGraphDestroy(g);
@@ -306,7 +320,7 @@ void Instance::enqueue_forward(int bs) {
     cudaGraphExec_t exec = nullptr;
     check_cuda(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
     cudaGraphDestroy(g);
-    it = graphs_.emplace(bs, exec).first;
+    it = graphs_.emplace(key, exec).first;
   }
   check_cuda(cudaGraphLaunch(it->second, stream_), "graph launch");
 }
@@ -326,6 +340,7 @@ Backend::Backend(const std::string& model_id, BackendConfig cfg, uint64_t seed, 
   inst_.resize(cfg_.max_mtl);
   inflight_.resize(cfg_.max_mtl);
   io_cursor_.assign(cfg_.max_mtl, 0);
+  io_seq_.assign(cfg_.max_mtl, 0);
   pinned_logits_.assign(cfg_.max_mtl, nullptr);
   instance(0);
 }
@@ -389,25 +404,36 @@ void Backend::enqueue_request(int i, int bs) {
   Instance& I = instance(i);
   Inflight f{take_event(), take_event(), bs};
   cudaStream_t s = I.stream();
-  check_cuda(cudaEventRecord(f.start, s), "event record");
   const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
-  if (host_io_) {
+  if (!host_io_) {
+    check_cuda(cudaEventRecord(f.start, s), "event record");
+    I.enqueue_forward(bs);
+  } else {
+    // End to end: the request's images cross PCIe on the instance's copy
+    // stream into one of two input slots (so the next request's copy runs
+    // under this forward); the timed span starts before the copy and ends
+    // after the logits are back in pinned host memory.
+    const int slot = static_cast<int>(io_seq_[i]++ & 1);
     int64_t& cur = io_cursor_[i];
     if (cur + bs > pool_images_) cur = 0;
     const uint8_t* src = pinned_images_ + img_bytes * static_cast<size_t>(cur);
     cur = (i == 0) ? cur + bs : (cur + cfg_.max_mtl) % pool_images_;
-    check_cuda(cudaMemcpyAsync(I.images(), src, img_bytes * bs, cudaMemcpyHostToDevice, s),
+    cudaStream_t cs = I.copy_stream();
+    check_cuda(cudaStreamWaitEvent(cs, I.slot_free(slot), 0), "wait slot");
+    check_cuda(cudaEventRecord(f.start, cs), "event record");
+    check_cuda(cudaMemcpyAsync(I.images(slot), src, img_bytes * bs, cudaMemcpyHostToDevice, cs),
                "H2D images");
+    check_cuda(cudaEventRecord(I.h2d_done(slot), cs), "event record");
     h2d_bytes_ += static_cast<int64_t>(img_bytes) * bs;
-  }
-  I.enqueue_forward(bs);
-  kernel_launches_ += I.kernels_per_forward();
-  if (host_io_) {
+    check_cuda(cudaStreamWaitEvent(s, I.h2d_done(slot), 0), "wait h2d");
+    I.enqueue_forward(bs, slot);
+    check_cuda(cudaEventRecord(I.slot_free(slot), s), "event record");
     const size_t lb = static_cast<size_t>(bs) * model_.classes * sizeof(float);
     check_cuda(cudaMemcpyAsync(pinned_logits_[i], I.logits(), lb, cudaMemcpyDeviceToHost, s),
                "D2H logits");
     d2h_bytes_ += static_cast<int64_t>(lb);
   }
+  kernel_launches_ += I.kernels_per_forward();
   check_cuda(cudaEventRecord(f.end, s), "event record");
   inflight_[i].push_back(f);
 }

@@ -41,12 +41,14 @@ class Instance {
   Instance(const Instance&) = delete;
   Instance& operator=(const Instance&) = delete;
 
-  // Enqueues one forward over the first bs images of images() (graph per bs).
-  void enqueue_forward(int bs);
+  // Enqueues one forward over the first bs images of input slot `slot`
+  // (graph per (bs, slot)). Two slots let the next request's H2D copy (on
+  // copy_stream()) overlap the current forward.
+  void enqueue_forward(int bs, int slot = 0);
   // Same sequence without a graph (used for capture and first launch). When
   // `marks` is given (kernels_per_forward()+1 events), an externally visible
   // event is recorded before the first and after every kernel.
-  void enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks = nullptr);
+  void enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks = nullptr, int slot = 0);
   // Device time of every kernel of one forward (staging, ops..., softmax),
   // averaged over `reps` launches of a graph with event nodes between kernels.
   std::vector<double> profile_kernels(int bs, int reps);
@@ -54,7 +56,10 @@ class Instance {
   cudaStream_t stream() const { return stream_; }
   // Debug: copies activation buffer `id` (first bs images) to host, raw bytes.
   void read_buffer(int id, int bs, void* host) const;
-  uint8_t* images() const { return d_images_; }
+  uint8_t* images(int slot = 0) const { return d_images_[slot]; }
+  cudaStream_t copy_stream() const { return copy_stream_; }
+  cudaEvent_t slot_free(int slot) const { return slot_free_[slot]; }
+  cudaEvent_t h2d_done(int slot) const { return h2d_done_[slot]; }
   float* logits() const { return d_logits_; }
   float* probs() const { return d_probs_; }
   int max_bs() const { return max_bs_; }
@@ -75,7 +80,10 @@ class Instance {
   size_t device_bytes_ = 0;
   uint16_t* d_w_ = nullptr;
   float* d_b_ = nullptr;
-  uint8_t* d_images_ = nullptr;
+  uint8_t* d_images_[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream_ = nullptr;
+  cudaEvent_t slot_free_[2] = {nullptr, nullptr};  // forward done reading a slot
+  cudaEvent_t h2d_done_[2] = {nullptr, nullptr};   // a slot's images have landed
   float* d_logits_ = nullptr;
   float* d_probs_ = nullptr;
   std::vector<void*> bufs_;
@@ -163,6 +171,7 @@ class Backend {
   uint8_t* pinned_images_ = nullptr;  // pinned copy for host-I/O mode
   std::vector<float*> pinned_logits_;
   std::vector<int64_t> io_cursor_;
+  std::vector<uint64_t> io_seq_;  // per-instance request count (input slot parity)
   int pool_images_ = 0;
   bool host_io_ = false;
   int batch_bs_ = 0;  // bs of batches in flight on instance 0 (0: none)
