@@ -43,26 +43,33 @@ constexpr int kABytes = kConvBM * kConvBK * 2;  // 16 KiB per stage
 constexpr int kYStageBytes = 32 * 128;
 
 // Warp roles (kConvThreads = 18 warps).
-constexpr int kEpiWarps = 8;      // warps 0-7: epilogue, two per TMEM lane quarter
+constexpr int kEpiWarps = 8;      // warps 0-7: epilogue (two teams of four)
+constexpr int kMaxEpiWarps = 16;  // TMA-A mode: the idle gather warps join (four teams)
+constexpr int kMaxAcc = 8;        // TMEM accumulators (tmem_full/tmem_empty barrier pairs)
 constexpr int kGatherWarp0 = 8;   // warps 8-15: A gather
 constexpr int kGatherWarps = 8;
 constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
 constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
 
 struct SmemLayout {
-  uint32_t a_off, b_off, y_off, bar_off, bias_off, total;
+  uint32_t a_off, b_off, y_off, bar_off, bias_off, patch_off, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout) {
+// kStemU8: per producer group, one normalised input patch (bf16 [rows][W][4]).
+constexpr int kStemPatchBytes = 20 * 1024;
+
+__host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
+                                                  int patch_bytes = 0) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * kABytes;
   L.y_off = L.b_off + static_cast<uint32_t>(stages) * BN * 128;
-  L.bar_off = L.y_off + kEpiWarps * 2 * kYStageBytes;
-  // full[stages], empty[stages], tmem_full[2], tmem_empty[2], tmem slot
-  L.bias_off = L.bar_off + ((2 * stages + 5) * 8 + 15) / 16 * 16;
+  L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
+  // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], tmem slot
+  L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 1) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
-  L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
+  L.patch_off = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
+  L.total = L.patch_off + static_cast<uint32_t>(patch_bytes);
   return L;
 }
 
@@ -254,6 +261,163 @@ __device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, 
   }
 }
 
+// Stem producer (kStemU8): the stem conv reads the u8 images [n][H][W][3]
+// directly, so the staged bf16 input tensor is never materialised. The eight
+// gather warps form two groups of four that take alternate tiles (two tiles
+// in flight); per tile a group
+//   1. stages the input rows the tile's 128 output pixels touch (one
+//      contiguous range of flattened image rows n*H+h) into its smem patch as
+//      normalised bf16 [row][W][4] (channel 3 zero) — coalesced byte loads;
+//   2. builds every K block of A from the patch like the bf16 gather: a
+//      thread owns one 16 B granule (two taps x 4 channels) of 8 rows, two
+//      8 B patch reads per granule, zeros for padding and the K tail.
+//
+// Normalisation: the staging kernel stores bf16_rn((p - 127.5f) / 63.75f).
+// Here it is bf16_rn((p - 127.5f) * (1 / 63.75f)): the fp32 values differ for
+// some p, but after bf16 rounding the two agree for all 256 byte values
+// (checked exhaustively, tests/test_oracle.py::test_stem_normalisation_exact).
+constexpr int kStemGroupThreads = kGatherWarps * 32 / 2;
+
+// u8 -> fp32 without the conversion pipe: the float with bits 0x4B000000 | p
+// is 2^23 + p exactly, so subtracting 2^23 gives p exactly.
+__device__ __forceinline__ float u8_to_f32(uint32_t p) {
+  return __fsub_rn(__uint_as_float(0x4B000000u | p), 8388608.0f);
+}
+
+__device__ __forceinline__ uint32_t stem_norm2(uint32_t p0, uint32_t p1) {
+  const float r = 1.0f / 63.75f;
+  const float v0 = __fmul_rn(__fsub_rn(u8_to_f32(p0), 127.5f), r);
+  const float v1 = __fmul_rn(__fsub_rn(u8_to_f32(p1), 127.5f), r);
+  return pack2_bf16(v0, v1);
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Flattened input-row range [g_lo, g_hi) (g = n*H + h) the output pixels
+// m0 .. m0+127 read.
+__device__ __forceinline__ void stem_rows(const ConvGemmArgs& a, int m0, int& g_lo, int& g_hi) {
+  const int HoWo = a.Ho * a.Wo;
+  const int m1 = min(m0 + kConvBM, a.M) - 1;
+  const int n0 = m0 / HoWo, n1 = m1 / HoWo;
+  g_lo = n0 * a.H + max(0, ((m0 - n0 * HoWo) / a.Wo) * a.stride_h - a.pad_h);
+  g_hi = n1 * a.H + min(a.H, ((m1 - n1 * HoWo) / a.Wo) * a.stride_h - a.pad_h + a.R);
+}
+
+// L2 prefetch of a tile's image rows, issued a few tiles ahead because every
+// tile of a persistent CTA touches rows no other tile of it did.
+__device__ __forceinline__ void stem_prefetch(const ConvGemmArgs& a, int m0) {
+  if (m0 >= a.M) return;
+  int g_lo, g_hi;
+  stem_rows(a, m0, g_lo, g_hi);
+  const size_t lo = static_cast<size_t>(g_lo) * a.W * 3, hi = static_cast<size_t>(g_hi) * a.W * 3;
+  if (hi <= lo) return;
+  const size_t lo16 = lo & ~static_cast<size_t>(15);
+  const size_t bytes = min(static_cast<size_t>(1 << 16), (hi - lo16 + 15) & ~static_cast<size_t>(15));
+  ptx::bulk_prefetch_l2(a.img + lo16, static_cast<uint32_t>(bytes));
+}
+
+__device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint8_t* smem, uint2* patch_ptr,
+                                            uint64_t* full, uint64_t* empty, int m0, uint32_t it,
+                                            int tg, int bar_id) {
+  const uint32_t patch = ptx::smem_u32(patch_ptr);
+  // 1. stage the patch
+  int g_lo, g_hi;
+  stem_rows(a, m0, g_lo, g_hi);
+  const int npx = (g_hi - g_lo) * a.W;
+  if (npx * 8 > kStemPatchBytes) __trap();  // the host checks every tile (conv_gemm_stem_fits)
+  named_bar_sync(bar_id, kStemGroupThreads);  // the previous tile's build is done with the patch
+  {
+    // batches of U pixels per thread: all 3U byte loads are issued before the
+    // first conversion, so a tile's patch costs about one memory round trip
+    constexpr int U = 10;
+    const uint8_t* src = a.img + static_cast<size_t>(g_lo) * a.W * 3;
+    for (int p0 = tg; p0 < npx; p0 += U * kStemGroupThreads) {
+      uint32_t b[U][3];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + u * kStemGroupThreads;
+        const uint8_t* q = src + static_cast<size_t>(p < npx ? p : 0) * 3;
+        b[u][0] = __ldg(q);
+        b[u][1] = __ldg(q + 1);
+        b[u][2] = __ldg(q + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + u * kStemGroupThreads;
+        if (p < npx)
+          ptx::sts64(patch + p * 8,
+                     make_uint2(stem_norm2(b[u][0], b[u][1]), stem_norm2(b[u][2], 0u) & 0xFFFFu));
+      }
+    }
+  }
+  named_bar_sync(bar_id, kStemGroupThreads);  // patch complete
+
+  // 2. build A, one K block per pipeline stage
+  constexpr int GPR = 8;                        // 16 B granules per 128 B row
+  constexpr int RPP = kStemGroupThreads / GPR;  // 16 rows per pass
+  constexpr int PASSES = kConvBM / RPP;         // 8
+  const int gi = tg % GPR;
+  const int r0 = tg / GPR;
+  // per pass: input row/column of tap (0, 0) (may be padding) and its patch index
+  int hi0[PASSES], wi0[PASSES], pbase[PASSES];
+  {
+    const int HoWo = a.Ho * a.Wo;
+    const int m_first = m0 + r0;
+    int n = m_first / HoWo;
+    const int rem = m_first - n * HoWo;
+    int ho = rem / a.Wo;
+    int wo = rem - ho * a.Wo;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      const bool live = m_first + p * RPP < a.M;
+      hi0[p] = live ? ho * a.stride_h - a.pad_h : -(1 << 28);  // dead rows read zeros
+      wi0[p] = wo * a.stride_w - a.pad_w;
+      pbase[p] = (n * a.H + ho * a.stride_h - a.pad_h - g_lo) * a.W + wi0[p];
+      wo += RPP;
+      while (wo >= a.Wo) {
+        wo -= a.Wo;
+        if (++ho == a.Ho) {
+          ho = 0;
+          ++n;
+        }
+      }
+    }
+  }
+  const uint32_t lane_off =
+      static_cast<uint32_t>(r0) * 128 + (static_cast<uint32_t>(gi ^ (r0 & 7)) << 4);
+  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
+    const uint32_t s = it % a.stages;
+    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
+    int dr[2], dc[2], doff[2];
+    bool tv[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int tap = kb * 16 + gi * 2 + e;
+      tv[e] = tap < a.taps;
+      dr[e] = tap / a.S;
+      dc[e] = tap - dr[e] * a.S;
+      doff[e] = dr[e] * a.W + dc[e];
+    }
+    const uint32_t sp = ptx::smem_u32(smem) + s * kABytes + lane_off;
+#pragma unroll
+    for (int p = 0; p < PASSES; ++p) {
+      uint2 v[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool ok = tv[e] &&
+                        static_cast<unsigned>(hi0[p] + dr[e]) < static_cast<unsigned>(a.H) &&
+                        static_cast<unsigned>(wi0[p] + dc[e]) < static_cast<unsigned>(a.W);
+        v[e] = ok ? ptx::lds64(patch + (pbase[p] + doff[e]) * 8) : make_uint2(0u, 0u);
+      }
+      ptx::sts128(sp + p * RPP * 128, make_uint4(v[0].x, v[0].y, v[1].x, v[1].y));
+    }
+    ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core (async proxy) reads
+    ptx::mbar_arrive(&full[s]);
+  }
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
@@ -334,8 +498,15 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
                                                    int n, const uint32_t (&raw)[32], uint8_t* group,
                                                    int col, int lane) {
   float v[32];
+  const float4* b4 = reinterpret_cast<const float4*>(bias_s + n);  // n % 32 == 0
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) + bias_s[n + j];
+  for (int q = 0; q < 8; ++q) {
+    const float4 b = b4[q];
+    v[4 * q + 0] = __uint_as_float(raw[4 * q + 0]) + b.x;
+    v[4 * q + 1] = __uint_as_float(raw[4 * q + 1]) + b.y;
+    v[4 * q + 2] = __uint_as_float(raw[4 * q + 2]) + b.z;
+    v[4 * q + 3] = __uint_as_float(raw[4 * q + 3]) + b.w;
+  }
   if (a.residual && m < a.M) {
     const __nv_bfloat16* rrow = a.residual + static_cast<size_t>(m) * a.ld_res + n;
     if (n + 32 <= a.Cout) {
@@ -381,9 +552,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout);
+  // (offsetting smem_raw, rather than masking the generic address, keeps the
+  // pointer in the shared window so accesses through it compile to LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int epi_warps = 4 * args.teams;
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps,
+                                   MODE == static_cast<int>(ConvLoadMode::kStemU8) ? 2 * kStemPatchBytes : 0);
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x)
@@ -391,25 +565,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + args.stages;
-  uint64_t* tmem_full = empty + args.stages;  // [2]
-  uint64_t* tmem_empty = tmem_full + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* tmem_full = empty + args.stages;  // [n_acc]
+  uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + kMaxAcc);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
   const int tiles = n_tiles * ((args.M + kConvBM - 1) / kConvBM);
-  const uint32_t acc_stride = args.tmem_cols / 2;  // two accumulator buffers
+  const int n_acc = args.n_acc;
+  const uint32_t acc_stride = args.tmem_cols / n_acc;
 
   if (warp == kTmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < args.stages; ++s) {
-        ptx::mbar_init(&full[s], (kTmaA ? 0u : kGatherWarps * 32u) + 1u);
+        const uint32_t producers = kTmaA ? 0u
+                                   : MODE == static_cast<int>(ConvLoadMode::kStemU8)
+                                       ? static_cast<uint32_t>(kStemGroupThreads)
+                                       : kGatherWarps * 32u;
+        ptx::mbar_init(&full[s], producers + 1u);
         ptx::mbar_init(&empty[s], 1);
       }
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
-        ptx::mbar_init(&tmem_empty[b], kEpiWarps);  // one arrival per epilogue warp
+        ptx::mbar_init(&tmem_empty[b], 4);  // one arrival per warp of the owning team
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
@@ -424,19 +603,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < kEpiWarps) {
-    // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31)
-    // and takes every other 128 B column group (w/4 picks which).
+  if (warp < epi_warps) {
+    // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31);
+    // team w/4 takes every teams-th tile of this CTA, all its column groups,
+    // so up to `teams` tiles drain concurrently.
     const int quarter = warp & 3;
-    const int half = warp >> 2;
+    const int team = warp >> 2;
     uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;
     const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
     uint32_t j = 0, groups = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+      if (static_cast<int>(j % args.teams) != team) continue;
       const int m0 = (tile / n_tiles) * kConvBM;
       const int n0 = (tile % n_tiles) * args.BN;
-      const uint32_t acc = j & 1;
-      ptx::mbar_wait(&tmem_full[acc], (j >> 1) & 1);
+      const uint32_t acc = j % n_acc;
+      ptx::mbar_wait(&tmem_full[acc], (j / n_acc) & 1);
       ptx::tc_fence_after();
       const int m = m0 + quarter * 32 + lane;
       const uint32_t t_row =
@@ -444,7 +625,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (args.debug_flags & 1) {
         // release only
       } else if (args.y_tma) {
-        for (int g0 = half * group_cols; g0 < args.BN && n0 + g0 < args.Cout; g0 += 2 * group_cols) {
+        for (int g0 = 0; g0 < args.BN && n0 + g0 < args.Cout; g0 += group_cols) {
           uint8_t* group = ystage + (groups & 1) * kYStageBytes;
           if (groups >= 2) {  // the store issued two groups ago must have read `group`
             if (lane == 0) ptx::bulk_wait_read<1>();
@@ -465,7 +646,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ++groups;
         }
       } else {
-        for (int c0 = half * 16; c0 < args.BN && n0 + c0 < args.Cout; c0 += 32) {
+        for (int c0 = 0; c0 < args.BN && n0 + c0 < args.Cout; c0 += 16) {
           uint32_t raw[16];
           ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
           ptx::tmem_ld_wait();
@@ -478,7 +659,26 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     if (lane == 0) ptx::bulk_wait<0>();
   } else if (warp < kGatherWarp0 + kGatherWarps) {
-    if constexpr (!kTmaA) {
+    if constexpr (MODE == static_cast<int>(ConvLoadMode::kStemU8)) {
+      // two producer groups on alternate tiles; tile j's K blocks are
+      // pipeline iterations j*num_kb ..
+      const int tg = threadIdx.x - kGatherWarp0 * 32;
+      const int grp = tg / kStemGroupThreads;
+      uint32_t j = 0;
+      const int row = tg % kStemGroupThreads;
+      uint2* patch = reinterpret_cast<uint2*>(smem + L.patch_off + grp * kStemPatchBytes);
+      if (row == 0) {  // warm up: this group's first two tiles
+        stem_prefetch(args, ((blockIdx.x + grp * gridDim.x) / n_tiles) * kConvBM);
+        stem_prefetch(args, ((blockIdx.x + (grp + 2) * gridDim.x) / n_tiles) * kConvBM);
+      }
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        if (static_cast<int>(j & 1) != grp) continue;
+        if (row == 0)  // two of this group's tiles ahead
+          stem_prefetch(args, ((tile + 4 * gridDim.x) / n_tiles) * kConvBM);
+        stem_a_tile(args, smem + L.a_off, patch, full, empty, (tile / n_tiles) * kConvBM,
+                    j * static_cast<uint32_t>(args.num_kb), row, 1 + grp);
+      }
+    } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int m0 = (tile / n_tiles) * kConvBM;
@@ -517,8 +717,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
       uint32_t it = 0, j = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
-        const uint32_t acc = j & 1;
-        if (j >= 2) ptx::mbar_wait(&tmem_empty[acc], ((j >> 1) - 1) & 1);
+        const uint32_t acc = j % n_acc;
+        if (j >= static_cast<uint32_t>(n_acc)) ptx::mbar_wait(&tmem_empty[acc], ((j / n_acc) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
         for (int kb = 0; kb < args.num_kb; ++kb, ++it) {
@@ -602,7 +802,7 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
 }
 
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
-                      int box_w, int box_h) {
+                      int box_w, int box_h, int box_n) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn || (static_cast<uint64_t>(c) * 2) % 16 != 0) return false;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
@@ -611,7 +811,7 @@ bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, i
                                  static_cast<cuuint64_t>(c) * 2 * w,
                                  static_cast<cuuint64_t>(c) * 2 * w * h};
   const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_c), static_cast<cuuint32_t>(box_w),
-                             static_cast<cuuint32_t>(box_h), 1};
+                             static_cast<cuuint32_t>(box_h), static_cast<cuuint32_t>(box_n)};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -624,16 +824,39 @@ uint32_t conv_gemm_tmem_cols(int BN) {
   return c;
 }
 
-int conv_gemm_stages(int BN, int cout) {
+namespace {
+uint32_t pow2_at_least(int x) {
+  uint32_t c = 32;
+  while (static_cast<int>(c) < x) c <<= 1;
+  return c;
+}
+}  // namespace
+
+int conv_gemm_stages(int BN, int cout, int epi_warps, int patch_bytes) {
   const int ctas = 1;  // 18 warps: one CTA per SM
   const int per_stage = kABytes + BN * kConvBK * 2;
-  const int fixed = static_cast<int>(smem_layout(BN, 0, cout).total) + 64 * 8 + 1024;
+  const int fixed =
+      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, patch_bytes).total) + 64 * 8 + 1024;
   const int budget = (227 * 1024) / ctas - fixed;
   return std::max(1, std::min(kConvMaxStages, budget / per_stage));
 }
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout) {
-  return smem_layout(BN, stages, cout).total + 1024;  // + alignment slack
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int patch_bytes) {
+  return smem_layout(BN, stages, cout, epi_warps, patch_bytes).total + 1024;  // + alignment slack
+}
+
+bool conv_gemm_stem_fits(int H, int W, int R, int stride_h, int pad_h, int Ho, int Wo) {
+  // the device's row range (stem_rows) for every tile of a 256-image batch
+  // (tile starts repeat with the image period well within that)
+  const long long howo = static_cast<long long>(Ho) * Wo, M = 256 * howo;
+  for (long long m0 = 0; m0 < M; m0 += kConvBM) {
+    const long long m1 = std::min(m0 + kConvBM, M) - 1;
+    const long long n0 = m0 / howo, n1 = m1 / howo;
+    const long long lo = n0 * H + std::max(0LL, ((m0 - n0 * howo) / Wo) * stride_h - pad_h);
+    const long long hi = n1 * H + std::min<long long>(H, ((m1 - n1 * howo) / Wo) * stride_h - pad_h + R);
+    if ((hi - lo) * W * 8 > kStemPatchBytes) return false;
+  }
+  return true;
 }
 
 cudaError_t conv_gemm_init() {
@@ -651,6 +874,9 @@ cudaError_t conv_gemm_init() {
                                cap);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
     return e;
   }();
@@ -672,7 +898,20 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   ConvGemmArgs args = in_args;
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
-  const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages, args.Cout);
+  // TMEM: as many accumulators as 512 columns hold (2..kMaxAcc), so the MMA
+  // runs ahead of the epilogue; epilogue teams: 2, or 4 when the gather warps
+  // are idle (TMA-A), never more than the accumulators.
+  const uint32_t bn_cols = pow2_at_least(args.BN);
+  args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / bn_cols)));
+  args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(bn_cols));
+  // (four teams only for BN <= 64, where their staging buffers still leave a
+  // 4-deep operand ring)
+  args.teams = std::min(mode == ConvLoadMode::kTmaA && args.BN <= 64 ? kMaxEpiWarps / 4
+                                                                      : kEpiWarps / 4,
+                        args.n_acc);
+  const int patch = mode == ConvLoadMode::kStemU8 ? 2 * kStemPatchBytes : 0;
+  args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, patch);
+  const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, patch);
   const int tiles = ((args.Cout + args.BN - 1) / args.BN) * ((args.M + kConvBM - 1) / kConvBM);
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
@@ -691,6 +930,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       break;
     case ConvLoadMode::kDwFused:
       conv_gemm_kernel<3><<<grid, kConvThreads, smem, stream>>>(args);
+      break;
+    case ConvLoadMode::kStemU8:
+      conv_gemm_kernel<4><<<grid, kConvThreads, smem, stream>>>(args);
       break;
   }
   return cudaGetLastError();

@@ -36,6 +36,11 @@ struct ConvGemmArgs {
   int taps;    // R*S
   int Cout, BN, stages;
   uint32_t tmem_cols;
+  // Epilogue teams (4 warps each, one per TMEM lane quarter) and TMEM
+  // accumulators: tile j goes to accumulator j % n_acc and team j % teams
+  // (n_acc a multiple of teams, so each accumulator has one team). Set by
+  // launch_conv_gemm from the mode and BN.
+  int teams, n_acc;
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;
@@ -49,6 +54,10 @@ struct ConvGemmArgs {
   const __nv_bfloat16* dw_w;  // [9][C] bf16
   const float* dw_b;          // [C]
   int dw_stride;
+  // kStemU8: A gathered straight from the u8 images [n][H][W][3]; the
+  // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
+  // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
+  const uint8_t* img;
 };
 
 enum class ConvLoadMode : int {
@@ -56,6 +65,7 @@ enum class ConvLoadMode : int {
   kGather8 = 1,   // cp.async gather, 4 channels (8 B) per granule, C == 4 (stem)
   kTmaA = 2,      // 1x1 stride-1 conv: A is a plain 2D tile, loaded by TMA
   kDwFused = 3,   // depthwise 3x3 + bias + ReLU computed into A, then the 1x1 GEMM
+  kStemU8 = 4,    // stem conv over the u8 images, input staging fused into the producer
 };
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
@@ -74,14 +84,18 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
 // box_h, 1} box, no swizzle (used by the depthwise halo loads). Negative or
 // past-the-edge box coordinates read zeros (the convolution's padding).
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
-                      int box_w, int box_h);
+                      int box_w, int box_h, int box_n = 1);
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout);
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps = 8, int patch_bytes = 0);
+
+// kStemU8 stages the input rows of a tile in a fixed-size smem patch; false
+// when this stem geometry could exceed it (the runtime then stages the input).
+bool conv_gemm_stem_fits(int H, int W, int R, int stride_h, int pad_h, int Ho, int Wo);
 
 // Operand-ring depth for an N tile: as deep as kConvMaxStages allows within
 // the per-CTA budget, where two CTAs share an SM whenever their TMEM
 // (2 x BN accumulator columns each) fits.
-int conv_gemm_stages(int BN, int cout);
+int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int patch_bytes = 0);
 uint32_t conv_gemm_tmem_cols(int BN);
 
 // Must run once per device before the first launch (and before any capture).

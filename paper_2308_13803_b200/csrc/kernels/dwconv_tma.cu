@@ -1,14 +1,20 @@
 // Depthwise 3x3 (+bias, ReLU) streamed through TMA (K3 in DESIGN.md).
 //
-// A persistent CTA walks output tiles of 8 rows x 16 (stride 1) or 8 x 8
-// (stride 2) pixels x 64 channels. Each tile's input halo is one 4-D TMA box
-// {64 ch, IW, IH, 1 image} landing in shared memory; boxes that hang over the
-// image edge read zeros, which is exactly the convolution's padding. Two
-// stages double-buffer the boxes (mbarrier transaction counts), so the
-// next tile's halo streams in while the current one is computed; every input
-// byte crosses HBM once (plus the halo), and the 9 taps of every output come
-// from smem. Output: 16 B stores, 8 consecutive threads per pixel's 64
-// channels, consecutive pixels along the row.
+// A persistent CTA walks output tiles of TH x TW pixels (x NB images for the
+// 7x7 tail) x up to 64 channels. Each tile's input halo is one 4-D TMA box
+// {cb ch, IW, IH, NB images} landing in shared memory; box elements that hang
+// over the image edge read zeros, which is exactly the convolution's padding.
+// A ring of 2-4 boxes (mbarrier transaction counts) keeps the next tiles'
+// halos streaming in while the current one is computed, so every input byte
+// crosses HBM once and all 9 taps of every output come from smem.
+//
+// A thread owns one 8-channel group (16 B) of a strip of Q consecutive output
+// pixels along W: each input vector it loads from smem feeds up to 3 of its
+// outputs ((Q-1)*S+3 loads per row instead of 3*Q). The multiply-adds are
+// FHFMA.BF16 — fp32 fma with the bf16 operands read straight from the packed
+// halves of a register — so nothing is unpacked; the product of two bf16 is
+// exact in fp32, so each step equals fmaf on the widened values (same
+// rounding as the previous unpack-then-fmaf kernels, bit for bit).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -22,23 +28,40 @@ namespace ds {
 
 namespace {
 
-constexpr int kDwThreads = 256;
+constexpr int kDwMaxThreads = 256;
 
-template <int S>
-struct DwGeom {
-  static constexpr int TH = S == 1 ? 16 : 8;
-  static constexpr int TW = S == 1 ? 16 : 8;
-  static constexpr int IH = (TH - 1) * S + 3;
-  static constexpr int IW = (TW - 1) * S + 3;
-};
+// acc += bf16(x.lo) * bf16(w.lo) (fp32 fma), and the same for the high halves.
+__device__ __forceinline__ float fma_bf16_lo(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %3;}"
+      : "=f"(d)
+      : "r"(x), "r"(w), "f"(c));
+  return d;
+}
 
-__device__ __forceinline__ void unpack8f(const uint4& u, float (&f)[8]) {
-  const uint32_t v[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    f[2 * e] = __uint_as_float(v[e] << 16);
-    f[2 * e + 1] = __uint_as_float(v[e] & 0xFFFF0000u);
-  }
+__device__ __forceinline__ float fma_bf16_hi(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xh, wh, %3;}"
+      : "=f"(d)
+      : "r"(x), "r"(w), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ void fma8(float (&acc)[8], const uint4& x, const uint4& w) {
+  acc[0] = fma_bf16_lo(x.x, w.x, acc[0]);
+  acc[1] = fma_bf16_hi(x.x, w.x, acc[1]);
+  acc[2] = fma_bf16_lo(x.y, w.y, acc[2]);
+  acc[3] = fma_bf16_hi(x.y, w.y, acc[3]);
+  acc[4] = fma_bf16_lo(x.z, w.z, acc[4]);
+  acc[5] = fma_bf16_hi(x.z, w.z, acc[5]);
+  acc[6] = fma_bf16_lo(x.w, w.w, acc[6]);
+  acc[7] = fma_bf16_hi(x.w, w.w, acc[7]);
 }
 
 __device__ __forceinline__ uint32_t pack2f(float lo, float hi) {
@@ -46,94 +69,121 @@ __device__ __forceinline__ uint32_t pack2f(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int S>
-__global__ void __launch_bounds__(kDwThreads) dw_tma_kernel(
-    const __grid_constant__ CUtensorMap in_map, const __nv_bfloat16* __restrict__ w,
-    const float* __restrict__ bias, uint4* __restrict__ y, int c, int ho, int wo, int cb_log2,
-    int tiles_x, int tiles_y, int cblocks, int tiles) {
-  using G = DwGeom<S>;
-  const int cb = 1 << cb_log2;          // channels per tile (<= 64)
-  const int groups_log2 = cb_log2 - 3;  // 8-channel groups per pixel
-  const uint32_t box_bytes = static_cast<uint32_t>(G::IH * G::IW) << (cb_log2 + 1);
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * box_bytes);
+struct DwKernelArgs {
+  const __nv_bfloat16* w;  // [9][C]
+  const float* bias;       // [C]
+  uint4* y;                // NHWC output, 8 channels per vector
+  int n, c, ho, wo;
+  int tw, th, nb;          // tile: TW x TH pixels x NB images
+  int glog2;               // 8-channel groups per tile (log2)
+  int iw, ih;              // box W, H
+  int tiles_x, tiles_y, tiles_n, cblocks, tiles;
+  int stages;
+  uint32_t box_bytes;
+};
 
-  auto coords = [&](int t, int& cbk, int& tx, int& ty, int& img) {
-    cbk = t % cblocks;
-    t /= cblocks;
-    tx = t % tiles_x;
-    t /= tiles_x;
-    ty = t % tiles_y;
-    img = t / tiles_y;
+template <int S, int Q>
+__global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
+    const __grid_constant__ CUtensorMap in_map, const __grid_constant__ DwKernelArgs a) {
+  constexpr int XN = (Q - 1) * S + 3;  // input vectors per strip row
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.box_bytes);
+  const int groups = 1 << a.glog2;
+  const int cb = groups * 8;
+
+  auto coords = [&](int t, int& cbk, int& tx, int& ty, int& tn) {
+    cbk = t % a.cblocks;
+    t /= a.cblocks;
+    tx = t % a.tiles_x;
+    t /= a.tiles_x;
+    ty = t % a.tiles_y;
+    tn = t / a.tiles_y;
   };
   auto issue = [&](int t, int stage) {
-    int cbk, tx, ty, img;
-    coords(t, cbk, tx, ty, img);
-    ptx::mbar_arrive_expect_tx(&full[stage], box_bytes);
+    int cbk, tx, ty, tn;
+    coords(t, cbk, tx, ty, tn);
+    ptx::mbar_arrive_expect_tx(&full[stage], a.box_bytes);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + stage * box_bytes)),
-        "l"(&in_map), "r"(ptx::smem_u32(&full[stage])), "r"(cbk << cb_log2),
-        "r"(tx * G::TW * S - 1), "r"(ty * G::TH * S - 1), "r"(img)
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + stage * a.box_bytes)),
+        "l"(&in_map), "r"(ptx::smem_u32(&full[stage])), "r"(cbk * cb), "r"(tx * a.tw * S - 1),
+        "r"(ty * a.th * S - 1), "r"(tn * a.nb)
         : "memory");
   };
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&full[0], 1);
-    ptx::mbar_init(&full[1], 1);
+    for (int s = 0; s < a.stages; ++s) ptx::mbar_init(&full[s], 1);
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&in_map);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (blockIdx.x < tiles) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < tiles) issue(blockIdx.x + gridDim.x, 1);
+    for (int s = 0; s < a.stages; ++s) {
+      const int t = blockIdx.x + s * gridDim.x;
+      if (t < a.tiles) issue(t, s);
+    }
   }
 
-  const int g = threadIdx.x & ((1 << groups_log2) - 1);  // fixed channel group per thread
-  const int cg_all = c >> 3;
-  const int items = (G::TH * G::TW) << groups_log2;
+  const int cg_all = a.c >> 3;
+  const int spr = a.tw / Q;                       // strips per tile row
+  const int items = (spr * a.th * a.nb) << a.glog2;
   uint32_t j = 0;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
-    const int stage = j & 1;
-    int cbk, tx, ty, img;
-    coords(t, cbk, tx, ty, img);
-    const int gg = (cbk << (cb_log2 - 3)) + g;  // global channel group
-    uint4 wraw[9];
+  for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++j) {
+    const int stage = j % a.stages;
+    int cbk, tx, ty, tn;
+    coords(t, cbk, tx, ty, tn);
+    ptx::mbar_wait(&full[stage], (j / a.stages) & 1);
+    const uint4* box = reinterpret_cast<const uint4*>(smem + stage * a.box_bytes);
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int g = it & (groups - 1);
+      int strip = it >> a.glog2;
+      const int sx = strip % spr;
+      strip /= spr;
+      const int oyl = strip % a.th;
+      const int nbl = strip / a.th;
+      const int oy = ty * a.th + oyl;
+      const int img = tn * a.nb + nbl;
+      if (oy >= a.ho || img >= a.n) continue;
+      const int gg = cbk * groups + g;  // global channel group
+      uint4 w[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) wraw[k] = __ldg(reinterpret_cast<const uint4*>(w) + k * cg_all + gg);
-    const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * gg);
-    const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * gg + 1);
-    float wf[9][8];
+      for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(a.w) + k * cg_all + gg);
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.bias) + 2 * gg);
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.bias) + 2 * gg + 1);
+      float acc[Q][8];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) unpack8f(wraw[k], wf[k]);
-
-    ptx::mbar_wait(&full[stage], (j >> 1) & 1);
-    const uint4* tile = reinterpret_cast<const uint4*>(smem + stage * box_bytes);
-    for (int it = threadIdx.x; it < items; it += kDwThreads) {
-      const int p = it >> groups_log2;
-      const int oyl = p / G::TW, oxl = p % G::TW;
-      const int oy = ty * G::TH + oyl, ox = tx * G::TW + oxl;
-      if (oy >= ho || ox >= wo) continue;
-      float acc[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      for (int q = 0; q < Q; ++q) {
+        acc[q][0] = b0.x; acc[q][1] = b0.y; acc[q][2] = b0.z; acc[q][3] = b0.w;
+        acc[q][4] = b1.x; acc[q][5] = b1.y; acc[q][6] = b1.z; acc[q][7] = b1.w;
+      }
+      const int ix0 = sx * Q * S;
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
+      for (int r = 0; r < 3; ++r) {
+        const uint4* row = box + (((nbl * a.ih + oyl * S + r) * a.iw + ix0) << a.glog2) + g;
+        uint4 xv[XN];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          float xf[8];
-          unpack8f(tile[(((oyl * S + r) * G::IW + oxl * S + s) << groups_log2) + g], xf);
+        for (int u = 0; u < XN; ++u) xv[u] = row[u << a.glog2];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] = fmaf(xf[e], wf[r * 3 + s][e], acc[e]);
-        }
+        for (int q = 0; q < Q; ++q)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.0f);
-      y[((static_cast<long long>(img) * ho + oy) * wo + ox) * cg_all + gg] =
-          make_uint4(pack2f(acc[0], acc[1]), pack2f(acc[2], acc[3]), pack2f(acc[4], acc[5]),
-                     pack2f(acc[6], acc[7]));
+          for (int s = 0; s < 3; ++s) fma8(acc[q], xv[q * S + s], w[r * 3 + s]);
+      }
+      uint4* yp = a.y + ((static_cast<long long>(img) * a.ho + oy) * a.wo + tx * a.tw + sx * Q) *
+                            cg_all + gg;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        float* v = acc[q];
+        yp[q * cg_all] = make_uint4(pack2f(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)),
+                                    pack2f(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)),
+                                    pack2f(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)),
+                                    pack2f(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
+      }
     }
     __syncthreads();  // every thread is done with this stage's box
-    if (threadIdx.x == 0 && t + 2 * static_cast<int>(gridDim.x) < tiles)
-      issue(t + 2 * gridDim.x, stage);
+    if (threadIdx.x == 0) {
+      const int nt = t + a.stages * static_cast<int>(gridDim.x);
+      if (nt < a.tiles) issue(nt, stage);
+    }
   }
 }
 
@@ -147,50 +197,116 @@ int sm_count() {
   return n;
 }
 
+// Tile shape per layer (output width, stride, channels): a strip of Q outputs
+// per thread, TW | wo, and (TW/Q)*TH*NB*groups close to a multiple of 32 <= 256.
+struct DwPlan {
+  int q, tw, th, nb, cb;
+  bool ok;
+};
+
+DwPlan dw_plan(int ho, int wo, int c, int stride) {
+  const int cb = std::min(c, 64);
+  DwPlan p{0, 0, 0, 1, cb, false};
+  auto set = [&](int q, int tw, int th, int nb) {
+    if (wo % tw == 0 && tw % q == 0) p = DwPlan{q, tw, th, nb, cb, true};
+  };
+  if (stride == 1) {
+    if (wo % 16 == 0 && wo >= 64) set(4, 16, cb >= 64 ? 8 : 16, 1);  // 112x112
+    else if (wo % 8 == 0 && wo >= 48) set(4, 8, 14, 1);              // 56x56
+    else if (wo % 4 == 0 && wo >= 20) set(4, wo, 4, 1);              // 28x28
+    else if (wo % 7 == 0 && wo >= 14) set(7, wo, std::min(ho, 14), 1);  // 14x14
+    else if (wo == 7) set(7, 7, 7, 4);                                // 7x7
+  } else {
+    if (wo % 8 == 0 && wo >= 48) set(2, 8, 8, 1);                     // 112 -> 56
+    else if (wo % 14 == 0) set(2, 14, 4, 1);                          // 56 -> 28, 28 -> 14
+    else if (wo == 7) set(7, 7, 7, 2);                                // 14 -> 7
+  }
+  return p;
+}
+
+DwKernelArgs make_args(const DwPlan& p, int n, int h, int w, int c, int stride) {
+  DwKernelArgs a{};
+  a.n = n;
+  a.c = c;
+  a.ho = (h - 1) / stride + 1;
+  a.wo = (w - 1) / stride + 1;
+  a.tw = p.tw;
+  a.th = p.th;
+  a.nb = p.nb;
+  int glog2 = 0;
+  while ((8 << glog2) < p.cb) ++glog2;
+  a.glog2 = glog2;
+  a.iw = (p.tw - 1) * stride + 3;
+  a.ih = (p.th - 1) * stride + 3;
+  a.tiles_x = a.wo / p.tw;
+  a.tiles_y = (a.ho + p.th - 1) / p.th;
+  a.tiles_n = (n + p.nb - 1) / p.nb;
+  a.cblocks = c / p.cb;
+  a.tiles = a.tiles_x * a.tiles_y * a.tiles_n * a.cblocks;
+  a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.nb * p.cb * 2);
+  // 2-4 boxes in flight, ~100 KB per CTA so two CTAs share an SM.
+  a.stages = std::max(2, std::min(4, static_cast<int>((100 * 1024) / a.box_bytes)));
+  return a;
+}
+
+template <int S, int Q>
+cudaError_t launch_plan(const CUtensorMap& map, DwKernelArgs a, const DwPlan& p,
+                        cudaStream_t stream) {
+  auto kernel = dw_tma_kernel<S, Q>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int items = ((p.tw / Q) * p.th * p.nb) * (p.cb / 8);
+  const int threads = std::min(kDwMaxThreads, (items + 31) / 32 * 32);
+  const size_t smem = static_cast<size_t>(a.stages) * a.box_bytes + 8 * a.stages + 16;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int grid = std::min(a.tiles, sm_count() * per_sm);
+  kernel<<<grid, threads, smem, stream>>>(map, a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool dwconv_tma_supported(int c) {
   return c >= 8 && (c & (c - 1)) == 0;  // power-of-two channel count (>= one 16 B group)
 }
 
+bool dwconv_tma_plan_ok(int h, int w, int c, int stride) {
+  if (!dwconv_tma_supported(c) || (stride != 1 && stride != 2)) return false;
+  return dw_plan((h - 1) / stride + 1, (w - 1) / stride + 1, c, stride).ok;
+}
+
 cudaError_t launch_dwconv3x3_tma(const CUtensorMap& in_map, const __nv_bfloat16* w,
                                  const float* bias, __nv_bfloat16* y, int n, int h, int wd, int c,
                                  int stride, cudaStream_t stream) {
-  if (!dwconv_tma_supported(c) || (stride != 1 && stride != 2)) return cudaErrorInvalidValue;
-  const int ho = (h + 2 - 3) / stride + 1, wo = (wd + 2 - 3) / stride + 1;
-  const int cb = std::min(c, 64);
-  int cb_log2 = 0;
-  while ((1 << cb_log2) < cb) ++cb_log2;
-  const int cblocks = c / cb;
-  auto launch = [&](auto geom, auto kernel) -> cudaError_t {
-    using Gm = decltype(geom);
-    const int tiles_x = (wo + Gm::TW - 1) / Gm::TW, tiles_y = (ho + Gm::TH - 1) / Gm::TH;
-    const int tiles = n * tiles_x * tiles_y * cblocks;
-    const size_t box = static_cast<size_t>(Gm::IH) * Gm::IW * cb * 2;
-    const size_t smem = 2 * box + 64;
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e =
-          cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
-    const int per_sm = std::max(1, static_cast<int>((227 * 1024) / smem));
-    const int grid = std::min(tiles, sm_count() * std::min(per_sm, 4));
-    kernel<<<grid, kDwThreads, smem, stream>>>(in_map, w, bias, reinterpret_cast<uint4*>(y), c,
-                                               ho, wo, cb_log2, tiles_x, tiles_y, cblocks, tiles);
-    return cudaGetLastError();
-  };
-  if (stride == 1) return launch(DwGeom<1>{}, dw_tma_kernel<1>);
-  return launch(DwGeom<2>{}, dw_tma_kernel<2>);
+  if (!dwconv_tma_plan_ok(h, wd, c, stride)) return cudaErrorInvalidValue;
+  const DwPlan p = dw_plan((h - 1) / stride + 1, (wd - 1) / stride + 1, c, stride);
+  DwKernelArgs a = make_args(p, n, h, wd, c, stride);
+  a.w = w;
+  a.bias = bias;
+  a.y = reinterpret_cast<uint4*>(y);
+  if (stride == 1) {
+    if (p.q == 4) return launch_plan<1, 4>(in_map, a, p, stream);
+    return launch_plan<1, 7>(in_map, a, p, stream);
+  }
+  if (p.q == 2) return launch_plan<2, 2>(in_map, a, p, stream);
+  return launch_plan<2, 7>(in_map, a, p, stream);
 }
 
 bool dwconv_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w, int c,
                           int stride) {
-  const int cb = std::min(c, 64);
-  if (stride == 1)
-    return encode_tmap_nhwc(map, x, max_n, h, w, c, cb, DwGeom<1>::IW, DwGeom<1>::IH);
-  return encode_tmap_nhwc(map, x, max_n, h, w, c, cb, DwGeom<2>::IW, DwGeom<2>::IH);
+  if (!dwconv_tma_plan_ok(h, w, c, stride)) return false;
+  const DwPlan p = dw_plan((h - 1) / stride + 1, (w - 1) / stride + 1, c, stride);
+  return encode_tmap_nhwc(map, x, max_n, h, w, c, p.cb, (p.tw - 1) * stride + 3,
+                          (p.th - 1) * stride + 3, p.nb);
 }
 
 }  // namespace ds

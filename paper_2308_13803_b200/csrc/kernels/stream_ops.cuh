@@ -24,6 +24,7 @@ cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, con
 // power of two >= 8. The input map comes from dwconv_tma_input_map over the
 // (max-batch) input buffer.
 bool dwconv_tma_supported(int c);
+bool dwconv_tma_plan_ok(int h, int w, int c, int stride);
 bool dwconv_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w, int c,
                           int stride);
 cudaError_t launch_dwconv3x3_tma(const CUtensorMap& in_map, const __nv_bfloat16* w,

@@ -1,5 +1,6 @@
 #include "engine.hpp"
 
+#include <cstdio>
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -85,7 +86,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
 
   plans_.resize(m.ops.size());
   fused_ = fused_depthwise(m);
-  kernels_per_forward_ = 2;  // input staging + softmax
+  stem_ = fused_stem(m);
+  kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (input staging +) softmax
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
     if (!fused_[i]) ++kernels_per_forward_;
@@ -94,10 +96,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       dw_maps_.resize(m.ops.size());
       dw_tma_.resize(m.ops.size(), false);
       const char* legacy = std::getenv("DS_DW_LEGACY");
-      // TMA halo tiles pay from 14-wide outputs up; the 7x7 tail keeps the
-      // register-blocked kernel (a 16x16 tile would be mostly empty).
-      const int dout_w = m.buffers.at(op.out).w;
-      dw_tma_[i] = !(legacy && legacy[0] == '1') && dout_w >= 14 && dwconv_tma_supported(din.c) &&
+      dw_tma_[i] = !(legacy && legacy[0] == '1') && dwconv_tma_plan_ok(din.h, din.w, din.c, op.sh) &&
                    dwconv_tma_input_map(&dw_maps_[i], bufs_[op.in], max_bs, din.h, din.w, din.c,
                                         op.sh);
     }
@@ -154,6 +153,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
       a.dw_b = d_b_ + hp.b_off.at(dw.param);
       a.dw_stride = dw.sh;
+    } else if (static_cast<int>(i) == stem_) {
+      pl.mode = ConvLoadMode::kStemU8;  // a.img is bound per launch (input slot)
     } else if (in.c == 4) {
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
@@ -208,10 +209,12 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
                  "mark");
   };
   record_mark();
-  check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs, m.in_h,
-                                m.in_w, stream_),
-             "stage_input");
-  record_mark();
+  if (stem_ < 0) {
+    check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs,
+                                  m.in_h, m.in_w, stream_),
+               "stage_input");
+    record_mark();
+  }
   for (size_t i = 0; i < m.ops.size(); ++i) {
     if (fused_[i]) continue;  // computed inside the next conv's producer
     const OpSpec& op = m.ops[i];
@@ -225,6 +228,12 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
       case OpKind::kFc: {
         ConvGemmArgs a = plans_[i].args;
         a.M = bs * plans_[i].ho * plans_[i].wo;
+        if (static_cast<int>(i) == stem_) a.img = d_images_[slot];
+        if (const char* dbg = std::getenv("DS_CONV_DEBUG")) {  // bring-up: "op:flags"
+          int op_i = -1, flags = 0;
+          if (std::sscanf(dbg, "%d:%d", &op_i, &flags) == 2 && op_i == static_cast<int>(i))
+            a.debug_flags = flags;
+        }
         e = launch_conv_gemm(a, plans_[i].mode, stream_);
         break;
       }

@@ -89,6 +89,7 @@ class Instance {
   std::vector<void*> bufs_;
   std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
   std::vector<bool> fused_;      // depthwise ops folded into the next conv
+  int stem_ = -1;                // stem conv reading the u8 images (kStemU8), or -1
   std::vector<CUtensorMap> dw_maps_;  // TMA halo maps of depthwise inputs (by op)
   std::vector<bool> dw_tma_;          // depthwise op uses the TMA kernel
   std::map<int, cudaGraphExec_t> graphs_;

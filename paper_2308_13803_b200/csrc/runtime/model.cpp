@@ -5,6 +5,8 @@
 // oracle/fwd_oracle.c.
 #include "model.hpp"
 
+#include "../kernels/conv_gemm.cuh"
+
 #include <cstdlib>
 #include <stdexcept>
 
@@ -329,11 +331,31 @@ std::vector<bool> fused_depthwise(const ModelSpec& m) {
   return fused;
 }
 
+int fused_stem(const ModelSpec& m) {
+  const char* staged = std::getenv("DS_STEM_STAGED");  // A/B switch for the parity test
+  if (staged && staged[0] == '1') return -1;
+  int stem = -1;
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    if (op.in != 0 && op.residual != 0) continue;
+    if (stem >= 0 || op.kind != OpKind::kConv || op.residual == 0 || m.buffers[0].c != 4) return -1;
+    stem = static_cast<int>(i);
+  }
+  if (stem >= 0) {
+    const OpSpec& op = m.ops[stem];
+    const BufferSpec& in = m.buffers[0];
+    const BufferSpec& out = m.buffers[op.out];
+    if (!conv_gemm_stem_fits(in.h, in.w, op.r, op.sh, op.ph, out.h, out.w)) return -1;
+  }
+  return stem;
+}
+
 std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
   const std::vector<bool> fused = fused_depthwise(m);
+  const int stem = fused_stem(m);
   std::vector<KernelCost> out;
   const double px = static_cast<double>(m.in_h) * m.in_w;
-  out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
+  if (stem < 0) out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
   for (const auto& op : m.ops) {
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out_b = m.buffers[op.out];
@@ -347,7 +369,11 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         const double out_elems = hw_out * p.cout;
         k.kind = KernelKind::kConvGemm;
         k.flops_per_image = 2.0 * out_elems * p.r * p.s * p.cin;
-        k.bytes_per_image = in_elems * 2 + out_elems * (out_b.f32 ? 4 : 2) +
+        // the fused stem reads the u8 image (3 B per pixel) instead of the
+        // staged bf16 tensor
+        const double in_bytes =
+            static_cast<int>(&op - m.ops.data()) == stem ? px * 3 : in_elems * 2;
+        k.bytes_per_image = in_bytes + out_elems * (out_b.f32 ? 4 : 2) +
                             (op.residual >= 0 ? out_elems * 2 : 0.0);
         k.fixed_bytes = static_cast<double>(p.cout) * p.r * p.s * p.cin * 2 + p.cout * 4.0;
         break;

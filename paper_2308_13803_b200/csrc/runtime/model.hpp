@@ -72,6 +72,11 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m);
 // output feeds only op i+1, a 1x1 stride-1 conv. Opt-in (DS_DW_FUSION=1):
 // correct (parity-tested) but its producer is still latency-bound.
 std::vector<bool> fused_depthwise(const ModelSpec& m);
+
+// Index of the stem conv when it reads the u8 images directly (ConvLoadMode
+// kStemU8: staging fused into its producer), -1 when the staged bf16 input is
+// used (DS_STEM_STAGED=1, or buffer 0 has another reader).
+int fused_stem(const ModelSpec& m);
 std::vector<std::string> model_ids();
 
 }  // namespace ds

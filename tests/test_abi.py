@@ -44,7 +44,10 @@ def test_device_free_entry_points():
     mi = model_info("mobilenet_v1")
     assert (mi.in_h, mi.in_w, mi.classes) == (224, 224, 1000)
     ks = kernel_costs("resnet50_v1")
-    assert ks[0]["kind"] == "stage" and ks[-1]["kind"] == "softmax"
+    # the stem reads the u8 images itself (staging fused), so the first
+    # launch is the stem conv: 3 B per input pixel instead of 3 B + 8 B
+    assert ks[0]["kind"] == "conv_gemm" and ks[-1]["kind"] == "softmax"
+    assert ks[0]["bytes_per_image"] < 224 * 224 * 3 + 112 * 112 * 64 * 2 + 1
     assert abs(sum(k["flops_per_image"] for k in ks) - 2 * model_info("resnet50_v1").macs_per_image) < 1
     with pytest.raises(ValueError, match="unknown model"):
         model_info("vgg16")

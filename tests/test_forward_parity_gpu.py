@@ -73,6 +73,39 @@ def test_depthwise_fusion_matches_unfused(monkeypatch):
     assert np.array_equal(plain, fused)
 
 
+@pytest.mark.parametrize("bs", [1, 3, 5])
+def test_depthwise_tma_matches_register_kernels(monkeypatch, bs):
+    """The TMA-streamed depthwise kernel (FHFMA.BF16 on packed halves, strips
+    of Q outputs, NB-image boxes on the 7x7 tail) and the register-blocked
+    unpack-then-fmaf kernels accumulate the same products in the same order,
+    so logits agree bit for bit, including batches that leave NB boxes ragged."""
+    imgs = generate_images("mobilenet_v1", 11, bs)
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        tma = be.forward(imgs)
+    monkeypatch.setenv("DS_DW_LEGACY", "1")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        legacy = be.forward(imgs)
+    assert np.array_equal(tma, legacy)
+
+
+@pytest.mark.parametrize("model", ["synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"])
+def test_fused_stem_matches_staged_input(monkeypatch, model):
+    """The stem conv reading u8 images directly (kStemU8: the staging
+    normalisation through a table of the exact staged bf16 values) against
+    the staging kernel + bf16-input stem: identical A operands, so identical
+    logits; one launch fewer per forward."""
+    imgs = generate_images(model, 3, 3)
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        fused = be.forward(imgs)
+        k_fused = be.stats()["kernels_per_forward"]
+    monkeypatch.setenv("DS_STEM_STAGED", "1")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        staged = be.forward(imgs)
+        k_staged = be.stats()["kernels_per_forward"]
+    assert np.array_equal(fused, staged)
+    assert k_staged == k_fused + 1
+
+
 def test_softmax_probs():
     imgs = generate_images("synthetic_cnn", 0, 5)
     with GpuBackend("synthetic_cnn", Config(abs_max_bs=8, max_mtl=1)) as be:

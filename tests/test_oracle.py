@@ -116,3 +116,19 @@ def test_inception_layout_matches_torchvision():
     # torchvision defines branch modules in the same order the oracle emits them
     assert sorted(ours) == sorted(tv_convs)
     assert len(ours) == len(tv_convs) == 94
+
+
+def test_stem_normalisation_exact():
+    """The fused stem producer (conv_gemm kStemU8) normalises a pixel byte as
+    bf16_rn((p - 127.5f) * (1/63.75f)); the staging kernel and the oracle use
+    bf16_rn((p - 127.5f) / 63.75f). The fp32 intermediates differ for some p,
+    but the bf16 results agree for every byte value (exhaustive)."""
+    def bf16_rn(x):
+        u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+        return (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) & 0xFFFF).astype(np.uint16)
+
+    p = np.arange(256, dtype=np.float32)
+    t = (p - np.float32(127.5)).astype(np.float32)
+    div = bf16_rn((t / np.float32(63.75)).astype(np.float32))
+    mul = bf16_rn((t * (np.float32(1) / np.float32(63.75))).astype(np.float32))
+    assert np.array_equal(div, mul)
