@@ -69,6 +69,26 @@ __device__ __forceinline__ uint32_t pack2f(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// n / d for 0 <= n < 2^31 by multiply-high and shift (d >= 1, host-built).
+struct FastDiv {
+  uint32_t d, mul, shift;
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    return (__umulhi(n, mul) + n) >> shift;
+#else
+    return static_cast<uint32_t>(((static_cast<uint64_t>(n) * mul >> 32) + n) >> shift);
+#endif
+  }
+};
+
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  while ((1u << f.shift) < d) ++f.shift;
+  f.mul = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 32) *
+                                 ((static_cast<uint64_t>(1) << f.shift) - d)) / d + 1);
+  return f;
+}
+
 struct DwKernelArgs {
   const __nv_bfloat16* w;  // [9][C]
   const float* bias;       // [C]
@@ -78,10 +98,14 @@ struct DwKernelArgs {
   int glog2;               // 8-channel groups per tile (log2)
   int iw, ih;              // box W, H
   int tiles_x, tiles_y, tiles_n, cblocks, tiles;
+  FastDiv div_tx, div_ty, div_sp;  // by tiles_x, tiles_y, tiles_x*tiles_y*tiles_n
   int stages;
   uint32_t box_bytes;
 };
 
+// Tile t -> (channel block, x, y, image block). The channel block varies
+// slowest, so a persistent CTA keeps one block's weights in registers for
+// many consecutive tiles.
 template <int S, int Q>
 __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
     const __grid_constant__ CUtensorMap in_map, const __grid_constant__ DwKernelArgs a) {
@@ -92,12 +116,12 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
   const int cb = groups * 8;
 
   auto coords = [&](int t, int& cbk, int& tx, int& ty, int& tn) {
-    cbk = t % a.cblocks;
-    t /= a.cblocks;
-    tx = t % a.tiles_x;
-    t /= a.tiles_x;
-    ty = t % a.tiles_y;
-    tn = t / a.tiles_y;
+    cbk = static_cast<int>(a.div_sp.div(static_cast<uint32_t>(t)));
+    int r = t - cbk * static_cast<int>(a.div_sp.d);
+    const int q = static_cast<int>(a.div_tx.div(static_cast<uint32_t>(r)));
+    tx = r - q * a.tiles_x;
+    tn = static_cast<int>(a.div_ty.div(static_cast<uint32_t>(q)));
+    ty = q - tn * a.tiles_y;
   };
   auto issue = [&](int t, int stage) {
     int cbk, tx, ty, tn;
@@ -124,42 +148,55 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
     }
   }
 
+  // This thread's item — one strip of Q outputs x 8 channels — is the same in
+  // every tile (the host sizes the block to the tile's items).
   const int cg_all = a.c >> 3;
-  const int spr = a.tw / Q;                       // strips per tile row
+  const int spr = a.tw / Q;  // strips per tile row
   const int items = (spr * a.th * a.nb) << a.glog2;
+  const bool active = static_cast<int>(threadIdx.x) < items;
+  const int g = threadIdx.x & (groups - 1);
+  int sx, oyl, nbl;
+  {
+    int strip = threadIdx.x >> a.glog2;
+    sx = strip % spr;
+    strip /= spr;
+    oyl = strip % a.th;
+    nbl = strip / a.th;
+  }
+  const uint4* my_box = reinterpret_cast<const uint4*>(smem) +
+                        (((nbl * a.ih + oyl * S) * a.iw + sx * Q * S) << a.glog2) + g;
+  const int box_vecs = static_cast<int>(a.box_bytes >> 4);
+  uint4 w[9];
+  float bias[8];
+  int cur_cbk = -1;
   uint32_t j = 0;
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++j) {
     const int stage = j % a.stages;
     int cbk, tx, ty, tn;
     coords(t, cbk, tx, ty, tn);
-    ptx::mbar_wait(&full[stage], (j / a.stages) & 1);
-    const uint4* box = reinterpret_cast<const uint4*>(smem + stage * a.box_bytes);
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int g = it & (groups - 1);
-      int strip = it >> a.glog2;
-      const int sx = strip % spr;
-      strip /= spr;
-      const int oyl = strip % a.th;
-      const int nbl = strip / a.th;
-      const int oy = ty * a.th + oyl;
-      const int img = tn * a.nb + nbl;
-      if (oy >= a.ho || img >= a.n) continue;
-      const int gg = cbk * groups + g;  // global channel group
-      uint4 w[9];
+    const int oy = ty * a.th + oyl;
+    const int img = tn * a.nb + nbl;
+    const int gg = cbk * groups + g;  // global channel group
+    if (cbk != cur_cbk) {
+      cur_cbk = cbk;
 #pragma unroll
       for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(a.w) + k * cg_all + gg);
       const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.bias) + 2 * gg);
       const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.bias) + 2 * gg + 1);
+      bias[0] = b0.x; bias[1] = b0.y; bias[2] = b0.z; bias[3] = b0.w;
+      bias[4] = b1.x; bias[5] = b1.y; bias[6] = b1.z; bias[7] = b1.w;
+    }
+    ptx::mbar_wait(&full[stage], (j / a.stages) & 1);
+    if (active && oy < a.ho && img < a.n) {
       float acc[Q][8];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        acc[q][0] = b0.x; acc[q][1] = b0.y; acc[q][2] = b0.z; acc[q][3] = b0.w;
-        acc[q][4] = b1.x; acc[q][5] = b1.y; acc[q][6] = b1.z; acc[q][7] = b1.w;
-      }
-      const int ix0 = sx * Q * S;
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[q][e] = bias[e];
+      const uint4* box = my_box + stage * box_vecs;
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const uint4* row = box + (((nbl * a.ih + oyl * S + r) * a.iw + ix0) << a.glog2) + g;
+        const uint4* row = box + ((r * a.iw) << a.glog2);
         uint4 xv[XN];
 #pragma unroll
         for (int u = 0; u < XN; ++u) xv[u] = row[u << a.glog2];
@@ -208,7 +245,8 @@ DwPlan dw_plan(int ho, int wo, int c, int stride) {
   const int cb = std::min(c, 64);
   DwPlan p{0, 0, 0, 1, cb, false};
   auto set = [&](int q, int tw, int th, int nb) {
-    if (wo % tw == 0 && tw % q == 0) p = DwPlan{q, tw, th, nb, cb, true};
+    const int items = (tw / q) * th * nb * (cb / 8);  // one per thread
+    if (wo % tw == 0 && tw % q == 0 && items <= kDwMaxThreads) p = DwPlan{q, tw, th, nb, cb, true};
   };
   if (stride == 1) {
     if (wo % 16 == 0 && wo >= 64) set(4, 16, cb >= 64 ? 8 : 16, 1);  // 112x112
@@ -243,9 +281,12 @@ DwKernelArgs make_args(const DwPlan& p, int n, int h, int w, int c, int stride) 
   a.tiles_n = (n + p.nb - 1) / p.nb;
   a.cblocks = c / p.cb;
   a.tiles = a.tiles_x * a.tiles_y * a.tiles_n * a.cblocks;
+  a.div_tx = make_fastdiv(static_cast<uint32_t>(a.tiles_x));
+  a.div_ty = make_fastdiv(static_cast<uint32_t>(a.tiles_y));
+  a.div_sp = make_fastdiv(static_cast<uint32_t>(a.tiles_x * a.tiles_y * a.tiles_n));
   a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.nb * p.cb * 2);
-  // 2-4 boxes in flight, ~100 KB per CTA so two CTAs share an SM.
-  a.stages = std::max(2, std::min(4, static_cast<int>((100 * 1024) / a.box_bytes)));
+  // 2-4 boxes in flight, <= ~72 KB per CTA so three CTAs share an SM.
+  a.stages = std::max(2, std::min(4, static_cast<int>((72 * 1024) / a.box_bytes)));
   return a;
 }
 
