@@ -26,6 +26,7 @@
 //   warp 17    one thread issues tcgen05.mma (M=128, N=BN, K=16) into the
 //              current fp32 TMEM accumulator and commits stage releases.
 #include "conv_gemm.cuh"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 #include <algorithm>
@@ -602,6 +603,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // activations (and the residual) come from earlier layers
 
   if (warp < epi_warps) {
     // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31);
@@ -920,20 +923,15 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
   switch (mode) {
     case ConvLoadMode::kGather16:
-      conv_gemm_kernel<0><<<grid, kConvThreads, smem, stream>>>(args);
-      break;
+      return launch_pdl(conv_gemm_kernel<0>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kGather8:
-      conv_gemm_kernel<1><<<grid, kConvThreads, smem, stream>>>(args);
-      break;
+      return launch_pdl(conv_gemm_kernel<1>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kTmaA:
-      conv_gemm_kernel<2><<<grid, kConvThreads, smem, stream>>>(args);
-      break;
+      return launch_pdl(conv_gemm_kernel<2>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kDwFused:
-      conv_gemm_kernel<3><<<grid, kConvThreads, smem, stream>>>(args);
-      break;
+      return launch_pdl(conv_gemm_kernel<3>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kStemU8:
-      conv_gemm_kernel<4><<<grid, kConvThreads, smem, stream>>>(args);
-      break;
+      return launch_pdl(conv_gemm_kernel<4>, grid, dim3(kConvThreads), smem, stream, args);
   }
   return cudaGetLastError();
 }

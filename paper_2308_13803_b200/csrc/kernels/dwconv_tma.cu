@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "conv_gemm.cuh"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 #include "stream_ops.cuh"
 
@@ -141,6 +142,8 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
     ptx::tma_prefetch_desc(&in_map);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // the input is the previous layer's output
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int t = blockIdx.x + s * gridDim.x;
@@ -310,8 +313,7 @@ cudaError_t launch_plan(const CUtensorMap& map, DwKernelArgs a, const DwPlan& p,
       per_sm < 1)
     per_sm = 1;
   const int grid = std::min(a.tiles, sm_count() * per_sm);
-  kernel<<<grid, threads, smem, stream>>>(map, a);
-  return cudaGetLastError();
+  return launch_pdl(kernel, dim3(grid), dim3(threads), smem, stream, map, a);
 }
 
 }  // namespace

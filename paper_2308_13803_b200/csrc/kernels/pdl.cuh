@@ -1,0 +1,47 @@
+// Programmatic dependent launch (PDL) for the forward's kernel chain: every
+// layer kernel is launched with programmatic stream serialization, triggers
+// its dependents as soon as it starts and waits for its predecessor's grid
+// (griddepcontrol.wait) only after its own prologue (barrier init, TMEM
+// allocation, descriptor prefetch, bias/weight loads — nothing a previous
+// layer writes). Inside a captured CUDA graph the edges become programmatic,
+// so a layer's launch and prologue overlap the previous layer's tail.
+// DS_PDL=0 launches plainly (A/B switch); griddepcontrol.wait is a no-op then.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+namespace ds {
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+}  // namespace ds

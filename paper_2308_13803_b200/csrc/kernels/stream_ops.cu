@@ -5,6 +5,8 @@
 // stays close to one read of the input and one write of the output.
 #include "stream_ops.cuh"
 
+#include "pdl.cuh"
+
 #include <algorithm>
 
 namespace ds {
@@ -37,6 +39,8 @@ inline unsigned grid_for(long long work) {
 
 __global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __restrict__ out,
                                    long long pixels) {
+  pdl_trigger();
+  pdl_wait();
   const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= pixels) return;
   const uint8_t* s = img + 3 * p;
@@ -58,6 +62,8 @@ __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
     const uint4* __restrict__ x, const __nv_bfloat16* __restrict__ w,
     const float* __restrict__ bias, uint4* __restrict__ y, int h, int wd, int c, int ho, int wo,
     int cg_log2, int xq_per_row) {
+  pdl_trigger();
+  pdl_wait();
   // grid.y = output row (image * ho + oy); x covers (column quad, channel group)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = 1 << cg_log2;
@@ -133,6 +139,8 @@ __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
 __global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
                                  const float4* __restrict__ bias, uint4* __restrict__ y, int h,
                                  int wd, int cg, int ho, int wo, int stride, long long work) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= work) return;
   const int g = static_cast<int>(i % cg);
@@ -169,6 +177,8 @@ __global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __
 __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
                                int cg, int ho, int wo, int stride, int pad, int is_max, int ldo_g,
                                int coff_g, long long work) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= work) return;
   const int g = static_cast<int>(i % cg);
@@ -205,6 +215,8 @@ __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ 
 
 __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int hw,
                                       int cg, long long work) {
+  pdl_trigger();
+  pdl_wait();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= work) return;
   const int g = static_cast<int>(i % cg);
@@ -225,6 +237,8 @@ __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __rest
 
 __global__ void softmax_kernel(const float* __restrict__ logits, float* __restrict__ probs, int n,
                                int classes) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -247,8 +261,8 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
 cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
                                cudaStream_t stream) {
   const long long pixels = static_cast<long long>(n) * h * w;
-  stage_input_kernel<<<grid_for(pixels), kBlock, 0, stream>>>(img, reinterpret_cast<uint2*>(out),
-                                                              pixels);
+  return launch_pdl(stage_input_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
+                    reinterpret_cast<uint2*>(out), pixels);
   return cudaGetLastError();
 }
 
@@ -266,15 +280,15 @@ cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, con
   if (stride == 1) {
     const int xq = (wo + kDwCols - 1) / kDwCols;
     const int bt = block_for(xq * cg);
-    dwconv3x3_kernel<1><<<dim3((xq * cg + bt - 1) / bt, rows), bt, 0, stream>>>(
-        reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h, wd, c, ho, wo,
-        cg_log2, xq);
+    return launch_pdl(dwconv3x3_kernel<1>, dim3((xq * cg + bt - 1) / bt, rows), dim3(bt), 0, stream,
+                      reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h,
+                      wd, c, ho, wo, cg_log2, xq);
   } else {
     const long long pw = static_cast<long long>(n) * ho * wo * cg;
-    dwconv3x3_px_kernel<<<grid_for(pw), kBlock, 0, stream>>>(
-        reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
-        reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd, cg, ho, wo,
-        stride, pw);
+    return launch_pdl(dwconv3x3_px_kernel, dim3(grid_for(pw)), dim3(kBlock), 0, stream,
+                      reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
+                      reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd,
+                      cg, ho, wo, stride, pw);
   }
   return cudaGetLastError();
 }
@@ -285,9 +299,9 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
   const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
   const int cg = c / 8;
   const long long work = static_cast<long long>(n) * ho * wo * cg;
-  pool3x3_kernel<<<grid_for(work), kBlock, 0, stream>>>(
-      reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, stride,
-      pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work);
+  return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
+                    reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho,
+                    wo, stride, pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work);
   return cudaGetLastError();
 }
 
@@ -295,16 +309,16 @@ cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int 
                                   cudaStream_t stream) {
   const int cg = c / 8;
   const long long work = static_cast<long long>(n) * cg;
-  global_avgpool_kernel<<<grid_for(work), kBlock, 0, stream>>>(
-      reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, work);
+  return launch_pdl(global_avgpool_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
+                    reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, work);
   return cudaGetLastError();
 }
 
 cudaError_t launch_softmax(const float* logits, float* probs, int n, int classes,
                            cudaStream_t stream) {
   const int rows_per_block = kBlock / 32;
-  softmax_kernel<<<(n + rows_per_block - 1) / rows_per_block, kBlock, 0, stream>>>(logits, probs,
-                                                                                  n, classes);
+  return launch_pdl(softmax_kernel, dim3((n + rows_per_block - 1) / rows_per_block), dim3(kBlock),
+                    0, stream, logits, probs, n, classes);
   return cudaGetLastError();
 }
 
