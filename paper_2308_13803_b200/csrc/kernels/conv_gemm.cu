@@ -30,6 +30,7 @@
 #include "sm100_ptx.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -53,25 +54,69 @@ constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
 constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
 
 struct SmemLayout {
-  uint32_t a_off, b_off, y_off, bar_off, bias_off, patch_off, total;
+  uint32_t a_off, b_off, y_off, bar_off, bias_off, total;
 };
 
-// kStemU8: per producer group, one normalised input patch (bf16 [rows][W][4]).
-constexpr int kStemPatchBytes = 20 * 1024;
-
+// b_res_blocks > 0: the layer's whole weight matrix (num_kb blocks of
+// BN x 64) stays resident in shared memory for all tiles (one N tile, small
+// K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
-                                                  int patch_bytes = 0) {
+                                                  int b_res_blocks = 0) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * kABytes;
-  L.y_off = L.b_off + static_cast<uint32_t>(stages) * BN * 128;
+  const int b_blocks = b_res_blocks > 0 ? b_res_blocks : stages;
+  L.y_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;
   L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
-  // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], tmem slot
-  L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 1) * 8 + 15) / 16 * 16;
+  // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full, tmem slot
+  L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 2) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
-  L.patch_off = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
-  L.total = L.patch_off + static_cast<uint32_t>(patch_bytes);
+  L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
+}
+
+// In-order position on the operand ring (iteration it = lap * stages + slot),
+// advanced incrementally: the single-thread MMA/TMA loops are latency-bound,
+// so no integer division sits on their per-tile path.
+struct RingPos {
+  uint32_t slot = 0, lap = 0;
+  __device__ __forceinline__ void next(int stages) {
+    if (++slot == static_cast<uint32_t>(stages)) {
+      slot = 0;
+      ++lap;
+    }
+  }
+};
+
+// This CTA's tiles (tile = blockIdx.x + j * gridDim.x) as (M block, N block),
+// N block fastest, walked without divisions.
+struct TileWalk {
+  int mb, nb, step_m, step_n, n_tiles;
+  __device__ __forceinline__ explicit TileWalk(int n) : n_tiles(n) {
+    mb = blockIdx.x / n;
+    nb = blockIdx.x - mb * n;
+    step_m = gridDim.x / n;
+    step_n = gridDim.x - step_m * n;
+  }
+  __device__ __forceinline__ void next() {
+    mb += step_m;
+    nb += step_n;
+    if (nb >= n_tiles) {
+      nb -= n_tiles;
+      ++mb;
+    }
+  }
+};
+
+// kStemU8: each of the eight gather warps produces whole tiles on its own
+// (tile j -> warp j % 8) and owns ring slot j % 8 (stages == 8), so its waits
+// on that slot stay in order (a shared ring would let one warp wait on a slot
+// two phases ahead, which a parity wait cannot tell apart). `use` counts
+// earlier uses of the slot.
+__device__ __forceinline__ void stem_slot(uint32_t j, int kb, int num_kb, uint32_t& slot,
+                                          uint32_t& use) {
+  slot = j % kGatherWarps;
+  use = (j / kGatherWarps) * static_cast<uint32_t>(num_kb) + static_cast<uint32_t>(kb);
 }
 
 // Gathers the A tiles of one output tile (128 im2col rows) for every K
@@ -80,7 +125,7 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
 template <int G>
 __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* smem,
                                               uint64_t* full, uint64_t* empty, int m0,
-                                              uint32_t& it) {
+                                              RingPos& rp) {
   constexpr int GPR = 64 / G;                   // granules per 128 B row
   constexpr int RPP = kGatherWarps * 32 / GPR;  // rows covered per pass of the gather warps
   constexpr int PASSES = kConvBM / RPP;         // passes per tile
@@ -122,9 +167,9 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
   // (row & 7) is fixed per thread.
   const uint32_t lane_off = static_cast<uint32_t>(r0) * 128 +
                             ((((col_bytes >> 4) ^ (r0 & 7)) << 4) | (col_bytes & 15));
-  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
-    const uint32_t s = it % a.stages;
-    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
+  for (int kb = 0; kb < a.num_kb; ++kb, rp.next(a.stages)) {
+    const uint32_t s = rp.slot;
+    if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
     const int k = kb * kConvBK + gi * G;
     const int tap = k / a.C;
     const int c = k - tap * a.C;
@@ -171,7 +216,7 @@ __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
 // activation never goes to HBM. Each thread owns one 8-channel granule of 4
 // rows; weights and bias of the granule are loaded once per K block.
 __device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, uint64_t* full,
-                                          uint64_t* empty, int m0, uint32_t& it) {
+                                          uint64_t* empty, int m0, RingPos& rp) {
   constexpr int GPR = 8;                        // 16 B granules per 128 B row
   constexpr int RPP = kGatherWarps * 32 / GPR;  // 32 rows per pass
   constexpr int PASSES = kConvBM / RPP;         // 4
@@ -212,9 +257,9 @@ __device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, 
   const uint32_t lane_off =
       static_cast<uint32_t>(r0) * 128 + (static_cast<uint32_t>(gi ^ (r0 & 7)) << 4);
   uint8_t* stage_base = smem + lane_off;
-  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
-    const uint32_t s = it % a.stages;
-    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
+  for (int kb = 0; kb < a.num_kb; ++kb, rp.next(a.stages)) {
+    const uint32_t s = rp.slot;
+    if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
     const int g = kb * GPR + gi;  // channel group of this thread
     const bool cvalid = g < cg_all;
     float w[9][8], b[8];
@@ -263,21 +308,19 @@ __device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, 
 }
 
 // Stem producer (kStemU8): the stem conv reads the u8 images [n][H][W][3]
-// directly, so the staged bf16 input tensor is never materialised. The eight
-// gather warps form two groups of four that take alternate tiles (two tiles
-// in flight); per tile a group
-//   1. stages the input rows the tile's 128 output pixels touch (one
-//      contiguous range of flattened image rows n*H+h) into its smem patch as
-//      normalised bf16 [row][W][4] (channel 3 zero) — coalesced byte loads;
-//   2. builds every K block of A from the patch like the bf16 gather: a
-//      thread owns one 16 B granule (two taps x 4 channels) of 8 rows, two
-//      8 B patch reads per granule, zeros for padding and the K tail.
+// directly, so the staged bf16 input tensor is never materialised. Each of
+// the eight gather warps owns whole tiles (tile j of this CTA -> warp j % 8),
+// so eight tiles' loads are in flight and no block-level barrier is needed.
+// Lane l owns tile rows l, l+32, l+64, l+96 (consecutive output pixels across
+// lanes, so a warp's byte loads of one tap fall in one or two 128 B lines):
+// for each tap it loads the pixel's 3 bytes, normalises them and writes the
+// row's 16 B granules (two taps x 4 channels, the 4th zero) into the
+// 128 B-swizzled A stage; padding and the K tail become zeros.
 //
 // Normalisation: the staging kernel stores bf16_rn((p - 127.5f) / 63.75f).
 // Here it is bf16_rn((p - 127.5f) * (1 / 63.75f)): the fp32 values differ for
 // some p, but after bf16 rounding the two agree for all 256 byte values
 // (checked exhaustively, tests/test_oracle.py::test_stem_normalisation_exact).
-constexpr int kStemGroupThreads = kGatherWarps * 32 / 2;
 
 // u8 -> fp32 without the conversion pipe: the float with bits 0x4B000000 | p
 // is 2^23 + p exactly, so subtracting 2^23 gives p exactly.
@@ -292,26 +335,16 @@ __device__ __forceinline__ uint32_t stem_norm2(uint32_t p0, uint32_t p1) {
   return pack2_bf16(v0, v1);
 }
 
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-// Flattened input-row range [g_lo, g_hi) (g = n*H + h) the output pixels
-// m0 .. m0+127 read.
-__device__ __forceinline__ void stem_rows(const ConvGemmArgs& a, int m0, int& g_lo, int& g_hi) {
-  const int HoWo = a.Ho * a.Wo;
-  const int m1 = min(m0 + kConvBM, a.M) - 1;
-  const int n0 = m0 / HoWo, n1 = m1 / HoWo;
-  g_lo = n0 * a.H + max(0, ((m0 - n0 * HoWo) / a.Wo) * a.stride_h - a.pad_h);
-  g_hi = n1 * a.H + min(a.H, ((m1 - n1 * HoWo) / a.Wo) * a.stride_h - a.pad_h + a.R);
-}
-
-// L2 prefetch of a tile's image rows, issued a few tiles ahead because every
+// L2 prefetch of the image rows a stem tile reads (one contiguous byte range:
+// NHWC rows of consecutive images are contiguous), issued ahead because every
 // tile of a persistent CTA touches rows no other tile of it did.
 __device__ __forceinline__ void stem_prefetch(const ConvGemmArgs& a, int m0) {
   if (m0 >= a.M) return;
-  int g_lo, g_hi;
-  stem_rows(a, m0, g_lo, g_hi);
+  const int HoWo = a.Ho * a.Wo;
+  const int m1 = min(m0 + kConvBM, a.M) - 1;
+  const int n0 = m0 / HoWo, n1 = m1 / HoWo;
+  const int g_lo = n0 * a.H + max(0, ((m0 - n0 * HoWo) / a.Wo) * a.stride_h - a.pad_h);
+  const int g_hi = n1 * a.H + min(a.H, ((m1 - n1 * HoWo) / a.Wo) * a.stride_h - a.pad_h + a.R);
   const size_t lo = static_cast<size_t>(g_lo) * a.W * 3, hi = static_cast<size_t>(g_hi) * a.W * 3;
   if (hi <= lo) return;
   const size_t lo16 = lo & ~static_cast<size_t>(15);
@@ -319,64 +352,67 @@ __device__ __forceinline__ void stem_prefetch(const ConvGemmArgs& a, int m0) {
   ptx::bulk_prefetch_l2(a.img + lo16, static_cast<uint32_t>(bytes));
 }
 
-__device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint8_t* smem, uint2* patch_ptr,
-                                            uint64_t* full, uint64_t* empty, int m0, uint32_t it,
-                                            int tg, int bar_id) {
-  const uint32_t patch = ptx::smem_u32(patch_ptr);
-  // 1. stage the patch
-  int g_lo, g_hi;
-  stem_rows(a, m0, g_lo, g_hi);
-  const int npx = (g_hi - g_lo) * a.W;
-  if (npx * 8 > kStemPatchBytes) __trap();  // the host checks every tile (conv_gemm_stem_fits)
-  named_bar_sync(bar_id, kStemGroupThreads);  // the previous tile's build is done with the patch
-  {
-    // batches of U pixels per thread: all 3U byte loads are issued before the
-    // first conversion, so a tile's patch costs about one memory round trip
-    constexpr int U = 10;
-    const uint8_t* src = a.img + static_cast<size_t>(g_lo) * a.W * 3;
-    for (int p0 = tg; p0 < npx; p0 += U * kStemGroupThreads) {
-      uint32_t b[U][3];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = p0 + u * kStemGroupThreads;
-        const uint8_t* q = src + static_cast<size_t>(p < npx ? p : 0) * 3;
-        b[u][0] = __ldg(q);
-        b[u][1] = __ldg(q + 1);
-        b[u][2] = __ldg(q + 2);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = p0 + u * kStemGroupThreads;
-        if (p < npx)
-          ptx::sts64(patch + p * 8,
-                     make_uint2(stem_norm2(b[u][0], b[u][1]), stem_norm2(b[u][2], 0u) & 0xFFFFu));
-      }
-    }
-  }
-  named_bar_sync(bar_id, kStemGroupThreads);  // patch complete
-
-  // 2. build A, one K block per pipeline stage
-  constexpr int GPR = 8;                        // 16 B granules per 128 B row
-  constexpr int RPP = kStemGroupThreads / GPR;  // 16 rows per pass
-  constexpr int PASSES = kConvBM / RPP;         // 8
-  const int gi = tg % GPR;
-  const int r0 = tg / GPR;
-  // per pass: input row/column of tap (0, 0) (may be padding) and its patch index
-  int hi0[PASSES], wi0[PASSES], pbase[PASSES];
-  {
-    const int HoWo = a.Ho * a.Wo;
-    const int m_first = m0 + r0;
-    int n = m_first / HoWo;
-    const int rem = m_first - n * HoWo;
+__device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem_a, uint64_t* full,
+                                            uint64_t* empty, int m0, uint32_t j, int lane) {
+  const int HoWo = a.Ho * a.Wo;
+  const int row_step = (a.W - a.S) * 3;
+  for (int kb = 0; kb < a.num_kb; ++kb) {
+    uint32_t s, use;
+    stem_slot(j, kb, a.num_kb, s, use);
+    if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
+    const int tap0 = kb * 16;
+    const int ntaps = min(16, a.taps - tap0);  // real taps in this K block (uniform)
+    const int dr0 = tap0 / a.S;
+    const int dc0 = tap0 - dr0 * a.S;
+    // lane l: tile rows l, l+32, l+64, l+96 (kept rolled: the body is large)
+    int m = m0 + lane;
+    int n = m / HoWo;
+    const int rem = m - n * HoWo;
     int ho = rem / a.Wo;
     int wo = rem - ho * a.Wo;
+#pragma unroll 1
+    for (int r = lane; r < (a.debug_flags & 8 ? 0 : kConvBM); r += 32, m += 32) {  // (flag 8: bring-up)
+      const int hi0 = ho * a.stride_h - a.pad_h;
+      const int wi0 = wo * a.stride_w - a.pad_w;
+      uint32_t rmask = 0, cmask = 0;  // kernel rows / columns inside the image
+      if (m < a.M) {
+        for (int d = 0; d < a.R; ++d)
+          rmask |= static_cast<uint32_t>(static_cast<unsigned>(hi0 + d) < static_cast<unsigned>(a.H)) << d;
+        for (int d = 0; d < a.S; ++d)
+          cmask |= static_cast<uint32_t>(static_cast<unsigned>(wi0 + d) < static_cast<unsigned>(a.W)) << d;
+      }
+      const uint8_t* base = a.img + (static_cast<long long>(n * a.H + hi0) * a.W + wi0) * 3;
+      const uint32_t rowa = smem_a + s * kABytes + r * 128;
+      const int sw = r & 7;
+      uint32_t px[16][3];
+      bool ok[16];
+      int dr = dr0, dc = dc0, off = (dr0 * a.W + dc0) * 3;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      const bool live = m_first + p * RPP < a.M;
-      hi0[p] = live ? ho * a.stride_h - a.pad_h : -(1 << 28);  // dead rows read zeros
-      wi0[p] = wo * a.stride_w - a.pad_w;
-      pbase[p] = (n * a.H + ho * a.stride_h - a.pad_h - g_lo) * a.W + wi0[p];
-      wo += RPP;
+      for (int e = 0; e < 16; ++e) {
+        ok[e] = e < ntaps && ((rmask >> dr) & (cmask >> dc) & 1u);
+        const uint8_t* src = ok[e] ? base + off : a.img;
+        px[e][0] = __ldg(src);
+        px[e][1] = __ldg(src + 1);
+        px[e][2] = __ldg(src + 2);
+        off += 3;
+        if (++dc == a.S) {
+          dc = 0;
+          ++dr;
+          off += row_step;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = 2 * g + u;
+          wv[2 * u] = ok[e] ? stem_norm2(px[e][0], px[e][1]) : 0u;
+          wv[2 * u + 1] = ok[e] ? stem_norm2(px[e][2], 0u) & 0xFFFFu : 0u;
+        }
+        ptx::sts128(rowa + ((g ^ sw) << 4), make_uint4(wv[0], wv[1], wv[2], wv[3]));
+      }
+      wo += 32;
       while (wo >= a.Wo) {
         wo -= a.Wo;
         if (++ho == a.Ho) {
@@ -385,37 +421,9 @@ __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint8_t* smem
         }
       }
     }
-  }
-  const uint32_t lane_off =
-      static_cast<uint32_t>(r0) * 128 + (static_cast<uint32_t>(gi ^ (r0 & 7)) << 4);
-  for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
-    const uint32_t s = it % a.stages;
-    if (it >= static_cast<uint32_t>(a.stages)) ptx::mbar_wait(&empty[s], ((it / a.stages) - 1) & 1);
-    int dr[2], dc[2], doff[2];
-    bool tv[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int tap = kb * 16 + gi * 2 + e;
-      tv[e] = tap < a.taps;
-      dr[e] = tap / a.S;
-      dc[e] = tap - dr[e] * a.S;
-      doff[e] = dr[e] * a.W + dc[e];
-    }
-    const uint32_t sp = ptx::smem_u32(smem) + s * kABytes + lane_off;
-#pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      uint2 v[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool ok = tv[e] &&
-                        static_cast<unsigned>(hi0[p] + dr[e]) < static_cast<unsigned>(a.H) &&
-                        static_cast<unsigned>(wi0[p] + dc[e]) < static_cast<unsigned>(a.W);
-        v[e] = ok ? ptx::lds64(patch + (pbase[p] + doff[e]) * 8) : make_uint2(0u, 0u);
-      }
-      ptx::sts128(sp + p * RPP * 128, make_uint4(v[0].x, v[0].y, v[1].x, v[1].y));
-    }
     ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core (async proxy) reads
-    ptx::mbar_arrive(&full[s]);
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&full[s]);
   }
 }
 
@@ -557,8 +565,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // pointer in the shared window so accesses through it compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int epi_warps = 4 * args.teams;
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps,
-                                   MODE == static_cast<int>(ConvLoadMode::kStemU8) ? 2 * kStemPatchBytes : 0);
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res);
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x)
@@ -568,25 +575,29 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* empty = full + args.stages;
   uint64_t* tmem_full = empty + args.stages;  // [n_acc]
   uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + kMaxAcc);
+  uint64_t* b_full = tmem_empty + kMaxAcc;    // resident B landed (b_res)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
   const int tiles = n_tiles * ((args.M + kConvBM - 1) / kConvBM);
-  const int n_acc = args.n_acc;
+  const int n_acc = args.n_acc;  // power of two
+  const int acc_log2 = __ffs(n_acc) - 1;
   const uint32_t acc_stride = args.tmem_cols / n_acc;
+  constexpr bool kStem = MODE == static_cast<int>(ConvLoadMode::kStemU8);
 
   if (warp == kTmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < args.stages; ++s) {
         const uint32_t producers = kTmaA ? 0u
                                    : MODE == static_cast<int>(ConvLoadMode::kStemU8)
-                                       ? static_cast<uint32_t>(kStemGroupThreads)
+                                       ? 1u  // one arrival per producer warp (lane 0)
                                        : kGatherWarps * 32u;
-        ptx::mbar_init(&full[s], producers + 1u);
+        ptx::mbar_init(&full[s], producers + (kTmaA || args.b_res == 0 ? 1u : 0u));
         ptx::mbar_init(&empty[s], 1);
       }
+      ptx::mbar_init(b_full, 1);
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
         ptx::mbar_init(&tmem_empty[b], 4);  // one arrival per warp of the owning team
@@ -615,12 +626,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;
     const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
     uint32_t j = 0, groups = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
-      if (static_cast<int>(j % args.teams) != team) continue;
-      const int m0 = (tile / n_tiles) * kConvBM;
-      const int n0 = (tile % n_tiles) * args.BN;
-      const uint32_t acc = j % n_acc;
-      ptx::mbar_wait(&tmem_full[acc], (j / n_acc) & 1);
+    TileWalk tw(n_tiles);
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j, tw.next()) {
+      if (static_cast<int>(j & (args.teams - 1)) != team) continue;  // teams: power of two
+      const int m0 = tw.mb * kConvBM;
+      const int n0 = tw.nb * args.BN;
+      const uint32_t acc = j & (n_acc - 1);
+      ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
       ptx::tc_fence_after();
       const int m = m0 + quarter * 32 + lane;
       const uint32_t t_row =
@@ -663,51 +675,65 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) ptx::bulk_wait<0>();
   } else if (warp < kGatherWarp0 + kGatherWarps) {
     if constexpr (MODE == static_cast<int>(ConvLoadMode::kStemU8)) {
-      // two producer groups on alternate tiles; tile j's K blocks are
-      // pipeline iterations j*num_kb ..
-      const int tg = threadIdx.x - kGatherWarp0 * 32;
-      const int grp = tg / kStemGroupThreads;
+      // one producer warp per tile (tile j -> gather warp j % 8); tile j's
+      // K blocks are pipeline iterations j*num_kb ..
+      // (the stem conv has one N tile: tile index == M block)
+      const int pw = warp - kGatherWarp0;
       uint32_t j = 0;
-      const int row = tg % kStemGroupThreads;
-      uint2* patch = reinterpret_cast<uint2*>(smem + L.patch_off + grp * kStemPatchBytes);
-      if (row == 0) {  // warm up: this group's first two tiles
-        stem_prefetch(args, ((blockIdx.x + grp * gridDim.x) / n_tiles) * kConvBM);
-        stem_prefetch(args, ((blockIdx.x + (grp + 2) * gridDim.x) / n_tiles) * kConvBM);
+      if (lane == 0) {  // warm up: this warp's first two tiles
+        stem_prefetch(args, (blockIdx.x + pw * gridDim.x) * kConvBM);
+        stem_prefetch(args, (blockIdx.x + (pw + kGatherWarps) * gridDim.x) * kConvBM);
       }
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
-        if (static_cast<int>(j & 1) != grp) continue;
-        if (row == 0)  // two of this group's tiles ahead
-          stem_prefetch(args, ((tile + 4 * gridDim.x) / n_tiles) * kConvBM);
-        stem_a_tile(args, smem + L.a_off, patch, full, empty, (tile / n_tiles) * kConvBM,
-                    j * static_cast<uint32_t>(args.num_kb), row, 1 + grp);
+        if (static_cast<int>(j % kGatherWarps) != pw) continue;
+        if (lane == 0)  // two of this warp's tiles ahead
+          stem_prefetch(args, (tile + 2 * kGatherWarps * gridDim.x) * kConvBM);
+        stem_a_tile(args, ptx::smem_u32(smem + L.a_off), full, empty, tile * kConvBM, j, lane);
       }
     } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile / n_tiles) * kConvBM;
+      RingPos rp;
+      TileWalk tw(n_tiles);
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
+        const int m0 = tw.mb * kConvBM;
         if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather16))
-          gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, it);
+          gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
         else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8))
-          gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, it);
+          gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, rp);
         else
-          dw_a_tile(args, smem + L.a_off, full, empty, m0, it);
+          dw_a_tile(args, smem + L.a_off, full, empty, m0, rp);
       }
     }
   } else if (warp == kTmaWarp) {
     if (lane == 0) {
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      const uint32_t tx = b_bytes + (kTmaA ? kABytes : 0);
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile / n_tiles) * kConvBM;
-        const int n0 = (tile % n_tiles) * args.BN;
-        for (int kb = 0; kb < args.num_kb; ++kb, ++it) {
-          const uint32_t s = it % args.stages;
-          if (it >= static_cast<uint32_t>(args.stages))
-            ptx::mbar_wait(&empty[s], ((it / args.stages) - 1) & 1);
+      const bool b_res = args.b_res > 0;
+      if (b_res) {  // the whole weight matrix, once
+        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
+        for (int kb = 0; kb < args.num_kb; ++kb)
+          ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
+                           kb * kConvBK, 0);
+      }
+      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? kABytes : 0);
+      uint32_t j = 0;
+      RingPos rp;
+      TileWalk tw(n_tiles);
+      for (int tile = blockIdx.x; tile < (tx ? tiles : 0); tile += gridDim.x, ++j, tw.next()) {
+        const int m0 = tw.mb * kConvBM;
+        const int n0 = tw.nb * args.BN;
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          uint32_t s, use;
+          if constexpr (kStem) {
+            stem_slot(j, kb, args.num_kb, s, use);
+          } else {
+            s = rp.slot;
+            use = rp.lap;
+            rp.next(args.stages);
+          }
+          if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
           ptx::mbar_arrive_expect_tx(&full[s], tx);
-          ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
-                           kb * kConvBK, n0);
+          if (!b_res)
+            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
+                             kb * kConvBK, n0);
           if constexpr (kTmaA)
             ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * kABytes), &args.tmap_a, &full[s],
                              kb * kConvBK, m0);
@@ -718,21 +744,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      uint32_t it = 0, j = 0;
+      if (args.b_res > 0) ptx::mbar_wait(b_full, 0);
+      uint32_t j = 0;
+      RingPos rp;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
-        const uint32_t acc = j % n_acc;
-        if (j >= static_cast<uint32_t>(n_acc)) ptx::mbar_wait(&tmem_empty[acc], ((j / n_acc) - 1) & 1);
+        const uint32_t acc = j & (n_acc - 1);
+        if (j >= static_cast<uint32_t>(n_acc))
+          ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
-        for (int kb = 0; kb < args.num_kb; ++kb, ++it) {
-          const uint32_t s = it % args.stages;
-          ptx::mbar_wait(&full[s], (it / args.stages) & 1);
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          uint32_t s, use;
+          if constexpr (kStem) {
+            stem_slot(j, kb, args.num_kb, s, use);
+          } else {
+            s = rp.slot;
+            use = rp.lap;
+            rp.next(args.stages);
+          }
+          ptx::mbar_wait(&full[s], use & 1);
           ptx::tc_fence_after();
           if constexpr (!kTmaA) ptx::fence_proxy_async_smem();
           const uint64_t da =
               ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.a_off + s * kABytes));
           const uint64_t db =
-              ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + s * b_bytes));
+              ptx::umma_desc_sw128_kmajor(
+                  ptx::smem_u32(smem + L.b_off + (args.b_res > 0 ? kb : static_cast<int>(s)) * b_bytes));
 #pragma unroll
           for (int k = 0; k < kConvBK / 16; ++k) {
             // +32 B along K inside the swizzle row = +2 in the >>4 start field.
@@ -835,31 +872,25 @@ uint32_t pow2_at_least(int x) {
 }
 }  // namespace
 
-int conv_gemm_stages(int BN, int cout, int epi_warps, int patch_bytes) {
+int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks) {
   const int ctas = 1;  // 18 warps: one CTA per SM
-  const int per_stage = kABytes + BN * kConvBK * 2;
+  const int per_stage = kABytes + (b_res_blocks > 0 ? 0 : BN * kConvBK * 2);
   const int fixed =
-      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, patch_bytes).total) + 64 * 8 + 1024;
+      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, b_res_blocks).total) + 64 * 8 + 1024;
   const int budget = (227 * 1024) / ctas - fixed;
   return std::max(1, std::min(kConvMaxStages, budget / per_stage));
 }
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int patch_bytes) {
-  return smem_layout(BN, stages, cout, epi_warps, patch_bytes).total + 1024;  // + alignment slack
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks) {
+  return smem_layout(BN, stages, cout, epi_warps, b_res_blocks).total + 1024;  // + alignment slack
 }
 
-bool conv_gemm_stem_fits(int H, int W, int R, int stride_h, int pad_h, int Ho, int Wo) {
-  // the device's row range (stem_rows) for every tile of a 256-image batch
-  // (tile starts repeat with the image period well within that)
-  const long long howo = static_cast<long long>(Ho) * Wo, M = 256 * howo;
-  for (long long m0 = 0; m0 < M; m0 += kConvBM) {
-    const long long m1 = std::min(m0 + kConvBM, M) - 1;
-    const long long n0 = m0 / howo, n1 = m1 / howo;
-    const long long lo = n0 * H + std::max(0LL, ((m0 - n0 * howo) / Wo) * stride_h - pad_h);
-    const long long hi = n1 * H + std::min<long long>(H, ((m1 - n1 * howo) / Wo) * stride_h - pad_h + R);
-    if ((hi - lo) * W * 8 > kStemPatchBytes) return false;
-  }
-  return true;
+bool conv_gemm_stem_fits(int R, int S, int cout) {
+  // kernel-row / kernel-column masks are 16-bit fields; eight ring slots
+  // (one per producer warp) with one epilogue team must fit in shared memory
+  if (R > 16 || S > 16) return false;
+  int bn = cout <= 256 ? (cout + 15) / 16 * 16 : 256;
+  return conv_gemm_stages(bn, cout, 4, 0) >= kGatherWarps;
 }
 
 cudaError_t conv_gemm_init() {
@@ -912,8 +943,26 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.teams = std::min(mode == ConvLoadMode::kTmaA && args.BN <= 64 ? kMaxEpiWarps / 4
                                                                       : kEpiWarps / 4,
                         args.n_acc);
-  const int patch = mode == ConvLoadMode::kStemU8 ? 2 * kStemPatchBytes : 0;
+  // B resident in smem when the layer has one N tile and a small K: no
+  // per-tile weight loads (and no TMA hop on the operand ring's critical path)
+  const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
+  static const bool b_res_on = [] {
+    const char* e = std::getenv("DS_B_RESIDENT");
+    return !(e && e[0] == '0');
+  }();
+  args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
+  const int patch = args.b_res;
   args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, patch);
+  if (mode == ConvLoadMode::kStemU8) {
+    // one private slot per producer warp (ring_slot); drop to one epilogue
+    // team if that is what makes eight slots fit
+    if (args.stages < kGatherWarps) {
+      args.teams = 1;
+      args.stages = conv_gemm_stages(args.BN, args.Cout, 4, patch);
+    }
+    if (args.stages < kGatherWarps) return cudaErrorInvalidValue;
+    args.stages = kGatherWarps;
+  }
   const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, patch);
   const int tiles = ((args.Cout + args.BN - 1) / args.BN) * ((args.M + kConvBM - 1) / kConvBM);
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
