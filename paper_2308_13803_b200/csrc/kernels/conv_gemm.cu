@@ -61,10 +61,10 @@ struct SmemLayout {
 // BN x 64) stays resident in shared memory for all tiles (one N tile, small
 // K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
-                                                  int b_res_blocks = 0) {
+                                                  int b_res_blocks = 0, int mt = 1) {
   SmemLayout L;
   L.a_off = 0;
-  L.b_off = static_cast<uint32_t>(stages) * kABytes;
+  L.b_off = static_cast<uint32_t>(stages) * mt * kABytes;  // stage = mt A sub-tiles
   const int b_blocks = b_res_blocks > 0 ? b_res_blocks : stages;
   L.y_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;
   L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
@@ -108,15 +108,16 @@ struct TileWalk {
   }
 };
 
-// kStemU8: each of the eight gather warps produces whole tiles on its own
-// (tile j -> warp j % 8) and owns ring slot j % 8 (stages == 8), so its waits
-// on that slot stay in order (a shared ring would let one warp wait on a slot
-// two phases ahead, which a parity wait cannot tell apart). `use` counts
-// earlier uses of the slot.
-__device__ __forceinline__ void stem_slot(uint32_t j, int kb, int num_kb, uint32_t& slot,
-                                          uint32_t& use) {
-  slot = j % kGatherWarps;
-  use = (j / kGatherWarps) * static_cast<uint32_t>(num_kb) + static_cast<uint32_t>(kb);
+// kStemU8: the eight gather warps form 8/mt groups of mt warps; a group
+// produces whole tiles on its own (tile j -> group j % groups, warp q of the
+// group fills sub-tile q) and owns ring slot j % groups (stages == groups),
+// so its waits on that slot stay in order (a shared ring would let one group
+// wait on a slot two phases ahead, which a parity wait cannot tell apart).
+// `use` counts earlier uses of the slot.
+__device__ __forceinline__ void stem_slot(uint32_t j, int kb, int num_kb, int groups,
+                                          uint32_t& slot, uint32_t& use) {
+  slot = j % static_cast<uint32_t>(groups);
+  use = (j / static_cast<uint32_t>(groups)) * static_cast<uint32_t>(num_kb) + static_cast<uint32_t>(kb);
 }
 
 // Gathers the A tiles of one output tile (128 im2col rows) for every K
@@ -353,12 +354,17 @@ __device__ __forceinline__ void stem_prefetch(const ConvGemmArgs& a, int m0) {
 }
 
 __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem_a, uint64_t* full,
-                                            uint64_t* empty, int m0, uint32_t j, int lane) {
+                                            uint64_t* empty, int m0, uint32_t j, int lane, int q,
+                                            int groups) {
+  // sub-tile q of the tile at m0 (rows m0 + 128 q ..)
+  const uint32_t a_stage = static_cast<uint32_t>(a.mt) * kABytes;
+  m0 += q * kConvBM;
+  smem_a += q * kABytes;
   const int HoWo = a.Ho * a.Wo;
   const int row_step = (a.W - a.S) * 3;
   for (int kb = 0; kb < a.num_kb; ++kb) {
     uint32_t s, use;
-    stem_slot(j, kb, a.num_kb, s, use);
+    stem_slot(j, kb, a.num_kb, groups, s, use);
     if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
     const int tap0 = kb * 16;
     const int ntaps = min(16, a.taps - tap0);  // real taps in this K block (uniform)
@@ -382,7 +388,7 @@ __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem
           cmask |= static_cast<uint32_t>(static_cast<unsigned>(wi0 + d) < static_cast<unsigned>(a.W)) << d;
       }
       const uint8_t* base = a.img + (static_cast<long long>(n * a.H + hi0) * a.W + wi0) * 3;
-      const uint32_t rowa = smem_a + s * kABytes + r * 128;
+      const uint32_t rowa = smem_a + s * a_stage + r * 128;
       const int sw = r & 7;
       uint32_t px[16][3];
       bool ok[16];
@@ -565,7 +571,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // pointer in the shared window so accesses through it compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int epi_warps = 4 * args.teams;
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res);
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt);
+  const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
+  const uint32_t a_stage = static_cast<uint32_t>(mt) * kABytes;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x)
@@ -581,7 +589,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
-  const int tiles = n_tiles * ((args.M + kConvBM - 1) / kConvBM);
+  const int tile_rows = kConvBM * mt;
+  const int tiles = n_tiles * ((args.M + tile_rows - 1) / tile_rows);
   const int n_acc = args.n_acc;  // power of two
   const int acc_log2 = __ffs(n_acc) - 1;
   const uint32_t acc_stride = args.tmem_cols / n_acc;
@@ -592,7 +601,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int s = 0; s < args.stages; ++s) {
         const uint32_t producers = kTmaA ? 0u
                                    : MODE == static_cast<int>(ConvLoadMode::kStemU8)
-                                       ? 1u  // one arrival per producer warp (lane 0)
+                                       ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
         ptx::mbar_init(&full[s], producers + (kTmaA || args.b_res == 0 ? 1u : 0u));
         ptx::mbar_init(&empty[s], 1);
@@ -629,43 +638,46 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     TileWalk tw(n_tiles);
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j, tw.next()) {
       if (static_cast<int>(j & (args.teams - 1)) != team) continue;  // teams: power of two
-      const int m0 = tw.mb * kConvBM;
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
       ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
       ptx::tc_fence_after();
-      const int m = m0 + quarter * 32 + lane;
-      const uint32_t t_row =
-          tmem_base + acc * acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
-      if (args.debug_flags & 1) {
-        // release only
-      } else if (args.y_tma) {
-        for (int g0 = 0; g0 < args.BN && n0 + g0 < args.Cout; g0 += group_cols) {
-          uint8_t* group = ystage + (groups & 1) * kYStageBytes;
-          if (groups >= 2) {  // the store issued two groups ago must have read `group`
-            if (lane == 0) ptx::bulk_wait_read<1>();
+      for (int q = 0; q < mt; ++q) {  // sub-tile q: rows m0 .. m0+127, columns q*BN ..
+        const int m0 = tw.mb * tile_rows + q * kConvBM;
+        if (m0 >= args.M) break;
+        const int m = m0 + quarter * 32 + lane;
+        const uint32_t t_row = tmem_base + acc * acc_stride + q * args.BN +
+                               (static_cast<uint32_t>(quarter * 32) << 16);
+        if (args.debug_flags & 1) {
+          // release only
+        } else if (args.y_tma) {
+          for (int g0 = 0; g0 < args.BN && n0 + g0 < args.Cout; g0 += group_cols) {
+            uint8_t* group = ystage + (groups & 1) * kYStageBytes;
+            if (groups >= 2) {  // the store issued two groups ago must have read `group`
+              if (lane == 0) ptx::bulk_wait_read<1>();
+              __syncwarp();
+            }
+            for (int c = 0; c < group_cols && g0 + c < args.BN; c += 32) {
+              uint32_t raw[32];
+              ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
+              ptx::tmem_ld_wait();
+              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane);
+            }
+            ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+              ptx::bulk_commit();
+            }
+            ++groups;
           }
-          for (int c = 0; c < group_cols && g0 + c < args.BN; c += 32) {
-            uint32_t raw[32];
-            ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
+        } else {
+          for (int c0 = 0; c0 < args.BN && n0 + c0 < args.Cout; c0 += 16) {
+            uint32_t raw[16];
+            ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
             ptx::tmem_ld_wait();
-            epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane);
+            if (m < args.M) epilogue_chunk(args, bias_s, m, n0 + c0, raw);
           }
-          ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
-            ptx::bulk_commit();
-          }
-          ++groups;
-        }
-      } else {
-        for (int c0 = 0; c0 < args.BN && n0 + c0 < args.Cout; c0 += 16) {
-          uint32_t raw[16];
-          ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
-          ptx::tmem_ld_wait();
-          if (m < args.M) epilogue_chunk(args, bias_s, m, n0 + c0, raw);
         }
       }
       ptx::tc_fence_before();
@@ -679,16 +691,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       // K blocks are pipeline iterations j*num_kb ..
       // (the stem conv has one N tile: tile index == M block)
       const int pw = warp - kGatherWarp0;
+      const int groups = kGatherWarps / mt;
+      const int grp = pw / mt, q = pw % mt;
       uint32_t j = 0;
-      if (lane == 0) {  // warm up: this warp's first two tiles
-        stem_prefetch(args, (blockIdx.x + pw * gridDim.x) * kConvBM);
-        stem_prefetch(args, (blockIdx.x + (pw + kGatherWarps) * gridDim.x) * kConvBM);
+      if (lane == 0) {  // warm up: this group's first two tiles
+        stem_prefetch(args, (blockIdx.x + grp * gridDim.x) * tile_rows + q * kConvBM);
+        stem_prefetch(args, (blockIdx.x + (grp + groups) * gridDim.x) * tile_rows + q * kConvBM);
       }
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
-        if (static_cast<int>(j % kGatherWarps) != pw) continue;
-        if (lane == 0)  // two of this warp's tiles ahead
-          stem_prefetch(args, (tile + 2 * kGatherWarps * gridDim.x) * kConvBM);
-        stem_a_tile(args, ptx::smem_u32(smem + L.a_off), full, empty, tile * kConvBM, j, lane);
+        if (static_cast<int>(j % groups) != grp) continue;
+        if (lane == 0)  // two of this group's tiles ahead
+          stem_prefetch(args, (tile + 2 * groups * gridDim.x) * tile_rows + q * kConvBM);
+        stem_a_tile(args, ptx::smem_u32(smem + L.a_off), full, empty, tile * tile_rows, j, lane, q,
+                    groups);
       }
     } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
       RingPos rp;
@@ -713,17 +728,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
                            kb * kConvBK, 0);
       }
-      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? kABytes : 0);
+      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0);
       uint32_t j = 0;
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < (tx ? tiles : 0); tile += gridDim.x, ++j, tw.next()) {
-        const int m0 = tw.mb * kConvBM;
+        const int m0 = tw.mb * tile_rows;
         const int n0 = tw.nb * args.BN;
         for (int kb = 0; kb < args.num_kb; ++kb) {
           uint32_t s, use;
           if constexpr (kStem) {
-            stem_slot(j, kb, args.num_kb, s, use);
+            stem_slot(j, kb, args.num_kb, kGatherWarps / mt, s, use);
           } else {
             s = rp.slot;
             use = rp.lap;
@@ -735,8 +750,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                              kb * kConvBK, n0);
           if constexpr (kTmaA)
-            ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * kABytes), &args.tmap_a, &full[s],
-                             kb * kConvBK, m0);
+            for (int q = 0; q < mt; ++q)  // (rows past M arrive as zeros)
+              ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes),
+                               &args.tmap_a, &full[s], kb * kConvBK, m0 + q * kConvBM);
         }
       }
     }
@@ -756,7 +772,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         for (int kb = 0; kb < args.num_kb; ++kb) {
           uint32_t s, use;
           if constexpr (kStem) {
-            stem_slot(j, kb, args.num_kb, s, use);
+            stem_slot(j, kb, args.num_kb, kGatherWarps / mt, s, use);
           } else {
             s = rp.slot;
             use = rp.lap;
@@ -764,16 +780,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
           ptx::mbar_wait(&full[s], use & 1);
           ptx::tc_fence_after();
-          if constexpr (!kTmaA) ptx::fence_proxy_async_smem();
-          const uint64_t da =
-              ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.a_off + s * kABytes));
           const uint64_t db =
               ptx::umma_desc_sw128_kmajor(
                   ptx::smem_u32(smem + L.b_off + (args.b_res > 0 ? kb : static_cast<int>(s)) * b_bytes));
+          for (int q = 0; q < mt && !(args.debug_flags & 16); ++q) {  // (flag 16: bring-up)
+            const uint64_t da = ptx::umma_desc_sw128_kmajor(
+                ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes));
 #pragma unroll
-          for (int k = 0; k < kConvBK / 16; ++k) {
-            // +32 B along K inside the swizzle row = +2 in the >>4 start field.
-            ptx::umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < kConvBK / 16; ++k) {
+              // +32 B along K inside the swizzle row = +2 in the >>4 start field.
+              ptx::umma_bf16(d + q * args.BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            }
           }
           ptx::umma_commit(&empty[s]);
         }
@@ -872,17 +889,17 @@ uint32_t pow2_at_least(int x) {
 }
 }  // namespace
 
-int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks) {
+int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks, int mt) {
   const int ctas = 1;  // 18 warps: one CTA per SM
-  const int per_stage = kABytes + (b_res_blocks > 0 ? 0 : BN * kConvBK * 2);
+  const int per_stage = mt * kABytes + (b_res_blocks > 0 ? 0 : BN * kConvBK * 2);
   const int fixed =
-      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, b_res_blocks).total) + 64 * 8 + 1024;
+      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, b_res_blocks, mt).total) + 64 * 8 + 1024;
   const int budget = (227 * 1024) / ctas - fixed;
   return std::max(1, std::min(kConvMaxStages, budget / per_stage));
 }
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks) {
-  return smem_layout(BN, stages, cout, epi_warps, b_res_blocks).total + 1024;  // + alignment slack
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks, int mt) {
+  return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt).total + 1024;  // + alignment slack
 }
 
 bool conv_gemm_stem_fits(int R, int S, int cout) {
@@ -932,17 +949,32 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   ConvGemmArgs args = in_args;
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
+  // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
+  // one ring stage, one accumulator (mt x BN columns) and one trip through
+  // the barriers, amortising the per-tile MMA-issue / barrier latency that
+  // bounds small-N layers. DS_CONV_MT=1 forces single sub-tiles (A/B).
+  auto env_int = [](const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::max(1, std::min(4, std::atoi(e))) : dflt;
+  };
+  static const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
+                   teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
+  const int mt_cap = mode == ConvLoadMode::kStemU8 ? mt_stem
+                     : mode == ConvLoadMode::kTmaA ? mt_tma
+                                                   : 1;
+  args.mt = 1;
+  while (args.mt * 2 <= mt_cap && args.mt * 2 * static_cast<int>(pow2_at_least(args.BN)) <= 256)
+    args.mt *= 2;
   // TMEM: as many accumulators as 512 columns hold (2..kMaxAcc), so the MMA
   // runs ahead of the epilogue; epilogue teams: 2, or 4 when the gather warps
-  // are idle (TMA-A), never more than the accumulators.
-  const uint32_t bn_cols = pow2_at_least(args.BN);
-  args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / bn_cols)));
-  args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(bn_cols));
-  // (four teams only for BN <= 64, where their staging buffers still leave a
-  // 4-deep operand ring)
-  args.teams = std::min(mode == ConvLoadMode::kTmaA && args.BN <= 64 ? kMaxEpiWarps / 4
-                                                                      : kEpiWarps / 4,
+  // are idle (TMA-A) and tiles are single small ones, never more than the
+  // accumulators.
+  const uint32_t acc_cols = pow2_at_least(args.mt * args.BN);
+  args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / acc_cols)));
+  args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(acc_cols));
+  args.teams = std::min(mode == ConvLoadMode::kTmaA && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
+  if (args.teams == 3) args.teams = 2;  // a power of two
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
@@ -951,20 +983,23 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     return !(e && e[0] == '0');
   }();
   args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
-  const int patch = args.b_res;
-  args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, patch);
+  const int bres = args.b_res;
+  args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, bres, args.mt);
   if (mode == ConvLoadMode::kStemU8) {
-    // one private slot per producer warp (ring_slot); drop to one epilogue
-    // team if that is what makes eight slots fit
-    if (args.stages < kGatherWarps) {
+    // one private slot per producer group (stem_slot); drop to one epilogue
+    // team if that is what makes the slots fit
+    const int groups = kGatherWarps / args.mt;
+    if (args.stages < groups) {
       args.teams = 1;
-      args.stages = conv_gemm_stages(args.BN, args.Cout, 4, patch);
+      args.stages = conv_gemm_stages(args.BN, args.Cout, 4, bres, args.mt);
     }
-    if (args.stages < kGatherWarps) return cudaErrorInvalidValue;
-    args.stages = kGatherWarps;
+    if (args.stages < groups) return cudaErrorInvalidValue;
+    args.stages = groups;
   }
-  const size_t smem = conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, patch);
-  const int tiles = ((args.Cout + args.BN - 1) / args.BN) * ((args.M + kConvBM - 1) / kConvBM);
+  const size_t smem =
+      conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
+  const int tiles =
+      n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);

@@ -42,6 +42,7 @@ struct ConvGemmArgs {
   // launch_conv_gemm from the mode and BN.
   int teams, n_acc;
   int b_res;  // > 0: all num_kb weight blocks resident in smem (one N tile)
+  int mt;     // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;
@@ -87,7 +88,8 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
                       int box_w, int box_h, int box_n = 1);
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps = 8, int b_res_blocks = 0);
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps = 8, int b_res_blocks = 0,
+                            int mt = 1);
 
 // kStemU8 needs eight operand-ring slots (one per producer warp) next to one
 // epilogue team; false when this stem cannot have them (the runtime then
@@ -97,7 +99,7 @@ bool conv_gemm_stem_fits(int R, int S, int cout);
 // Operand-ring depth for an N tile: as deep as kConvMaxStages allows within
 // the per-CTA budget, where two CTAs share an SM whenever their TMEM
 // (2 x BN accumulator columns each) fits.
-int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0);
+int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0, int mt = 1);
 uint32_t conv_gemm_tmem_cols(int BN);
 
 // Must run once per device before the first launch (and before any capture).

@@ -38,17 +38,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Blocks until the phase with the given parity has completed.
+// Blocks until the phase with the given parity has completed. The suspend
+// time hint lets the hardware park the warp until the phase flips (it wakes on
+// completion) instead of returning early: a plain try_wait loop re-issues
+// every few cycles and steals issue slots from the warps doing the work.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t"
       ".reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t"
       "}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 
