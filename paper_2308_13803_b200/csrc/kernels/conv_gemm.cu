@@ -353,6 +353,11 @@ __device__ __forceinline__ void stem_prefetch(const ConvGemmArgs& a, int m0) {
   ptx::bulk_prefetch_l2(a.img + lo16, static_cast<uint32_t>(bytes));
 }
 
+// Bits [lo, hi) of a mask (empty when hi <= lo); lo, hi in [0, 16].
+__device__ __forceinline__ uint32_t bit_range(int lo, int hi) {
+  return hi > lo ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
+}
+
 __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem_a, uint64_t* full,
                                             uint64_t* empty, int m0, uint32_t j, int lane, int q,
                                             int groups) {
@@ -361,15 +366,11 @@ __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem
   m0 += q * kConvBM;
   smem_a += q * kABytes;
   const int HoWo = a.Ho * a.Wo;
-  const int row_step = (a.W - a.S) * 3;
   for (int kb = 0; kb < a.num_kb; ++kb) {
     uint32_t s, use;
     stem_slot(j, kb, a.num_kb, groups, s, use);
     if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
-    const int tap0 = kb * 16;
-    const int ntaps = min(16, a.taps - tap0);  // real taps in this K block (uniform)
-    const int dr0 = tap0 / a.S;
-    const int dc0 = tap0 - dr0 * a.S;
+    const int ntaps = min(16, a.taps - kb * 16);  // real taps in this K block (uniform)
     // lane l: tile rows l, l+32, l+64, l+96 (kept rolled: the body is large)
     int m = m0 + lane;
     int n = m / HoWo;
@@ -380,32 +381,23 @@ __device__ __forceinline__ void stem_a_tile(const ConvGemmArgs& a, uint32_t smem
     for (int r = lane; r < (a.debug_flags & 8 ? 0 : kConvBM); r += 32, m += 32) {  // (flag 8: bring-up)
       const int hi0 = ho * a.stride_h - a.pad_h;
       const int wi0 = wo * a.stride_w - a.pad_w;
-      uint32_t rmask = 0, cmask = 0;  // kernel rows / columns inside the image
-      if (m < a.M) {
-        for (int d = 0; d < a.R; ++d)
-          rmask |= static_cast<uint32_t>(static_cast<unsigned>(hi0 + d) < static_cast<unsigned>(a.H)) << d;
-        for (int d = 0; d < a.S; ++d)
-          cmask |= static_cast<uint32_t>(static_cast<unsigned>(wi0 + d) < static_cast<unsigned>(a.W)) << d;
-      }
+      // kernel rows / columns that fall inside the image (none for rows >= M)
+      const uint32_t rmask = m < a.M ? bit_range(max(0, -hi0), min(a.R, a.H - hi0)) : 0u;
+      const uint32_t cmask = bit_range(max(0, -wi0), min(a.S, a.W - wi0));
       const uint8_t* base = a.img + (static_cast<long long>(n * a.H + hi0) * a.W + wi0) * 3;
       const uint32_t rowa = smem_a + s * a_stage + r * 128;
       const int sw = r & 7;
       uint32_t px[16][3];
       bool ok[16];
-      int dr = dr0, dc = dc0, off = (dr0 * a.W + dc0) * 3;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        ok[e] = e < ntaps && ((rmask >> dr) & (cmask >> dc) & 1u);
-        const uint8_t* src = ok[e] ? base + off : a.img;
+        const int info = a.tap_info[(kb * 16 + e) & 63];
+        ok[e] = e < ntaps && ((rmask >> ((info >> 24) & 15)) & (cmask >> ((info >> 28) & 15)) & 1u);
+        const uint8_t* src = base + (ok[e] ? (info & 0xFFFFFF) : 0);
+        src = ok[e] ? src : a.img;
         px[e][0] = __ldg(src);
         px[e][1] = __ldg(src + 1);
         px[e][2] = __ldg(src + 2);
-        off += 3;
-        if (++dc == a.S) {
-          dc = 0;
-          ++dr;
-          off += row_step;
-        }
       }
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
@@ -905,7 +897,7 @@ size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_r
 bool conv_gemm_stem_fits(int R, int S, int cout) {
   // kernel-row / kernel-column masks are 16-bit fields; eight ring slots
   // (one per producer warp) with one epilogue team must fit in shared memory
-  if (R > 16 || S > 16) return false;
+  if (R > 15 || S > 15 || R * S > 64) return false;
   int bn = cout <= 256 ? (cout + 15) / 16 * 16 : 256;
   return conv_gemm_stages(bn, cout, 4, 0) >= kGatherWarps;
 }
@@ -995,6 +987,13 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     }
     if (args.stages < groups) return cudaErrorInvalidValue;
     args.stages = groups;
+  }
+  if (mode == ConvLoadMode::kStemU8) {
+    if (args.taps > 64 || args.R > 15 || args.S > 15) return cudaErrorInvalidValue;
+    for (int t = 0; t < 64; ++t) {
+      const int r = t < args.taps ? t / args.S : 0, c = t < args.taps ? t % args.S : 0;
+      args.tap_info[t] = ((r * args.W + c) * 3) | (r << 24) | (c << 28);
+    }
   }
   const size_t smem =
       conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);

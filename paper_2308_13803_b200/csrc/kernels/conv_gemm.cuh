@@ -60,6 +60,9 @@ struct ConvGemmArgs {
   // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
   // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
   const uint8_t* img;
+  // kStemU8 tap table (launch_conv_gemm fills it): tap t = r*S + s ->
+  // byte offset (r*W + s)*3 | r << 24 | s << 28
+  int tap_info[64];
 };
 
 enum class ConvLoadMode : int {
