@@ -54,22 +54,26 @@ constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
 constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
 
 struct SmemLayout {
-  uint32_t a_off, b_off, y_off, bar_off, bias_off, total;
+  uint32_t a_off, b_off, box_off, y_off, bar_off, bias_off, total;
 };
 
 // b_res_blocks > 0: the layer's whole weight matrix (num_kb blocks of
 // BN x 64) stays resident in shared memory for all tiles (one N tile, small
 // K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
-                                                  int b_res_blocks = 0, int mt = 1) {
+                                                  int b_res_blocks = 0, int mt = 1,
+                                                  int box_bytes = 0) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * mt * kABytes;  // stage = mt A sub-tiles
   const int b_blocks = b_res_blocks > 0 ? b_res_blocks : stages;
-  L.y_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;
+  L.box_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;  // kDwFused halo boxes
+  // (box slots rounded to 1 KiB: the 128 B-swizzled staging after them needs it)
+  L.y_off = L.box_off + static_cast<uint32_t>(stages) * ((box_bytes + 1023) / 1024 * 1024);
   L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
-  // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full, tmem slot
-  L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 2) * 8 + 15) / 16 * 16;
+  // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
+  // box_full[stages], tmem slot
+  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
   L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
@@ -211,100 +215,102 @@ __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Depthwise-fused producer (kDwFused): for each K block (64 channels) the
-// gather warps compute A = relu(dw3x3(x) + b) for the tile's 128 depthwise
-// output pixels straight into the 128 B-swizzled A stage, so the depthwise
-// activation never goes to HBM. Each thread owns one 8-channel granule of 4
-// rows; weights and bias of the granule are loaded once per K block.
-__device__ __forceinline__ void dw_a_tile(const ConvGemmArgs& a, uint8_t* smem, uint64_t* full,
-                                          uint64_t* empty, int m0, RingPos& rp) {
-  constexpr int GPR = 8;                        // 16 B granules per 128 B row
-  constexpr int RPP = kGatherWarps * 32 / GPR;  // 32 rows per pass
-  constexpr int PASSES = kConvBM / RPP;         // 4
-  const int t = threadIdx.x - kGatherWarp0 * 32;
-  const int gi = t % GPR;
-  const int r0 = t / GPR;
-  const int st = a.dw_stride;
+// Depthwise-fused producer (kDwFused): the tile is a TH x TW block of output
+// pixels of one image (A row r = pixel (r / TW, r % TW); rows past TH*TW are
+// never stored). For each K block (cb <= 64 channels) the TMA warp lands the
+// block's input halo box {cb, IW, IH} in smem (padding reads as zeros); the
+// gather warps compute A = relu(dw3x3(x) + b) from it, two horizontally
+// adjacent outputs x 8 channels per item with FHFMA.BF16 (the same fp32 fma
+// sequence as the standalone depthwise kernels, so the bf16 A equals their
+// stored output bit for bit), straight into the 128 B-swizzled A stage. The
+// depthwise activation never goes to HBM.
+__device__ __forceinline__ float dw_fma_lo(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %3;}"
+      : "=f"(d)
+      : "r"(x), "r"(w), "f"(c));
+  return d;
+}
 
-  int pix[PASSES], hi0[PASSES], wi0[PASSES];
-  bool live[PASSES];
-  {
-    const int HoWo = a.Ho * a.Wo;
-    const int m_first = m0 + r0;
-    int n = m_first / HoWo;
-    const int rem = m_first - n * HoWo;
-    int ho = rem / a.Wo;
-    int wo = rem - ho * a.Wo;
+__device__ __forceinline__ float dw_fma_hi(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xh, wh, %3;}"
+      : "=f"(d)
+      : "r"(x), "r"(w), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ void dw_fma8(float (&acc)[8], const uint4& x, const uint4& w) {
+  acc[0] = dw_fma_lo(x.x, w.x, acc[0]);
+  acc[1] = dw_fma_hi(x.x, w.x, acc[1]);
+  acc[2] = dw_fma_lo(x.y, w.y, acc[2]);
+  acc[3] = dw_fma_hi(x.y, w.y, acc[3]);
+  acc[4] = dw_fma_lo(x.z, w.z, acc[4]);
+  acc[5] = dw_fma_hi(x.z, w.z, acc[5]);
+  acc[6] = dw_fma_lo(x.w, w.w, acc[6]);
+  acc[7] = dw_fma_hi(x.w, w.w, acc[7]);
+}
+
+__device__ __forceinline__ uint4 relu_pack8(const float (&v)[8]) {
+  return make_uint4(pack2_bf16(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)),
+                    pack2_bf16(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)),
+                    pack2_bf16(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)),
+                    pack2_bf16(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
+}
+
+// One K block of one tile: box (smem, [IH][IW][groups] uint4) -> A stage.
+template <int S>
+__device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* box, uint32_t a_stage,
+                                            int kb, int tid) {
+  constexpr int XN = S + 3;  // input columns of two adjacent outputs
+  const int groups = a.dw_cb >> 3;
+  const int g = tid & (groups - 1);  // fixed per thread (groups divides the thread count)
+  const int cg_all = a.C >> 3;
+  const int gg = kb * groups + g;
+  uint4 w[9];
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      live[p] = m_first + p * RPP < a.M;
-      pix[p] = n * a.H * a.W;
-      hi0[p] = ho * st - 1;
-      wi0[p] = wo * st - 1;
-      wo += RPP;
-      while (wo >= a.Wo) {
-        wo -= a.Wo;
-        if (++ho == a.Ho) {
-          ho = 0;
-          ++n;
-        }
-      }
+  for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(a.dw_w) + k * cg_all + gg);
+  const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg);
+  const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg + 1);
+  const int half_tw = a.dw_tw >> 1;
+  const int items = a.dw_th * half_tw * groups;
+  for (int it = tid; it < items; it += kGatherWarps * 32) {
+    const int strip = it / groups;
+    const int ty = strip / half_tw;
+    const int tx = (strip - ty * half_tw) * 2;
+    float acc[2][8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      acc[q][0] = b0.x; acc[q][1] = b0.y; acc[q][2] = b0.z; acc[q][3] = b0.w;
+      acc[q][4] = b1.x; acc[q][5] = b1.y; acc[q][6] = b1.z; acc[q][7] = b1.w;
     }
-  }
-  const uint4* xv = reinterpret_cast<const uint4*>(a.x);
-  const uint4* wv = reinterpret_cast<const uint4*>(a.dw_w);
-  const float4* bv = reinterpret_cast<const float4*>(a.dw_b);
-  const int cg_all = a.C / 8;
-  const uint32_t lane_off =
-      static_cast<uint32_t>(r0) * 128 + (static_cast<uint32_t>(gi ^ (r0 & 7)) << 4);
-  uint8_t* stage_base = smem + lane_off;
-  for (int kb = 0; kb < a.num_kb; ++kb, rp.next(a.stages)) {
-    const uint32_t s = rp.slot;
-    if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
-    const int g = kb * GPR + gi;  // channel group of this thread
-    const bool cvalid = g < cg_all;
-    float w[9][8], b[8];
-    if (cvalid) {
 #pragma unroll
-      for (int tap = 0; tap < 9; ++tap) unpack8_bf16(__ldg(wv + tap * cg_all + g), w[tap]);
-      const float4 b0 = __ldg(bv + 2 * g), b1 = __ldg(bv + 2 * g + 1);
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    for (int r = 0; r < 3; ++r) {
+      const uint4* row = box + ((ty * S + r) * a.dw_iw + tx * S) * groups + g;
+      uint4 xv[XN];
+#pragma unroll
+      for (int u = 0; u < XN; ++u) xv[u] = row[u * groups];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dw_fma8(acc[q], xv[q * S + c], w[r * 3 + c]);
     }
-    uint8_t* sp = stage_base + s * kABytes;
+    // A row of pixel (ty, tx): warp ty / rw, lane (ty % rw) * tw + tx
+    const int row_base = (ty / a.dw_rw) * 32 + (ty % a.dw_rw) * a.dw_tw + tx;
 #pragma unroll
-    for (int p = 0; p < PASSES; ++p) {
-      float acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
-      if (cvalid && live[p]) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = b[e];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const int hi = hi0[p] + r;
-          if (static_cast<unsigned>(hi) >= static_cast<unsigned>(a.H)) continue;
-#pragma unroll
-          for (int sx = 0; sx < 3; ++sx) {
-            const int wi = wi0[p] + sx;
-            if (static_cast<unsigned>(wi) >= static_cast<unsigned>(a.W)) continue;
-            float xf[8];
-            unpack8_bf16(__ldg(xv + static_cast<size_t>(pix[p] + hi * a.W + wi) * cg_all + g), xf);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = fmaf(xf[e], w[r * 3 + sx][e], acc[e]);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.0f);
-      }
-      // bf16 rounding here is exactly where the unfused path stores the
-      // depthwise output, so fused and unfused forwards agree bit for bit.
-      *reinterpret_cast<uint4*>(sp + p * RPP * 128) =
-          make_uint4(pack2_bf16(acc[0], acc[1]), pack2_bf16(acc[2], acc[3]),
-                     pack2_bf16(acc[4], acc[5]), pack2_bf16(acc[6], acc[7]));
+    for (int q = 0; q < 2; ++q) {
+      const int row_a = row_base + q;
+      const uint32_t rowp = a_stage + row_a * 128;
+      ptx::sts128(rowp + ((g ^ (row_a & 7)) << 4), relu_pack8(acc[q]));
+      if (groups == 4)  // 32-channel layer: the K block's upper half is zero
+        ptx::sts128(rowp + (((g + 4) ^ (row_a & 7)) << 4), make_uint4(0u, 0u, 0u, 0u));
     }
-    ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core (async proxy) reads
-    ptx::mbar_arrive(&full[s]);
   }
 }
 
@@ -563,7 +569,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // pointer in the shared window so accesses through it compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int epi_warps = 4 * args.teams;
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt);
+  constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt,
+                                   kDw ? static_cast<int>(args.dw_box_bytes) : 0);
+  const uint32_t box_stride = (args.dw_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
   const uint32_t a_stage = static_cast<uint32_t>(mt) * kABytes;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
@@ -576,13 +585,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* tmem_full = empty + args.stages;  // [n_acc]
   uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
   uint64_t* b_full = tmem_empty + kMaxAcc;    // resident B landed (b_res)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
+  uint64_t* box_full = b_full + 1;            // [stages] kDwFused halo box landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(box_full + args.stages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
   const int tile_rows = kConvBM * mt;
-  const int tiles = n_tiles * ((args.M + tile_rows - 1) / tile_rows);
+  // kDwFused: M blocks are TH x TW pixel blocks of one image
+  const int dw_blocks_per_img = args.dw_tiles_y * args.dw_tiles_x;
+  const int m_blocks = kDw ? (args.M / (args.Ho * args.Wo)) * dw_blocks_per_img
+                           : (args.M + tile_rows - 1) / tile_rows;
+  const int tiles = n_tiles * m_blocks;
   const int n_acc = args.n_acc;  // power of two
   const int acc_log2 = __ffs(n_acc) - 1;
   const uint32_t acc_stride = args.tmem_cols / n_acc;
@@ -597,6 +611,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                        : kGatherWarps * 32u;
         ptx::mbar_init(&full[s], producers + (kTmaA || args.b_res == 0 ? 1u : 0u));
         ptx::mbar_init(&empty[s], 1);
+        ptx::mbar_init(&box_full[s], 1);
       }
       ptx::mbar_init(b_full, 1);
       for (int b = 0; b < n_acc; ++b) {
@@ -605,7 +620,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
-      if (kTmaA) ptx::tma_prefetch_desc(&args.tmap_a);
+      if (kTmaA || kDw) ptx::tma_prefetch_desc(&args.tmap_a);
     }
     __syncwarp();
     ptx::tmem_alloc(tmem_slot, args.tmem_cols);
@@ -636,8 +651,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       ptx::tc_fence_after();
       for (int q = 0; q < mt; ++q) {  // sub-tile q: rows m0 .. m0+127, columns q*BN ..
         const int m0 = tw.mb * tile_rows + q * kConvBM;
-        if (m0 >= args.M) break;
-        const int m = m0 + quarter * 32 + lane;
+        if (!kDw && m0 >= args.M) break;
+        int m = m0 + quarter * 32 + lane;
+        if constexpr (kDw) {  // A row -> pixel of the TH x TW block (args.M = not stored)
+          const int r = quarter * 32 + lane;
+          const int img = tw.mb / dw_blocks_per_img;
+          const int blk = tw.mb - img * dw_blocks_per_img;
+          const int by = blk / args.dw_tiles_x;
+          const int oy = by * args.dw_th + r / args.dw_tw;
+          const int ox = (blk - by * args.dw_tiles_x) * args.dw_tw + r % args.dw_tw;
+          m = r < args.dw_th * args.dw_tw && oy < args.Ho && ox < args.Wo
+                  ? (img * args.Ho + oy) * args.Wo + ox
+                  : args.M;
+        }
         const uint32_t t_row = tmem_base + acc * acc_stride + q * args.BN +
                                (static_cast<uint32_t>(quarter * 32) << 16);
         if (args.debug_flags & 1) {
@@ -658,7 +684,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
             if (lane == 0) {
-              ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+              if constexpr (kDw) {  // this warp's rw pixel rows of the TH x TW block
+                const int img = tw.mb / dw_blocks_per_img;
+                const int blk = tw.mb - img * dw_blocks_per_img;
+                const int by = blk / args.dw_tiles_x;
+                const int y0 = by * args.dw_th + quarter * args.dw_rw;
+                if (quarter * args.dw_rw < args.dw_th)
+                  ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0,
+                                    (blk - by * args.dw_tiles_x) * args.dw_tw, y0, img);
+              } else {
+                ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+              }
               ptx::bulk_commit();
             }
             ++groups;
@@ -697,6 +733,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         stem_a_tile(args, ptx::smem_u32(smem + L.a_off), full, empty, tile * tile_rows, j, lane, q,
                     groups);
       }
+    } else if constexpr (kDw) {
+      const int tid = threadIdx.x - kGatherWarp0 * 32;
+      RingPos rp;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
+          const uint32_t s = rp.slot;
+          if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
+          ptx::mbar_wait(&box_full[s], rp.lap & 1);
+          const uint4* box = reinterpret_cast<const uint4*>(smem + L.box_off + s * box_stride);
+          const uint32_t a_st = ptx::smem_u32(smem + L.a_off) + s * a_stage;
+          if (args.dw_stride == 1)
+            dw_box_to_a<1>(args, box, a_st, kb, tid);
+          else
+            dw_box_to_a<2>(args, box, a_st, kb, tid);
+          ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core reads
+          ptx::mbar_arrive(&full[s]);
+        }
+      }
     } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
       RingPos rp;
       TileWalk tw(n_tiles);
@@ -706,8 +760,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
         else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8))
           gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, rp);
-        else
-          dw_a_tile(args, smem + L.a_off, full, empty, m0, rp);
       }
     }
   } else if (warp == kTmaWarp) {
@@ -720,7 +772,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
                            kb * kConvBK, 0);
       }
-      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0);
+      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0) + (kDw ? 1u : 0u);
       uint32_t j = 0;
       RingPos rp;
       TileWalk tw(n_tiles);
@@ -737,7 +789,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             rp.next(args.stages);
           }
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&full[s], tx);
+          if constexpr (kDw) {  // the K block's halo box
+            const int img = tw.mb / dw_blocks_per_img;
+            const int blk = tw.mb - img * dw_blocks_per_img;
+            const int by = blk / args.dw_tiles_x;
+            const int bx = blk - by * args.dw_tiles_x;
+            ptx::mbar_arrive_expect_tx(&box_full[s], args.dw_box_bytes);
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                    ptx::smem_u32(smem + L.box_off + s * box_stride)),
+                "l"(&args.tmap_a), "r"(ptx::smem_u32(&box_full[s])), "r"(kb * args.dw_cb),
+                "r"(bx * args.dw_tw * args.dw_stride - 1), "r"(by * args.dw_th * args.dw_stride - 1),
+                "r"(img)
+                : "memory");
+            if (b_res) continue;
+          }
+          ptx::mbar_arrive_expect_tx(&full[s], tx - (kDw ? 1u : 0u));
           if (!b_res)
             ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                              kb * kConvBK, n0);
@@ -850,6 +918,23 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool encode_tmap_out4d(CUtensorMap* map, void* base, int n, int h, int w, int cols, int ld,
+                       int box_w, int box_h) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn || (static_cast<uint64_t>(ld) * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0)
+    return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(w),
+                              static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 2,
+                                 static_cast<cuuint64_t>(ld) * 2 * w,
+                                 static_cast<cuuint64_t>(ld) * 2 * w * h};
+  const cuuint32_t box[4] = {64u, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1u};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
                       int box_w, int box_h, int box_n) {
   EncodeTiledFn fn = get_encode_fn();
@@ -892,6 +977,39 @@ int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks, int mt) 
 
 size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks, int mt) {
   return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt).total + 1024;  // + alignment slack
+}
+
+bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
+                       int& box_bytes) {
+  if (c < 32 || (c & (c - 1)) != 0 || (stride != 1 && stride != 2)) return false;
+  cb = std::min(c, 64);
+  th = tw = 0;
+  if (stride == 1) {
+    if (wo % 16 == 0) {
+      th = 8, tw = 16;
+    } else if (wo % 14 == 0) {
+      tw = 14, th = 8;
+    }
+  } else {
+    if (wo % 8 == 0) {
+      th = 8, tw = 8;
+    } else if (wo % 14 == 0) {
+      th = 4, tw = 14;
+    }
+  }
+  if (th == 0) return false;
+  const int rw = 32 / tw;  // pixel rows per epilogue warp (TMA store box)
+  if (th % rw != 0 || th / rw > 4) return false;
+  const int iw = (tw - 1) * stride + 3, ih = (th - 1) * stride + 3;
+  box_bytes = iw * ih * cb * 2;
+  // a ring of >= 2 stages of A + box (+ B per stage when it cannot stay resident)
+  const int bn = cout <= 256 ? (cout + 15) / 16 * 16 : 256;
+  const int n_tiles = (cout + bn - 1) / bn;
+  const int kpad = (c + 63) / 64 * 64;
+  const bool b_res = n_tiles == 1 && (kpad / 64) * bn * 128 <= 64 * 1024;
+  const int per_stage = kABytes + (box_bytes + 1023) / 1024 * 1024 + (b_res ? 0 : bn * 128);
+  const int fixed = (b_res ? (kpad / 64) * bn * 128 : 0) + 8 * 2 * 4096 + 8 * 1024;  // + staging
+  return (227 * 1024 - fixed) / per_stage >= 2;
 }
 
 bool conv_gemm_stem_fits(int R, int S, int cout) {
@@ -977,6 +1095,19 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
   const int bres = args.b_res;
   args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, bres, args.mt);
+  const bool dw = mode == ConvLoadMode::kDwFused;
+  const int box = dw ? static_cast<int>(args.dw_box_bytes) : 0;
+  if (dw) {
+    // the ring carries A, the halo box (and B unless resident); the epilogue
+    // stores each warp's pixel rows through the 4-D output map
+    if (!args.y_tma) return cudaErrorInvalidValue;
+    const int per_stage = kABytes + (box + 1023) / 1024 * 1024 + (bres > 0 ? 0 : args.BN * 128);
+    const int fixed =
+        static_cast<int>(smem_layout(args.BN, 0, args.Cout, 4 * args.teams, bres, 1, box).total) +
+        64 * 8 + 1024;
+    args.stages = std::min(4, (227 * 1024 - fixed) / per_stage);
+    if (args.stages < 2) return cudaErrorInvalidValue;
+  }
   if (mode == ConvLoadMode::kStemU8) {
     // one private slot per producer group (stem_slot); drop to one epilogue
     // team if that is what makes the slots fit
@@ -996,9 +1127,11 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     }
   }
   const size_t smem =
-      conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
+      dw ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres, 1, box).total + 1024
+         : conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
   const int tiles =
-      n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
+      dw ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
+         : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);

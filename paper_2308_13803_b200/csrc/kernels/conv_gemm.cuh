@@ -52,10 +52,15 @@ struct ConvGemmArgs {
   int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
   // kDwFused: A[m, c] = relu(dw3x3(x)[m, c] + dw_b[c]), computed in the
   // producer from the depthwise input x ([H][W][C], pad 1, stride dw_stride);
-  // Ho/Wo are the depthwise output dims, R = S = 1.
+  // Ho/Wo are the depthwise output dims, R = S = 1. Tiles are dw_th x dw_tw
+  // pixel blocks of one image; tmap_a is the 4-D halo-box map over x
+  // (box {dw_cb, dw_iw, (dw_th-1)*stride+3, 1}), see conv_gemm_dw_plan.
   const __nv_bfloat16* dw_w;  // [9][C] bf16
   const float* dw_b;          // [C]
   int dw_stride;
+  int dw_th, dw_tw, dw_cb, dw_iw, dw_tiles_y, dw_tiles_x;
+  int dw_rw;  // pixel rows per epilogue warp: TMEM lane l of warp q <-> pixel (q*rw + l/tw, l%tw)
+  uint32_t dw_box_bytes;
   // kStemU8: A gathered straight from the u8 images [n][H][W][3]; the
   // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
   // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
@@ -104,6 +109,18 @@ bool conv_gemm_stem_fits(int R, int S, int cout);
 // (2 x BN accumulator columns each) fits.
 int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0, int mt = 1);
 uint32_t conv_gemm_tmem_cols(int BN);
+
+// Tile plan of a depthwise-fused 1x1 conv (kDwFused): output block th x tw
+// (<= 128 pixels, tw even), channel block cb per K block, halo box bytes;
+// false when the layer is not fused (the runtime runs the two kernels).
+bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
+                       int& box_bytes);
+
+// 4-D output map {C, W, H, N} over an NHWC activation (channel slice at
+// `base`, row stride ld channels) with a {64, box_w, box_h, 1} box and 128 B
+// swizzle: the kDwFused epilogue stores each warp's pixel rows with it.
+bool encode_tmap_out4d(CUtensorMap* map, void* base, int n, int h, int w, int cols, int ld,
+                       int box_w, int box_h);
 
 // Must run once per device before the first launch (and before any capture).
 cudaError_t conv_gemm_init();

@@ -153,6 +153,17 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
       a.dw_b = d_b_ + hp.b_off.at(dw.param);
       a.dw_stride = dw.sh;
+      int box = 0;
+      if (!conv_gemm_dw_plan(out.h, out.w, dw_in.c, dw.sh, p.cout, a.dw_th, a.dw_tw, a.dw_cb, box))
+        throw std::logic_error("depthwise fusion without a tile plan");
+      a.dw_box_bytes = static_cast<uint32_t>(box);
+      a.dw_iw = (a.dw_tw - 1) * dw.sh + 3;
+      a.dw_rw = 32 / a.dw_tw;
+      a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
+      a.dw_tiles_x = (out.w + a.dw_tw - 1) / a.dw_tw;
+      if (!encode_tmap_nhwc(&a.tmap_a, bufs_[dw.in], max_bs, dw_in.h, dw_in.w, dw_in.c, a.dw_cb,
+                            a.dw_iw, (a.dw_th - 1) * dw.sh + 3, 1))
+        throw CudaError("cuTensorMapEncodeTiled failed (depthwise halo boxes)");
     } else if (static_cast<int>(i) == stem_) {
       pl.mode = ConvLoadMode::kStemU8;  // a.img is bound per launch (input slot)
     } else if (in.c == 4) {
@@ -179,7 +190,13 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       const size_t esz = out.f32 ? 4 : 2;
       void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
-      a.y_tma = encode_tmap_out(&a.tmap_y, base, rows, p.cout, out.c, out.f32) ? 1 : 0;
+      if (pl.mode == ConvLoadMode::kDwFused)  // per-warp pixel-row boxes
+        a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
+                                                a.dw_tw, a.dw_rw)
+                      ? 1
+                      : 0;
+      else
+        a.y_tma = encode_tmap_out(&a.tmap_y, base, rows, p.cout, out.c, out.f32) ? 1 : 0;
     }
   }
   check_cuda(cudaStreamSynchronize(stream_), "instance setup");

@@ -316,7 +316,10 @@ ModelSpec inception_v3() {
 
 std::vector<bool> fused_depthwise(const ModelSpec& m) {
   std::vector<bool> fused(m.ops.size(), false);
-  const char* on = std::getenv("DS_DW_FUSION");  // opt-in until the fused producer wins
+  // Opt-in (DS_DW_FUSION=1): bit-exact, but on B200 the fused producer
+  // (depthwise FHFMA + halo boxes sharing the SM's shared-memory bandwidth with
+  // the GEMM) is still slower than the two tuned kernels back to back.
+  const char* on = std::getenv("DS_DW_FUSION");
   if (!on || on[0] != '1') return fused;
   for (size_t i = 0; i + 1 < m.ops.size(); ++i) {
     const OpSpec& dw = m.ops[i];
@@ -326,7 +329,11 @@ std::vector<bool> fused_depthwise(const ModelSpec& m) {
     bool other_reader = false;
     for (size_t j = 0; j < m.ops.size(); ++j)
       if (j != i + 1 && (m.ops[j].in == dw.out || m.ops[j].residual == dw.out)) other_reader = true;
-    if (!other_reader) fused[i] = true;
+    const BufferSpec& out = m.buffers[dw.out];
+    int th, tw, cb, box;
+    if (!other_reader && conv_gemm_dw_plan(out.h, out.w, out.c, dw.sh, m.params[pw.param].cout, th,
+                                           tw, cb, box))
+      fused[i] = true;
   }
   return fused;
 }

@@ -59,18 +59,23 @@ def test_forward_deterministic_and_batch_invariant():
     assert np.array_equal(a, one)
 
 
-def test_depthwise_fusion_matches_unfused(monkeypatch):
-    """The kDwFused conv (depthwise computed in the 1x1 conv's producer) and
-    the two-kernel path round the depthwise output to bf16 at the same point
-    with the same FMA order, so their logits agree bit for bit."""
-    imgs = generate_images("mobilenet_v1", 7, 4)
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
-        plain = be.forward(imgs)
+@pytest.mark.parametrize("bs", [1, 4, 7])
+def test_depthwise_fusion_matches_unfused(monkeypatch, bs):
+    """The kDwFused conv (depthwise computed from TMA halo boxes in the 1x1
+    conv's producer, TH x TW pixel-block tiles, direct-store epilogue) and the
+    two-kernel path round the depthwise output to bf16 at the same point with
+    the same FMA order, so their logits agree bit for bit."""
+    imgs = generate_images("mobilenet_v1", 7, bs)
     monkeypatch.setenv("DS_DW_FUSION", "1")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
         fused = be.forward(imgs)
-        assert be.stats()["kernels_per_forward"] > 0
+        k_fused = be.stats()["kernels_per_forward"]
+    monkeypatch.setenv("DS_DW_FUSION", "0")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        plain = be.forward(imgs)
+        k_plain = be.stats()["kernels_per_forward"]
     assert np.array_equal(plain, fused)
+    assert k_fused < k_plain
 
 
 @pytest.mark.parametrize("bs", [1, 3, 5])
@@ -80,6 +85,7 @@ def test_depthwise_tma_matches_register_kernels(monkeypatch, bs):
     unpack-then-fmaf kernels accumulate the same products in the same order,
     so logits agree bit for bit, including batches that leave NB boxes ragged."""
     imgs = generate_images("mobilenet_v1", 11, bs)
+    monkeypatch.setenv("DS_DW_FUSION", "0")  # standalone depthwise kernels on every layer
     with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
         tma = be.forward(imgs)
     monkeypatch.setenv("DS_DW_LEGACY", "1")
