@@ -54,7 +54,7 @@ constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
 constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
 
 struct SmemLayout {
-  uint32_t a_off, b_off, box_off, y_off, bar_off, bias_off, total;
+  uint32_t a_off, b_off, box_off, win_off, y_off, bar_off, bias_off, total;
 };
 
 // b_res_blocks > 0: the layer's whole weight matrix (num_kb blocks of
@@ -62,7 +62,7 @@ struct SmemLayout {
 // K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
                                                   int b_res_blocks = 0, int mt = 1,
-                                                  int box_bytes = 0) {
+                                                  int box_bytes = 0, int win_bytes = 0) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * mt * kABytes;  // stage = mt A sub-tiles
@@ -70,10 +70,13 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
   L.box_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;  // kDwFused halo boxes
   // (box slots rounded to 1 KiB: the 128 B-swizzled staging after them needs it)
   L.y_off = L.box_off + static_cast<uint32_t>(stages) * ((box_bytes + 1023) / 1024 * 1024);
+  // kWindow: raw[2] + chunk-major[2] halo boxes
+  L.win_off = L.y_off;
+  L.y_off += 4 * static_cast<uint32_t>((win_bytes + 1023) / 1024 * 1024);
   L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
   // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
-  // box_full[stages], tmem slot
-  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2) * 8 + 15) / 16 * 16;
+  // box_full[stages], win barriers[8], tmem slot
+  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2 + 8) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
   L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
@@ -570,8 +573,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
+  constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
+  constexpr bool kBlk = kDw || kWin;  // tiles are 2-D pixel blocks, 4-D TMA-store epilogue
   const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt,
-                                   kDw ? static_cast<int>(args.dw_box_bytes) : 0);
+                                   kDw ? static_cast<int>(args.dw_box_bytes) : 0,
+                                   kWin ? static_cast<int>(args.win_box_bytes) : 0);
+  const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   const uint32_t box_stride = (args.dw_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
   const uint32_t a_stage = static_cast<uint32_t>(mt) * kABytes;
@@ -586,7 +593,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
   uint64_t* b_full = tmem_empty + kMaxAcc;    // resident B landed (b_res)
   uint64_t* box_full = b_full + 1;            // [stages] kDwFused halo box landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(box_full + args.stages);
+  uint64_t* raw_full = box_full + args.stages;  // [2] kWindow: pixel-major box landed
+  uint64_t* raw_free = raw_full + 2;            // [2] ... transposed (gather warps)
+  uint64_t* cm_full = raw_free + 2;             // [2] chunk-major box ready
+  uint64_t* cm_empty = cm_full + 2;             // [2] all taps of its K block consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cm_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -594,8 +605,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int tile_rows = kConvBM * mt;
   // kDwFused: M blocks are TH x TW pixel blocks of one image
   const int dw_blocks_per_img = args.dw_tiles_y * args.dw_tiles_x;
-  const int m_blocks = kDw ? (args.M / (args.Ho * args.Wo)) * dw_blocks_per_img
-                           : (args.M + tile_rows - 1) / tile_rows;
+  const int m_blocks = kBlk ? (args.M / (args.Ho * args.Wo)) * dw_blocks_per_img
+                            : (args.M + tile_rows - 1) / tile_rows;
+  const int win_cblocks = (args.C + 63) / 64;  // kWindow: 64-channel K blocks
+  const int win_taps = args.R * args.S;
   const int tiles = n_tiles * m_blocks;
   const int n_acc = args.n_acc;  // power of two
   const int acc_log2 = __ffs(n_acc) - 1;
@@ -605,7 +618,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == kTmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < args.stages; ++s) {
-        const uint32_t producers = kTmaA ? 0u
+        const uint32_t producers = kTmaA || kWin ? 0u
                                    : MODE == static_cast<int>(ConvLoadMode::kStemU8)
                                        ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
@@ -614,13 +627,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         ptx::mbar_init(&box_full[s], 1);
       }
       ptx::mbar_init(b_full, 1);
+      for (int b = 0; b < 2; ++b) {
+        ptx::mbar_init(&raw_full[b], 1);
+        ptx::mbar_init(&raw_free[b], kGatherWarps);
+        ptx::mbar_init(&cm_full[b], kGatherWarps);
+        ptx::mbar_init(&cm_empty[b], 1);
+      }
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
         ptx::mbar_init(&tmem_empty[b], 4);  // one arrival per warp of the owning team
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
-      if (kTmaA || kDw) ptx::tma_prefetch_desc(&args.tmap_a);
+      if (kTmaA || kBlk) ptx::tma_prefetch_desc(&args.tmap_a);
     }
     __syncwarp();
     ptx::tmem_alloc(tmem_slot, args.tmem_cols);
@@ -651,9 +670,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       ptx::tc_fence_after();
       for (int q = 0; q < mt; ++q) {  // sub-tile q: rows m0 .. m0+127, columns q*BN ..
         const int m0 = tw.mb * tile_rows + q * kConvBM;
-        if (!kDw && m0 >= args.M) break;
+        if (!kBlk && m0 >= args.M) break;
         int m = m0 + quarter * 32 + lane;
-        if constexpr (kDw) {  // A row -> pixel of the TH x TW block (args.M = not stored)
+        if constexpr (kBlk) {  // A row -> pixel of the TH x TW block (args.M = not stored)
           const int r = quarter * 32 + lane;
           const int img = tw.mb / dw_blocks_per_img;
           const int blk = tw.mb - img * dw_blocks_per_img;
@@ -684,7 +703,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
             if (lane == 0) {
-              if constexpr (kDw) {  // this warp's rw pixel rows of the TH x TW block
+              if constexpr (kBlk) {  // this warp's rw pixel rows of the TH x TW block
                 const int img = tw.mb / dw_blocks_per_img;
                 const int blk = tw.mb - img * dw_blocks_per_img;
                 const int by = blk / args.dw_tiles_x;
@@ -713,6 +732,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
     }
     if (lane == 0) ptx::bulk_wait<0>();
+  } else if (warp < kGatherWarp0) {
+    // (with a single epilogue team, warps 4-7 have no role)
   } else if (warp < kGatherWarp0 + kGatherWarps) {
     if constexpr (MODE == static_cast<int>(ConvLoadMode::kStemU8)) {
       // one producer warp per tile (tile j -> gather warp j % 8); tile j's
@@ -732,6 +753,38 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           stem_prefetch(args, (tile + 2 * groups * gridDim.x) * tile_rows + q * kConvBM);
         stem_a_tile(args, ptx::smem_u32(smem + L.a_off), full, empty, tile * tile_rows, j, lane, q,
                     groups);
+      }
+    } else if constexpr (kWin) {
+      // transpose each K block's halo box: raw [pixel][cb] -> chunk-major
+      // [chunk][pixel] 16 B pieces (the no-swizzle K-major operand layout)
+      const int tid = threadIdx.x - kGatherWarp0 * 32;
+      const int npix = args.win_iw * args.win_ih;
+      const int cb = args.C < 64 ? args.C : 64;
+      const int raw_chunks = cb / 8;  // 16 B chunks per raw pixel row
+      uint32_t u = 0;                  // box uses so far (slot u & 1, phase u >> 1)
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
+          const uint32_t b = u & 1, ph = (u >> 1) & 1;
+          ptx::mbar_wait(&raw_full[b], ph);
+          if (u >= 2) ptx::mbar_wait(&cm_empty[b], ph ^ 1);
+          const uint32_t raw = ptx::smem_u32(smem + L.win_off + b * win_stride);
+          const uint32_t cm = ptx::smem_u32(smem + L.win_off + (2 + b) * win_stride);
+          const int kch = min(8, (args.C - kb * 64) / 8);  // real chunks of this K block
+          for (int i = tid; i < npix * kch; i += kGatherWarps * 32) {
+            const int p = i / kch, k = i - p * kch;
+            uint4 v;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(raw + (p * raw_chunks + k) * 16));
+            ptx::sts128(cm + (k * npix + p) * 16, v);
+          }
+          ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core reads
+          __syncwarp();
+          if (lane == 0) {
+            ptx::mbar_arrive(&raw_free[b]);
+            ptx::mbar_arrive(&cm_full[b]);
+          }
+        }
       }
     } else if constexpr (kDw) {
       const int tid = threadIdx.x - kGatherWarp0 * 32;
@@ -760,6 +813,48 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
         else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8))
           gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, rp);
+      }
+    }
+  } else if (warp == kTmaWarp && kWin) {
+    if (lane == 0) {
+      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      const bool b_res = args.b_res > 0;
+      if (b_res) {  // every (K block, tap) weight tile, once
+        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(win_cblocks * win_taps) * b_bytes);
+        for (int kb = 0; kb < win_cblocks; ++kb)
+          for (int t = 0; t < win_taps; ++t)
+            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + (kb * win_taps + t) * b_bytes),
+                             &args.tmap_b, b_full, t * args.C + kb * 64, 0);
+      }
+      RingPos rp;
+      TileWalk tw(n_tiles);
+      uint32_t u = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
+        const int n0 = tw.nb * args.BN;
+        const int img = tw.mb / dw_blocks_per_img;
+        const int blk = tw.mb - img * dw_blocks_per_img;
+        const int by = blk / args.dw_tiles_x;
+        const int bx = blk - by * args.dw_tiles_x;
+        for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
+          const uint32_t b = u & 1, ph = (u >> 1) & 1;
+          if (u >= 2) ptx::mbar_wait(&raw_free[b], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&raw_full[b], args.win_box_bytes);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                  ptx::smem_u32(smem + L.win_off + b * win_stride)),
+              "l"(&args.tmap_a), "r"(ptx::smem_u32(&raw_full[b])), "r"(kb * 64),
+              "r"(bx * args.dw_tw - args.pad_w), "r"(by * args.dw_th - args.pad_h), "r"(img)
+              : "memory");
+          if (b_res) continue;
+          for (int t = 0; t < win_taps; ++t, rp.next(args.stages)) {
+            const uint32_t s = rp.slot;
+            if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&full[s], b_bytes);
+            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
+                             t * args.C + kb * 64, n0);
+          }
+        }
       }
     }
   } else if (warp == kTmaWarp) {
@@ -816,6 +911,58 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
       }
     }
+  } else if (kWin) {  // kMmaWarp, shifted-window MMAs
+    if (lane == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
+      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      const bool b_res = args.b_res > 0;
+      if (b_res) ptx::mbar_wait(b_full, 0);
+      const uint32_t npix = static_cast<uint32_t>(args.win_iw * args.win_ih);
+      const uint32_t lbo = npix * 16, sbo = static_cast<uint32_t>(args.win_iw) * 16;
+      uint32_t j = 0, u = 0;
+      RingPos rp;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        const uint32_t acc = j & (n_acc - 1);
+        if (j >= static_cast<uint32_t>(n_acc))
+          ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * acc_stride;
+        bool first = true;
+        for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
+          const uint32_t b = u & 1;
+          ptx::mbar_wait(&cm_full[b], (u >> 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t cm = ptx::smem_u32(smem + L.win_off + (2 + b) * win_stride);
+          const int ksteps = min(8, (args.C - kb * 64) / 8) / 2;
+          for (int t = 0; t < win_taps; ++t) {
+            uint32_t s = 0;
+            if (!b_res) {
+              s = rp.slot;
+              ptx::mbar_wait(&full[s], rp.lap & 1);
+              ptx::tc_fence_after();
+            }
+            const int dr = t / args.S, dc = t - (t / args.S) * args.S;
+            const uint64_t da = ptx::umma_desc_none_kmajor(
+                cm + static_cast<uint32_t>(dr * args.win_iw + dc) * 16, lbo, sbo);
+            const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(
+                smem + L.b_off + (b_res ? kb * win_taps + t : static_cast<int>(s)) * b_bytes));
+            for (int k = 0; k < ksteps; ++k) {
+              // next K=16 step: two chunk planes further (start field is addr >> 4)
+              ptx::umma_bf16(d, da + static_cast<uint64_t>(2 * k) * (lbo >> 4), db + 2 * k, idesc,
+                             first ? 0u : 1u);
+              first = false;
+            }
+            if (!b_res) {
+              ptx::umma_commit(&empty[s]);
+              rp.next(args.stages);
+            }
+          }
+          ptx::umma_commit(&cm_empty[b]);
+        }
+        ptx::umma_commit(&tmem_full[acc]);
+      }
+    }
+    __syncwarp();
   } else {  // kMmaWarp: MMA issuer
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
@@ -1012,6 +1159,43 @@ bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int
   return (227 * 1024 - fixed) / per_stage >= 2;
 }
 
+// kWindow ring sizing (shared by the launcher and conv_gemm_window_ok).
+bool window_rings(int R, int S, int C, int cout, int BN, int box_bytes, int& b_res, int& teams,
+                  int& stages) {
+  const int taps = R * S, cblocks = (C + 63) / 64;
+  const int win = 4 * ((box_bytes + 1023) / 1024 * 1024);
+  const int res_bytes = cblocks * taps * BN * 128;
+  const int n_tiles = (cout + BN - 1) / BN;
+  auto fits = [&](int res_blocks, int tm, int st) {
+    const int total = static_cast<int>(smem_layout(BN, st, cout, 4 * tm, res_blocks, 1, 0, box_bytes).total);
+    (void)win;
+    return total + 1024 <= 227 * 1024;
+  };
+  for (int tm = 2; tm >= 1; --tm) {
+    if (n_tiles == 1 && fits(cblocks * taps, tm, 1)) {
+      b_res = cblocks * taps, teams = tm, stages = 1;
+      (void)res_bytes;
+      return true;
+    }
+  }
+  for (int tm = 2; tm >= 1; --tm)
+    for (int st = 6; st >= 2; --st)
+      if (fits(0, tm, st)) {
+        b_res = 0, teams = tm, stages = st;
+        return true;
+      }
+  return false;
+}
+
+bool conv_gemm_window_ok(int r, int s, int c, int cout) {
+  if (r * s < 2 || c % 16 != 0 || r > 9 || s > 9) return false;
+  const int bn = cout <= 256 ? (cout + 15) / 16 * 16 : ((cout + (cout + 255) / 256 - 1) / ((cout + 255) / 256) + 63) / 64 * 64;
+  const int cb = std::min(c, 64);
+  const int box = (8 + s - 1) * (16 + r - 1) * cb * 2;
+  int b_res, teams, stages;
+  return window_rings(r, s, c, cout, bn, box, b_res, teams, stages);
+}
+
 bool conv_gemm_stem_fits(int R, int S, int cout) {
   // kernel-row / kernel-column masks are 16-bit fields; eight ring slots
   // (one per producer warp) with one epilogue team must fit in shared memory
@@ -1038,6 +1222,9 @@ cudaError_t conv_gemm_init() {
                                cap);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
     return e;
   }();
@@ -1126,12 +1313,25 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       args.tap_info[t] = ((r * args.W + c) * 3) | (r << 24) | (c << 28);
     }
   }
+  const bool win = mode == ConvLoadMode::kWindow;
+  if (win) {
+    // rings: 2 pixel-major + 2 chunk-major halo boxes; weights resident when
+    // every (K block, tap) tile fits, else streamed per tap; staging for the
+    // 4-D TMA-store epilogue
+    if (!args.y_tma) return cudaErrorInvalidValue;
+    if (!window_rings(args.R, args.S, args.C, args.Cout, args.BN, static_cast<int>(args.win_box_bytes),
+                      args.b_res, args.teams, args.stages))
+      return cudaErrorInvalidValue;
+  }
+  const int bres2 = args.b_res;
   const size_t smem =
       dw ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres, 1, box).total + 1024
-         : conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
+      : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
+                          static_cast<int>(args.win_box_bytes)).total + 1024
+            : conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
   const int tiles =
-      dw ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
-         : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
+      dw || win ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
+                : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
@@ -1148,6 +1348,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return launch_pdl(conv_gemm_kernel<3>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kStemU8:
       return launch_pdl(conv_gemm_kernel<4>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kWindow:
+      return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
   }
   return cudaGetLastError();
 }

@@ -61,6 +61,14 @@ struct ConvGemmArgs {
   int dw_th, dw_tw, dw_cb, dw_iw, dw_tiles_y, dw_tiles_x;
   int dw_rw;  // pixel rows per epilogue warp: TMEM lane l of warp q <-> pixel (q*rw + l/tw, l%tw)
   uint32_t dw_box_bytes;
+  // kWindow (stride-1 R x S conv, no im2col): tiles are 16 x 8 output-pixel
+  // blocks (dw_th/dw_tw/dw_rw/dw_tiles_* as above); per 64-channel K block
+  // the TMA lands the halo box {min(64, C), win_iw, win_ih} (pixel-major), the
+  // gather warps transpose it to chunk-major (16 B channel chunks x pixels),
+  // and every tap (r, s) is one MMA operand read straight out of that box
+  // at pixel offset r*win_iw + s (K-major, no swizzle).
+  int win_iw, win_ih;
+  uint32_t win_box_bytes;
   // kStemU8: A gathered straight from the u8 images [n][H][W][3]; the
   // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
   // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
@@ -76,6 +84,7 @@ enum class ConvLoadMode : int {
   kTmaA = 2,      // 1x1 stride-1 conv: A is a plain 2D tile, loaded by TMA
   kDwFused = 3,   // depthwise 3x3 + bias + ReLU computed into A, then the 1x1 GEMM
   kStemU8 = 4,    // stem conv over the u8 images, input staging fused into the producer
+  kWindow = 5,    // stride-1 R x S conv as shifted-window MMAs over a per-K-block halo box
 };
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
@@ -115,6 +124,10 @@ uint32_t conv_gemm_tmem_cols(int BN);
 // false when the layer is not fused (the runtime runs the two kernels).
 bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
                        int& box_bytes);
+
+// Whether a conv runs as kWindow: stride 1, R*S > 1, C % 16 == 0, and the
+// operand rings fit in shared memory next to the epilogue staging.
+bool conv_gemm_window_ok(int r, int s, int c, int cout);
 
 // 4-D output map {C, W, H, N} over an NHWC activation (channel slice at
 // `base`, row stride ld channels) with a {64, box_w, box_h, 1} box and 128 B

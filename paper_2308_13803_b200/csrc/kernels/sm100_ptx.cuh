@@ -240,6 +240,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_kmajor(uint32_t smem_addr) {
   return d;
 }
 
+// K-major, no swizzle ("interleaved") operand: core matrices of 8 rows x
+// 16 B stored as 128 contiguous bytes; lbo = byte distance between the two
+// 16 B K-chunks of one K=16 step, sbo = distance between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc_none_kmajor(uint32_t smem_addr, uint32_t lbo,
+                                                          uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100); layout 0 = SWIZZLE_NONE
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);

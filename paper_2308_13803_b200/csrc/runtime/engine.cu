@@ -35,6 +35,18 @@ int choose_stages(int bn, int cout) { return conv_gemm_stages(bn, cout); }
 
 uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 
+// DS_CONV_WINDOW=1: stride-1 R x S convs as kWindow (shifted-window MMAs).
+// Opt-in: parity-tested, but its fixed 16 x 8 pixel tiles waste a third of
+// the MMA rows on 28/14/7-wide layers and the 2-deep box rings expose the
+// halo load, so the im2col gather is still faster on B200.
+bool window_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DS_CONV_WINDOW");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ Instance
@@ -170,6 +182,22 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
+    } else if (window_on() && op.kind == OpKind::kConv && op.sh == 1 && op.sw == 1 &&
+               op.residual < 0 && !out.f32 && conv_gemm_window_ok(op.r, op.s, in.c, p.cout)) {
+      // stride-1 R x S conv: shifted-window MMAs over per-K-block halo boxes
+      pl.mode = ConvLoadMode::kWindow;
+      a.dw_th = 16;
+      a.dw_tw = 8;
+      a.dw_rw = 4;
+      a.dw_tiles_y = (out.h + 15) / 16;
+      a.dw_tiles_x = (out.w + 7) / 8;
+      a.win_iw = 8 + op.s - 1;
+      a.win_ih = 16 + op.r - 1;
+      const int cb = in.c < 64 ? in.c : 64;
+      a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * cb * 2);
+      if (!encode_tmap_nhwc(&a.tmap_a, bufs_[op.in], max_bs, in.h, in.w, in.c, cb, a.win_iw,
+                            a.win_ih, 1))
+        throw CudaError("cuTensorMapEncodeTiled failed (window halo boxes)");
     } else if (op.r == 1 && op.s == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 && op.pw == 0) {
       // A is a plain [pixels][C] matrix; for C < 64 the TMA box runs past
       // the row and the out-of-bounds columns arrive as zeros.
@@ -190,7 +218,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       const size_t esz = out.f32 ? 4 : 2;
       void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
-      if (pl.mode == ConvLoadMode::kDwFused)  // per-warp pixel-row boxes
+      if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow)  // pixel-row boxes
         a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
                                                 a.dw_tw, a.dw_rw)
                       ? 1

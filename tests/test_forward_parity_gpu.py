@@ -94,6 +94,23 @@ def test_depthwise_tma_matches_register_kernels(monkeypatch, bs):
     assert np.array_equal(tma, legacy)
 
 
+@pytest.mark.parametrize("model,bs", [("resnet50_v1", 3), ("inception_v3", 2)])
+def test_window_conv_matches_im2col_gather(monkeypatch, model, bs):
+    """kWindow (stride-1 R x S convs as shifted-window MMAs over halo boxes,
+    16 x 8 pixel-block tiles) against the im2col gather: the same products,
+    summed in a different K order (channel block outer, tap inner), so the
+    logits agree to fp32-accumulation rounding, far inside the oracle bound."""
+    imgs = generate_images(model, 5, bs)
+    monkeypatch.setenv("DS_CONV_WINDOW", "1")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        win = be.forward(imgs)
+    monkeypatch.setenv("DS_CONV_WINDOW", "0")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        gather = be.forward(imgs)
+    assert np.isfinite(win).all()
+    assert row_rel_err(win, gather).max() <= 2e-3
+
+
 @pytest.mark.parametrize("model", ["synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"])
 def test_fused_stem_matches_staged_input(monkeypatch, model):
     """The stem conv reading u8 images directly (kStemU8: the staging

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/models1
+for m in resnet50_v1 inception_v3 synthetic_cnn; do
+  timeout 600 python bench.py --model $m --kernel-table --no-cpu-baseline > gpurun_out/models1/$m.json 2>gpurun_out/models1/$m.err
+done

@@ -5,8 +5,8 @@ set -u
 TAG=$1; K=$2; shift 2
 OUT=gpurun_out/$TAG; mkdir -p "$OUT"
 if [ -n "$K" ]; then
-  timeout 600 python -m pytest tests -m gpu -x -q --timeout=150 -k "$K" > "$OUT/pytest_gpu.log" 2>&1
+  timeout 600 python -m pytest tests -m gpu -x -q --timeout=150 --timeout-method=thread -k "$K" > "$OUT/pytest_gpu.log" 2>&1
   echo "pytest exit $?" >> "$OUT/pytest_gpu.log"
 fi
-timeout 600 python bench.py --kernel-table --no-cpu-baseline "$@" > "$OUT/bench.json" 2> "$OUT/bench.err"
+timeout 300 python bench.py --kernel-table --no-cpu-baseline "$@" > "$OUT/bench.json" 2> "$OUT/bench.err"
 echo "bench exit $?" >> "$OUT/bench.err"
