@@ -574,7 +574,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
   constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
-  constexpr bool kBlk = kDw || kWin;  // tiles are 2-D pixel blocks, 4-D TMA-store epilogue
+  constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D);
+  constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
   const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt,
                                    kDw ? static_cast<int>(args.dw_box_bytes) : 0,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0);
@@ -618,11 +619,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == kTmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < args.stages; ++s) {
-        const uint32_t producers = kTmaA || kWin ? 0u
+        const uint32_t producers = kTmaA || kWin || kS2 ? 0u
                                    : MODE == static_cast<int>(ConvLoadMode::kStemU8)
                                        ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
-        ptx::mbar_init(&full[s], producers + (kTmaA || args.b_res == 0 ? 1u : 0u));
+        ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
         ptx::mbar_init(&empty[s], 1);
         ptx::mbar_init(&box_full[s], 1);
       }
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
-      if (kTmaA || kBlk) ptx::tma_prefetch_desc(&args.tmap_a);
+      if (kTmaA || kBlk) ptx::tma_prefetch_desc(&args.tmap_a);  // (A / halo / tap boxes)
     }
     __syncwarp();
     ptx::tmem_alloc(tmem_slot, args.tmem_cols);
@@ -707,8 +708,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 const int img = tw.mb / dw_blocks_per_img;
                 const int blk = tw.mb - img * dw_blocks_per_img;
                 const int by = blk / args.dw_tiles_x;
-                const int y0 = by * args.dw_th + quarter * args.dw_rw;
-                if (quarter * args.dw_rw < args.dw_th)
+                const int yq = q * (kConvBM / args.dw_tw) + quarter * args.dw_rw;  // in-block row
+                const int y0 = by * args.dw_th + yq;
+                if (yq < args.dw_th)
                   ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0,
                                     (blk - by * args.dw_tiles_x) * args.dw_tw, y0, img);
               } else {
@@ -815,6 +817,39 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, rp);
       }
     }
+  } else if (warp == kTmaWarp && kS2) {
+    if (lane == 0) {
+      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
+      for (int kb = 0; kb < args.num_kb; ++kb)
+        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
+                         kb * kConvBK, 0);
+      const int taps = args.R * args.S;
+      RingPos rp;
+      TileWalk tw(n_tiles);
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
+        const int img = tw.mb / dw_blocks_per_img;
+        const int blk = tw.mb - img * dw_blocks_per_img;
+        const int by = blk / args.dw_tiles_x;
+        const int bx = blk - by * args.dw_tiles_x;
+        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
+          const uint32_t s = rp.slot;
+          if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
+          const int nt = min(4, taps - kb * 4);  // taps of this K block (16 channels each)
+          ptx::mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nt) * args.win_box_bytes);
+          for (int tl = 0; tl < nt; ++tl) {
+            const int t = kb * 4 + tl, dr = t / args.S, dc = t - (t / args.S) * args.S;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                    ptx::smem_u32(smem + L.a_off + s * a_stage + tl * args.win_box_bytes)),
+                "l"(&args.tmap_a), "r"(ptx::smem_u32(&full[s])), "r"(0),
+                "r"(bx * args.dw_tw + dc), "r"(by * args.dw_th + dr), "r"(img)
+                : "memory");
+          }
+        }
+      }
+    }
   } else if (warp == kTmaWarp && kWin) {
     if (lane == 0) {
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
@@ -911,6 +946,38 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
       }
     }
+  } else if (kS2) {  // kMmaWarp: per tap, sub-tile q reads its 128 rows of the tap box
+    if (lane == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
+      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      ptx::mbar_wait(b_full, 0);
+      const int taps = args.R * args.S;
+      uint32_t j = 0;
+      RingPos rp;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        const uint32_t acc = j & (n_acc - 1);
+        if (j >= static_cast<uint32_t>(n_acc))
+          ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * acc_stride;
+        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
+          const uint32_t s = rp.slot;
+          ptx::mbar_wait(&full[s], rp.lap & 1);
+          ptx::tc_fence_after();
+          const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + kb * b_bytes));
+          const int nt = min(4, taps - kb * 4);
+          for (int tl = 0; tl < nt; ++tl)
+            for (int q = 0; q < mt; ++q) {
+              const uint64_t da = ptx::umma_desc_sw32_kmajor(ptx::smem_u32(
+                  smem + L.a_off + s * a_stage + tl * args.win_box_bytes + q * kConvBM * 32));
+              ptx::umma_bf16(d + q * args.BN, da, db + 2 * tl, idesc, (kb | tl) != 0);
+            }
+          ptx::umma_commit(&empty[s]);
+        }
+        ptx::umma_commit(&tmem_full[acc]);
+      }
+    }
+    __syncwarp();
   } else if (kWin) {  // kMmaWarp, shifted-window MMAs
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
@@ -1063,6 +1130,23 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
   return fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base,
             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int w, int c,
+                           int box_w, int box_h) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn || c * 2 != 32) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
+                              static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2,
+                                 static_cast<cuuint64_t>(c) * 2 * w,
+                                 static_cast<cuuint64_t>(c) * 2 * w * h};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(c), static_cast<cuuint32_t>(box_w),
+                             static_cast<cuuint32_t>(box_h), 1u};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool encode_tmap_out4d(CUtensorMap* map, void* base, int n, int h, int w, int cols, int ld,
@@ -1226,6 +1310,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -1256,7 +1343,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   };
   static const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
                    teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
-  const int mt_cap = mode == ConvLoadMode::kStemU8 ? mt_stem
+  const int mt_cap = mode == ConvLoadMode::kS2D ? 2
+                     : mode == ConvLoadMode::kStemU8 ? mt_stem
                      : mode == ConvLoadMode::kTmaA ? mt_tma
                                                    : 1;
   args.mt = 1;
@@ -1313,6 +1401,15 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       args.tap_info[t] = ((r * args.W + c) * 3) | (r << 24) | (c << 28);
     }
   }
+  if (mode == ConvLoadMode::kS2D) {
+    // 16 x 16 pixel blocks = two 128-row sub-tiles; all weights resident
+    args.mt = 2;
+    if (!args.y_tma || n_tiles != 1 || args.num_kb * args.BN * 128 > 64 * 1024)
+      return cudaErrorInvalidValue;
+    args.b_res = args.num_kb;
+    args.stages = std::min(6, conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, args.b_res, 2));
+    if (args.stages < 2) return cudaErrorInvalidValue;
+  }
   const bool win = mode == ConvLoadMode::kWindow;
   if (win) {
     // rings: 2 pixel-major + 2 chunk-major halo boxes; weights resident when
@@ -1329,8 +1426,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
                           static_cast<int>(args.win_box_bytes)).total + 1024
             : conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
+  const bool blk = dw || win || mode == ConvLoadMode::kS2D;
   const int tiles =
-      dw || win ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
+      blk ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
                 : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
@@ -1350,6 +1448,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return launch_pdl(conv_gemm_kernel<4>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kWindow:
       return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kS2D:
+      return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
   }
   return cudaGetLastError();
 }

@@ -85,6 +85,8 @@ enum class ConvLoadMode : int {
   kDwFused = 3,   // depthwise 3x3 + bias + ReLU computed into A, then the 1x1 GEMM
   kStemU8 = 4,    // stem conv over the u8 images, input staging fused into the producer
   kWindow = 5,    // stride-1 R x S conv as shifted-window MMAs over a per-K-block halo box
+  kS2D = 6,       // stride-2 stem over its space-to-depth input: per tap one TMA box, no
+                  // producer warps (A arrives in the MMA's 32 B-swizzled layout)
 };
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
@@ -128,6 +130,11 @@ bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int
 // Whether a conv runs as kWindow: stride 1, R*S > 1, C % 16 == 0, and the
 // operand rings fit in shared memory next to the epilogue staging.
 bool conv_gemm_window_ok(int r, int s, int c, int cout);
+
+// 4-D NHWC bf16 map with a {box_c, box_w, box_h, 1} box and 32 B swizzle
+// (box_c * 2 == 32): the kS2D per-tap A boxes.
+bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int w, int c,
+                           int box_w, int box_h);
 
 // 4-D output map {C, W, H, N} over an NHWC activation (channel slice at
 // `base`, row stride ld channels) with a {64, box_w, box_h, 1} box and 128 B

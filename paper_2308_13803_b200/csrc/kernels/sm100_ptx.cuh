@@ -253,6 +253,19 @@ __device__ __forceinline__ uint64_t umma_desc_none_kmajor(uint32_t smem_addr, ui
   return d;
 }
 
+// K-major, 32 B swizzle: rows of 32 B (one K=16 step of bf16), 8-row groups
+// 256 B apart (the layout a TMA box with a 32 B inner extent and
+// SWIZZLE_32B writes).
+__device__ __forceinline__ uint64_t umma_desc_sw32_kmajor(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;          // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(256 >> 4) << 32;   // SBO: next 8-row group
+  d |= static_cast<uint64_t>(1) << 46;          // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(6) << 61;          // SWIZZLE_32B
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);

@@ -50,6 +50,39 @@ __global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __res
   out[p] = make_uint2(pack2(v[0], v[1]), pack2(v[2], 0.0f));
 }
 
+// Space-to-depth staging for stride-2 stems (kS2D): S[n][Y][X][16] bf16 with
+// channel (a*2 + b)*4 + c = x(2Y + a - pad, 2X + b - pad, c) normalised as
+// above (zero outside the image and for c == 3). A stride-2 R x S conv over x
+// is then a stride-1 ceil(R/2) x ceil(S/2) conv over S with 16 channels.
+__global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restrict__ out, int h,
+                                 int w, int hs, int ws, int pad, long long pixels) {
+  pdl_trigger();
+  pdl_wait();
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= pixels) return;
+  const int X = static_cast<int>(i % ws);
+  const long long t = i / ws;
+  const int Y = static_cast<int>(t % hs);
+  const long long n = t / hs;
+  uint32_t v[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int y = 2 * Y + a - pad, x = 2 * X + b - pad;
+      float f[3] = {0.f, 0.f, 0.f};
+      if (y >= 0 && y < h && x >= 0 && x < w) {
+        const uint8_t* src = img + ((n * h + y) * w + x) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) f[c] = (static_cast<float>(src[c]) - 127.5f) / 63.75f;
+      }
+      v[(a * 2 + b) * 2] = pack2(f[0], f[1]);
+      v[(a * 2 + b) * 2 + 1] = pack2(f[2], 0.0f);
+    }
+  out[2 * i] = make_uint4(v[0], v[1], v[2], v[3]);
+  out[2 * i + 1] = make_uint4(v[4], v[5], v[6], v[7]);
+}
+
 // Depthwise 3x3, register-blocked: a thread owns 8 channels (one 16 B
 // vector) x kDwCols consecutive output columns of one output row, so each
 // loaded input vector feeds up to 3 outputs from registers; consecutive
@@ -264,6 +297,13 @@ cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, in
   return launch_pdl(stage_input_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
                     reinterpret_cast<uint2*>(out), pixels);
   return cudaGetLastError();
+}
+
+cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w, int hs,
+                             int ws, int pad, cudaStream_t stream) {
+  const long long pixels = static_cast<long long>(n) * hs * ws;
+  return launch_pdl(stage_s2d_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
+                    reinterpret_cast<uint4*>(out), h, w, hs, ws, pad, pixels);
 }
 
 cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,

@@ -15,6 +15,11 @@ namespace ds {
 cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
                                cudaStream_t stream);
 
+// Space-to-depth staging for stride-2 stems: u8 [n][h][w][3] -> bf16
+// [n][hs][ws][16], channel (a*2+b)*4+c = normalised x(2Y+a-pad, 2X+b-pad, c).
+cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w, int hs,
+                             int ws, int pad, cudaStream_t stream);
+
 // Depthwise 3x3, pad 1, stride 1|2, + bias, ReLU. w: [9][C] bf16 (tap-major).
 cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
                              __nv_bfloat16* y, int n, int h, int wd, int c, int stride,

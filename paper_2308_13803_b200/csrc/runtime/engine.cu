@@ -73,6 +73,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     buf_off.push_back(
         take(static_cast<size_t>(max_bs) * b.h * b.w * b.c * (b.f32 ? sizeof(float) : 2)));
   const size_t probs_off = take(static_cast<size_t>(max_bs) * m.classes * sizeof(float));
+  s2d_ = stem_s2d(m);
+  size_t s2d_off = 0, stem_w_off = 0;
+  if (s2d_.op >= 0) {
+    s2d_off = take(static_cast<size_t>(max_bs) * s2d_.hs * s2d_.ws * 16 * 2);
+    stem_w_off = take(static_cast<size_t>(m.params[m.ops[s2d_.op].param].cout) * s2d_.kpad * 2);
+  }
   device_bytes_ = off;
   check_cuda(cudaMalloc(&d_arena_, off), "cudaMalloc(instance arena)");
   uint8_t* base = static_cast<uint8_t*>(d_arena_);
@@ -81,6 +87,29 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   d_b_ = reinterpret_cast<float*>(base + b_off);
   d_images_[0] = base + img_off;
   d_images_[1] = base + img2_off;
+  if (s2d_.op >= 0) {
+    // stem weights for the s2d taps: W'[co][(dr*ds + dc)*16 + (a*2 + b)*4 + c] =
+    // W[co][(2dr+a)*S + (2dc+b)][c] (zero where 2dr+a >= R or 2dc+b >= S)
+    d_s2d_ = reinterpret_cast<__nv_bfloat16*>(base + s2d_off);
+    d_stem_w_ = reinterpret_cast<__nv_bfloat16*>(base + stem_w_off);
+    const OpSpec& op = m.ops[s2d_.op];
+    const ParamSpec& p = m.params[op.param];
+    const int kpad0 = hp.kpad.at(op.param);
+    std::vector<uint16_t> w2(static_cast<size_t>(p.cout) * s2d_.kpad, 0);
+    for (int co = 0; co < p.cout; ++co)
+      for (int r = 0; r < op.r; ++r)
+        for (int q = 0; q < op.s; ++q)
+          for (int c = 0; c < 4; ++c) {
+            const int k0 = (r * op.s + q) * 4 + c;
+            const int k1 = ((r / 2) * s2d_.ds + q / 2) * 16 + ((r % 2) * 2 + q % 2) * 4 + c;
+            w2[static_cast<size_t>(co) * s2d_.kpad + k1] =
+                hp.w[hp.w_off.at(op.param) + static_cast<size_t>(co) * kpad0 + k0];
+          }
+    // (on stream_, after the arena memset; synchronised before w2 goes away)
+    check_cuda(cudaMemcpyAsync(d_stem_w_, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice, stream_),
+               "upload s2d stem weights");
+    check_cuda(cudaStreamSynchronize(stream_), "upload s2d stem weights");
+  }
   check_cuda(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (int s = 0; s < 2; ++s) {
     check_cuda(cudaEventCreateWithFlags(&slot_free_[s], cudaEventDisableTiming), "event");
@@ -99,7 +128,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   plans_.resize(m.ops.size());
   fused_ = fused_depthwise(m);
   stem_ = fused_stem(m);
-  kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (input staging +) softmax
+  kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (input or s2d staging +) softmax
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
     if (!fused_[i]) ++kernels_per_forward_;
@@ -176,6 +205,22 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (!encode_tmap_nhwc(&a.tmap_a, bufs_[dw.in], max_bs, dw_in.h, dw_in.w, dw_in.c, a.dw_cb,
                             a.dw_iw, (a.dw_th - 1) * dw.sh + 3, 1))
         throw CudaError("cuTensorMapEncodeTiled failed (depthwise halo boxes)");
+    } else if (static_cast<int>(i) == s2d_.op) {
+      // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input
+      pl.mode = ConvLoadMode::kS2D;
+      a.R = s2d_.dr;
+      a.S = s2d_.ds;
+      a.C = 16;
+      a.taps = s2d_.dr * s2d_.ds;
+      a.num_kb = s2d_.kpad / kConvBK;
+      a.dw_th = 16;
+      a.dw_tw = 16;
+      a.dw_rw = 2;
+      a.dw_tiles_y = (out.h + 15) / 16;
+      a.dw_tiles_x = (out.w + 15) / 16;
+      a.win_box_bytes = 16 * 16 * 32;
+      if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, 16))
+        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem boxes)");
     } else if (static_cast<int>(i) == stem_) {
       pl.mode = ConvLoadMode::kStemU8;  // a.img is bound per launch (input slot)
     } else if (in.c == 4) {
@@ -205,8 +250,13 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }
-    if (!encode_tmap_2d_bf16(&a.tmap_b, d_w_ + hp.w_off.at(op.param), p.cout, kpad, kpad, a.BN))
+    if (pl.mode == ConvLoadMode::kS2D) {
+      if (!encode_tmap_2d_bf16(&a.tmap_b, d_stem_w_, p.cout, s2d_.kpad, s2d_.kpad, a.BN))
+        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem weights)");
+    } else if (!encode_tmap_2d_bf16(&a.tmap_b, d_w_ + hp.w_off.at(op.param), p.cout, kpad, kpad,
+                                    a.BN)) {
       throw CudaError("cuTensorMapEncodeTiled failed (weights)");
+    }
     if (pl.mode == ConvLoadMode::kTmaA) {
       const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
       if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
@@ -218,7 +268,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       const size_t esz = out.f32 ? 4 : 2;
       void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
-      if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow)  // pixel-row boxes
+      if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow ||
+          pl.mode == ConvLoadMode::kS2D)  // pixel-row boxes
         a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
                                                 a.dw_tw, a.dw_rw)
                       ? 1
@@ -254,7 +305,12 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
                  "mark");
   };
   record_mark();
-  if (stem_ < 0) {
+  if (s2d_.op >= 0) {
+    check_cuda(launch_stage_s2d(d_images_[slot], d_s2d_, bs, m.in_h, m.in_w, s2d_.hs, s2d_.ws,
+                                s2d_.pad, stream_),
+               "stage_s2d");
+    record_mark();
+  } else if (stem_ < 0) {
     check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs,
                                   m.in_h, m.in_w, stream_),
                "stage_input");

@@ -338,9 +338,46 @@ std::vector<bool> fused_depthwise(const ModelSpec& m) {
   return fused;
 }
 
+namespace {
+// The op that reads the staged input (buffer 0), when it is a conv and its only reader.
+int stem_op(const ModelSpec& m) {
+  int stem = -1;
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    if (op.in != 0 && op.residual != 0) continue;
+    if (stem >= 0 || op.kind != OpKind::kConv || op.residual == 0 || m.buffers[0].c != 4) return -1;
+    stem = static_cast<int>(i);
+  }
+  return stem;
+}
+}  // namespace
+
+S2dPlan stem_s2d(const ModelSpec& m) {
+  S2dPlan p;
+  const char* e = std::getenv("DS_STEM_S2D");
+  const char* staged = std::getenv("DS_STEM_STAGED");
+  if ((e && e[0] == '0') || (staged && staged[0] == '1')) return p;
+  const int stem = stem_op(m);
+  if (stem < 0) return p;
+  const OpSpec& op = m.ops[stem];
+  const BufferSpec& out = m.buffers[op.out];
+  const int cout = m.params[op.param].cout;
+  if (op.sh != 2 || op.sw != 2 || op.ph != op.pw || op.r > 8 || op.s > 8 || cout > 256) return p;
+  p.dr = (op.r + 1) / 2;
+  p.ds = (op.s + 1) / 2;
+  p.kpad = (p.dr * p.ds * 16 + 63) / 64 * 64;
+  if (p.kpad / 64 * ((cout + 15) / 16 * 16) * 128 > 64 * 1024) return p;  // weights stay resident
+  p.op = stem;
+  p.hs = out.h + p.dr - 1;
+  p.ws = out.w + p.ds - 1;
+  p.pad = op.ph;
+  return p;
+}
+
 int fused_stem(const ModelSpec& m) {
   const char* staged = std::getenv("DS_STEM_STAGED");  // A/B switch for the parity test
   if (staged && staged[0] == '1') return -1;
+  if (stem_s2d(m).op >= 0) return -1;  // the space-to-depth stem wins where it applies
   int stem = -1;
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
@@ -360,9 +397,14 @@ int fused_stem(const ModelSpec& m) {
 std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
   const std::vector<bool> fused = fused_depthwise(m);
   const int stem = fused_stem(m);
+  const S2dPlan s2d = stem_s2d(m);
   std::vector<KernelCost> out;
   const double px = static_cast<double>(m.in_h) * m.in_w;
-  if (stem < 0) out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
+  const double s2d_bytes = static_cast<double>(s2d.hs) * s2d.ws * 32;
+  if (s2d.op >= 0)
+    out.push_back({KernelKind::kStage, 0.0, px * 3 + s2d_bytes, 0.0});
+  else if (stem < 0)
+    out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
   for (const auto& op : m.ops) {
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out_b = m.buffers[op.out];
@@ -378,8 +420,8 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         k.flops_per_image = 2.0 * out_elems * p.r * p.s * p.cin;
         // the fused stem reads the u8 image (3 B per pixel) instead of the
         // staged bf16 tensor
-        const double in_bytes =
-            static_cast<int>(&op - m.ops.data()) == stem ? px * 3 : in_elems * 2;
+        const int oi = static_cast<int>(&op - m.ops.data());
+        const double in_bytes = oi == stem ? px * 3 : oi == s2d.op ? s2d_bytes : in_elems * 2;
         k.bytes_per_image = in_bytes + out_elems * (out_b.f32 ? 4 : 2) +
                             (op.residual >= 0 ? out_elems * 2 : 0.0);
         k.fixed_bytes = static_cast<double>(p.cout) * p.r * p.s * p.cin * 2 + p.cout * 4.0;

@@ -77,6 +77,16 @@ std::vector<bool> fused_depthwise(const ModelSpec& m);
 // kStemU8: staging fused into its producer), -1 when the staged bf16 input is
 // used (DS_STEM_STAGED=1, or buffer 0 has another reader).
 int fused_stem(const ModelSpec& m);
+
+// Stride-2 stem over a space-to-depth input (ConvLoadMode kS2D): a staging
+// kernel writes S[n][hs][ws][16] (2 x 2 pixel blocks of the normalised image)
+// and the stem becomes a stride-1 dr x ds conv over it. Returns the stem op
+// index (and the geometry) or -1 (DS_STEM_S2D=0, or not a stride-2 stem).
+struct S2dPlan {
+  int op = -1;
+  int hs = 0, ws = 0, dr = 0, ds = 0, pad = 0, kpad = 0;
+};
+S2dPlan stem_s2d(const ModelSpec& m);
 std::vector<std::string> model_ids();
 
 }  // namespace ds

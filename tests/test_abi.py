@@ -44,10 +44,14 @@ def test_device_free_entry_points():
     mi = model_info("mobilenet_v1")
     assert (mi.in_h, mi.in_w, mi.classes) == (224, 224, 1000)
     ks = kernel_costs("resnet50_v1")
-    # the stem reads the u8 images itself (staging fused), so the first
-    # launch is the stem conv: 3 B per input pixel instead of 3 B + 8 B
-    assert ks[0]["kind"] == "conv_gemm" and ks[-1]["kind"] == "softmax"
-    assert ks[0]["bytes_per_image"] < 224 * 224 * 3 + 112 * 112 * 64 * 2 + 1
+    # the 7x7/2 stem runs over a space-to-depth input: a staging launch
+    # (u8 image in, [115][115][16] bf16 out) then the stem conv
+    assert ks[0]["kind"] == "stage" and ks[1]["kind"] == "conv_gemm" and ks[-1]["kind"] == "softmax"
+    assert ks[0]["bytes_per_image"] == 224 * 224 * 3 + 115 * 115 * 16 * 2
+    # the stride-1 synthetic stem reads the u8 images itself (staging fused)
+    ks_syn = kernel_costs("synthetic_cnn")
+    assert ks_syn[0]["kind"] == "conv_gemm"
+    assert ks_syn[0]["bytes_per_image"] < 32 * 32 * 3 + 32 * 32 * 32 * 2 + 1
     assert abs(sum(k["flops_per_image"] for k in ks) - 2 * model_info("resnet50_v1").macs_per_image) < 1
     with pytest.raises(ValueError, match="unknown model"):
         model_info("vgg16")

@@ -118,6 +118,7 @@ def test_fused_stem_matches_staged_input(monkeypatch, model):
     the staging kernel + bf16-input stem: identical A operands, so identical
     logits; one launch fewer per forward."""
     imgs = generate_images(model, 3, 3)
+    monkeypatch.setenv("DS_STEM_S2D", "0")  # (the space-to-depth stem has its own test)
     with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
         fused = be.forward(imgs)
         k_fused = be.stats()["kernels_per_forward"]
@@ -127,6 +128,22 @@ def test_fused_stem_matches_staged_input(monkeypatch, model):
         k_staged = be.stats()["kernels_per_forward"]
     assert np.array_equal(fused, staged)
     assert k_staged == k_fused + 1
+
+
+@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2), ("inception_v3", 2)])
+def test_s2d_stem_matches_staged_input(monkeypatch, model, bs):
+    """Stride-2 stems over the space-to-depth input (kS2D: per-tap TMA boxes in
+    the MMA's 32 B-swizzled layout, 16 x 16 pixel blocks) against the staged
+    bf16 input + im2col gather: identical products, K summed in another
+    order, so logits agree to fp32-accumulation rounding."""
+    imgs = generate_images(model, 9, bs)
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        s2d = be.forward(imgs)
+    monkeypatch.setenv("DS_STEM_STAGED", "1")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        staged = be.forward(imgs)
+    assert np.isfinite(s2d).all()
+    assert row_rel_err(s2d, staged).max() <= 2e-3
 
 
 def test_softmax_probs():
