@@ -576,7 +576,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
   constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D);
   constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res, args.mt,
+  // (kWindow's A operands live in the halo boxes: its ring stages carry B only)
+  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res,
+                                   kWin ? 1 : args.mt,
                                    kDw ? static_cast<int>(args.dw_box_bytes) : 0,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0);
   const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
@@ -669,19 +671,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t acc = j & (n_acc - 1);
       ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
       ptx::tc_fence_after();
+      // pixel block of this tile (kBlk): image, block row / column
+      int b_img = 0, b_y = 0, b_x = 0;
+      if constexpr (kBlk) {
+        b_img = tw.mb / dw_blocks_per_img;
+        const int blk = tw.mb - b_img * dw_blocks_per_img;
+        b_y = blk / args.dw_tiles_x;
+        b_x = blk - b_y * args.dw_tiles_x;
+      }
       for (int q = 0; q < mt; ++q) {  // sub-tile q: rows m0 .. m0+127, columns q*BN ..
         const int m0 = tw.mb * tile_rows + q * kConvBM;
         if (!kBlk && m0 >= args.M) break;
         int m = m0 + quarter * 32 + lane;
-        if constexpr (kBlk) {  // A row -> pixel of the TH x TW block (args.M = not stored)
-          const int r = quarter * 32 + lane;
-          const int img = tw.mb / dw_blocks_per_img;
-          const int blk = tw.mb - img * dw_blocks_per_img;
-          const int by = blk / args.dw_tiles_x;
-          const int oy = by * args.dw_th + r / args.dw_tw;
-          const int ox = (blk - by * args.dw_tiles_x) * args.dw_tw + r % args.dw_tw;
+        if (kBlk && (args.residual || !args.y_tma)) {  // A row -> pixel (args.M = not stored)
+          const int r = q * kConvBM + quarter * 32 + lane;
+          const int oy = b_y * args.dw_th + r / args.dw_tw;
+          const int ox = b_x * args.dw_tw + r % args.dw_tw;
           m = r < args.dw_th * args.dw_tw && oy < args.Ho && ox < args.Wo
-                  ? (img * args.Ho + oy) * args.Wo + ox
+                  ? (b_img * args.Ho + oy) * args.Wo + ox
                   : args.M;
         }
         const uint32_t t_row = tmem_base + acc * acc_stride + q * args.BN +
@@ -705,14 +712,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             __syncwarp();
             if (lane == 0) {
               if constexpr (kBlk) {  // this warp's rw pixel rows of the TH x TW block
-                const int img = tw.mb / dw_blocks_per_img;
-                const int blk = tw.mb - img * dw_blocks_per_img;
-                const int by = blk / args.dw_tiles_x;
                 const int yq = q * (kConvBM / args.dw_tw) + quarter * args.dw_rw;  // in-block row
-                const int y0 = by * args.dw_th + yq;
                 if (yq < args.dw_th)
-                  ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0,
-                                    (blk - by * args.dw_tiles_x) * args.dw_tw, y0, img);
+                  ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, b_x * args.dw_tw,
+                                    b_y * args.dw_th + yq, b_img);
               } else {
                 ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
               }
@@ -966,7 +969,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tc_fence_after();
           const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + kb * b_bytes));
           const int nt = min(4, taps - kb * 4);
-          for (int tl = 0; tl < nt; ++tl)
+          for (int tl = 0; tl < nt && !(args.debug_flags & 16); ++tl)  // (flag 16: bring-up)
             for (int q = 0; q < mt; ++q) {
               const uint64_t da = ptx::umma_desc_sw32_kmajor(ptx::smem_u32(
                   smem + L.a_off + s * a_stage + tl * args.win_box_bytes + q * kConvBM * 32));
@@ -1009,16 +1012,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               ptx::tc_fence_after();
             }
             const int dr = t / args.S, dc = t - (t / args.S) * args.S;
-            const uint64_t da = ptx::umma_desc_none_kmajor(
-                cm + static_cast<uint32_t>(dr * args.win_iw + dc) * 16, lbo, sbo);
             const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(
                 smem + L.b_off + (b_res ? kb * win_taps + t : static_cast<int>(s)) * b_bytes));
-            for (int k = 0; k < ksteps; ++k) {
-              // next K=16 step: two chunk planes further (start field is addr >> 4)
-              ptx::umma_bf16(d, da + static_cast<uint64_t>(2 * k) * (lbo >> 4), db + 2 * k, idesc,
-                             first ? 0u : 1u);
-              first = false;
+            for (int q = 0; q < mt; ++q) {  // sub-tile q: pixel rows 16q .. 16q+15 of the block
+              const uint64_t da = ptx::umma_desc_none_kmajor(
+                  cm + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 16, lbo, sbo);
+              for (int k = 0; k < ksteps; ++k)  // next K=16 step: two chunk planes further
+                ptx::umma_bf16(d + q * args.BN, da + static_cast<uint64_t>(2 * k) * (lbo >> 4),
+                               db + 2 * k, idesc, first && k == 0 ? 0u : 1u);
             }
+            first = false;
             if (!b_res) {
               ptx::umma_commit(&empty[s]);
               rp.next(args.stages);
@@ -1343,7 +1346,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   };
   static const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
                    teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
-  const int mt_cap = mode == ConvLoadMode::kS2D ? 2
+  const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
+                     : mode == ConvLoadMode::kS2D ? 2
                      : mode == ConvLoadMode::kStemU8 ? mt_stem
                      : mode == ConvLoadMode::kTmaA ? mt_tma
                                                    : 1;
@@ -1407,6 +1411,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     if (!args.y_tma || n_tiles != 1 || args.num_kb * args.BN * 128 > 64 * 1024)
       return cudaErrorInvalidValue;
     args.b_res = args.num_kb;
+    // no producer warps: all sixteen non-TMA/MMA warps drain accumulators
+    // (four epilogue teams) when their staging still leaves a 2-deep ring
+    if (args.n_acc >= 4 && conv_gemm_stages(args.BN, args.Cout, 16, args.b_res, 2) >= 2) args.teams = 4;
     args.stages = std::min(6, conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, args.b_res, 2));
     if (args.stages < 2) return cudaErrorInvalidValue;
   }

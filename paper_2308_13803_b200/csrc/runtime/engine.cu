@@ -1,6 +1,7 @@
 #include "engine.hpp"
 
 #include <cstdio>
+#include <string>
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -39,6 +40,17 @@ uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 // Opt-in: parity-tested, but its fixed 16 x 8 pixel tiles waste a third of
 // the MMA rows on 28/14/7-wide layers and the 2-deep box rings expose the
 // halo load, so the im2col gather is still faster on B200.
+// DS_STEM_S2D_MODE=window: the s2d stem as a kWindow conv (one halo box per
+// 32 x 8 block, transposed by the gather warps) instead of kS2D (one TMA box
+// per tap in the MMA's layout, no producer warps; faster on B200). A/B switch.
+bool s2d_window() {
+  static const bool on = [] {
+    const char* e = std::getenv("DS_STEM_S2D_MODE");
+    return e && std::string(e) == "window";
+  }();
+  return on;
+}
+
 bool window_on() {
   static const bool on = [] {
     const char* e = std::getenv("DS_CONV_WINDOW");
@@ -205,6 +217,27 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (!encode_tmap_nhwc(&a.tmap_a, bufs_[dw.in], max_bs, dw_in.h, dw_in.w, dw_in.c, a.dw_cb,
                             a.dw_iw, (a.dw_th - 1) * dw.sh + 3, 1))
         throw CudaError("cuTensorMapEncodeTiled failed (depthwise halo boxes)");
+    } else if (static_cast<int>(i) == s2d_.op && s2d_window()) {
+      // stride-2 stem as a stride-1 dr x ds window conv over the 16-channel
+      // s2d input (padding already inside it): one halo box per 32 x 8 block
+      pl.mode = ConvLoadMode::kWindow;
+      a.R = s2d_.dr;
+      a.S = s2d_.ds;
+      a.C = 16;
+      a.pad_h = a.pad_w = 0;
+      a.taps = s2d_.dr * s2d_.ds;
+      a.mt = 2;
+      a.dw_th = 16 * a.mt;
+      a.dw_tw = 8;
+      a.dw_rw = 4;
+      a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
+      a.dw_tiles_x = (out.w + 7) / 8;
+      a.win_iw = 8 + a.S - 1;
+      a.win_ih = a.dw_th + a.R - 1;
+      a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * 16 * 2);
+      if (!encode_tmap_nhwc(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, a.win_iw,
+                            a.win_ih, 1))
+        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem halo boxes)");
     } else if (static_cast<int>(i) == s2d_.op) {
       // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input
       pl.mode = ConvLoadMode::kS2D;
@@ -250,7 +283,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }
-    if (pl.mode == ConvLoadMode::kS2D) {
+    if (static_cast<int>(i) == s2d_.op) {
       if (!encode_tmap_2d_bf16(&a.tmap_b, d_stem_w_, p.cout, s2d_.kpad, s2d_.kpad, a.BN))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem weights)");
     } else if (!encode_tmap_2d_bf16(&a.tmap_b, d_w_ + hp.w_off.at(op.param), p.cout, kpad, kpad,

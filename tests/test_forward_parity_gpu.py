@@ -130,13 +130,15 @@ def test_fused_stem_matches_staged_input(monkeypatch, model):
     assert k_staged == k_fused + 1
 
 
+@pytest.mark.parametrize("mode", ["tap", "window"])
 @pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2), ("inception_v3", 2)])
-def test_s2d_stem_matches_staged_input(monkeypatch, model, bs):
+def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
     """Stride-2 stems over the space-to-depth input (kS2D: per-tap TMA boxes in
     the MMA's 32 B-swizzled layout, 16 x 16 pixel blocks) against the staged
     bf16 input + im2col gather: identical products, K summed in another
     order, so logits agree to fp32-accumulation rounding."""
     imgs = generate_images(model, 9, bs)
+    monkeypatch.setenv("DS_STEM_S2D_MODE", mode)  # kS2D tap boxes | kWindow halo box
     with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
         s2d = be.forward(imgs)
     monkeypatch.setenv("DS_STEM_STAGED", "1")

@@ -1,4 +1,4 @@
-mkdir -p gpurun_out/models1
-for m in resnet50_v1 inception_v3 synthetic_cnn; do
-  timeout 600 python bench.py --model $m --kernel-table --no-cpu-baseline > gpurun_out/models1/$m.json 2>gpurun_out/models1/$m.err
+mkdir -p gpurun_out/dbg12
+for f in 0 1 16 17; do
+  DS_CONV_DEBUG=0:$f timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --steps 3 --warmup 3 --max-converge 1 > gpurun_out/dbg12/b$f.json 2>/dev/null
 done
