@@ -70,11 +70,17 @@ __global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restr
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       const int y = 2 * Y + a - pad, x = 2 * X + b - pad;
+      // bf16_rn(centered * (1/63.75)) == bf16_rn((p - 127.5) / 63.75) for every
+      // byte (tests/test_oracle.py::test_stem_normalisation_exact); the
+      // centred value comes from the bit pattern 0x4A800000 + 2p + 1 = 2^22 +
+      // p + 0.5 minus (2^22 + 128), exactly and without the conversion pipe
       float f[3] = {0.f, 0.f, 0.f};
       if (y >= 0 && y < h && x >= 0 && x < w) {
         const uint8_t* src = img + ((n * h + y) * w + x) * 3;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) f[c] = (static_cast<float>(src[c]) - 127.5f) / 63.75f;
+        for (int c = 0; c < 3; ++c)
+          f[c] = __fmul_rn(__fsub_rn(__uint_as_float(0x4A800001u + 2u * __ldg(src + c)), 4194432.0f),
+                           1.0f / 63.75f);
       }
       v[(a * 2 + b) * 2] = pack2(f[0], f[1]);
       v[(a * 2 + b) * 2 + 1] = pack2(f[2], 0.0f);
