@@ -204,7 +204,7 @@ def cpu_baseline(model, seconds=12.0):
     t0 = time.perf_counter()
     oracle.forward(model, imgs, bf16_storage=False, threads=threads)
     one = time.perf_counter() - t0
-    n = int(max(threads, min(512, seconds / max(one, 1e-6) * threads)))
+    n = int(max(threads, min(8192, seconds / max(one, 1e-6) * threads)))
     n = max(threads, (n // threads) * threads)
     imgs = oracle.images(model, 0, n)
     t0 = time.perf_counter()

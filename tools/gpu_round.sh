@@ -8,7 +8,7 @@ OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
 if [ "${2:-tests}" = "tests" ]; then
-  timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+  timeout 1200 python -m pytest tests -m gpu -q --timeout=300 --timeout-method=thread > "$OUT/pytest_gpu.log" 2>&1
   echo "pytest exit $?" >> "$OUT/pytest_gpu.log"
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
   echo "smoke exit $?" >> "$OUT/smoke.log"
