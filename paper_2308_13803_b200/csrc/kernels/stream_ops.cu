@@ -262,7 +262,22 @@ __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __rest
   const long long n = i / cg;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint4* p = x + n * hw * cg + g;
-  for (int q = 0; q < hw; ++q) {
+  // pixels in order (the oracle's summation order), loads issued 8 ahead
+  constexpr int U = 8;
+  int q = 0;
+  for (; q + U <= hw; q += U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(p + static_cast<long long>(q + u) * cg);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float xv[8];
+      unpack8(v[u], xv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += xv[e];
+    }
+  }
+  for (; q < hw; ++q) {
     float xv[8];
     unpack8(__ldg(p + static_cast<long long>(q) * cg), xv);
 #pragma unroll
@@ -282,6 +297,35 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const float* l = logits + static_cast<long long>(row) * classes;
+  float* p = probs + static_cast<long long>(row) * classes;
+  if (classes <= 32 * 32) {  // the row in registers: one independent load per element
+    float v[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int j = lane + 32 * u;
+      v[u] = j < classes ? l[j] : -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) mx = fmaxf(mx, v[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      v[u] = lane + 32 * u < classes ? expf(v[u] - mx) : 0.0f;
+      sum += v[u];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv = 1.0f / sum;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int j = lane + 32 * u;
+      if (j < classes) p[j] = v[u] * inv;
+    }
+    return;
+  }
   float mx = -INFINITY;
   for (int j = lane; j < classes; j += 32) mx = fmaxf(mx, l[j]);
 #pragma unroll
@@ -291,7 +335,6 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float inv = 1.0f / sum;
-  float* p = probs + static_cast<long long>(row) * classes;
   for (int j = lane; j < classes; j += 32) p[j] = expf(l[j] - mx) * inv;
 }
 

@@ -180,7 +180,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.num_kb = kpad / kConvBK;
     a.taps = op.r * op.s;
     a.Cout = p.cout;
-    a.BN = choose_bn(p.cout);
+    // FC heads have one or two M tiles at serving batch sizes: narrow N tiles
+    // spread their long K loop over 16+ SMs instead of 4
+    a.BN = op.kind == OpKind::kFc ? 64 : choose_bn(p.cout);
     a.stages = choose_stages(a.BN, p.cout);
     a.tmem_cols = tmem_cols_for(a.BN);
     a.bias = d_b_ + hp.b_off.at(op.param);
