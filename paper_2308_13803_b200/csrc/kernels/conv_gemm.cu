@@ -97,21 +97,28 @@ struct RingPos {
 
 // This CTA's tiles (tile = blockIdx.x + j * gridDim.x) as (M block, N block),
 // N block fastest, walked without divisions.
+// With clusters of 2 (multicast weights), the unit is an (M-block pair, N
+// block): cluster c walks units c, c + C, ... (C clusters) and its CTA of rank
+// r takes M block 2 * pair + r, so both CTAs share every B block.
 struct TileWalk {
-  int mb, nb, step_m, step_n, n_tiles;
-  __device__ __forceinline__ explicit TileWalk(int n) : n_tiles(n) {
-    mb = blockIdx.x / n;
-    nb = blockIdx.x - mb * n;
-    step_m = gridDim.x / n;
-    step_n = gridDim.x - step_m * n;
+  int mb, nb, step_m, step_n, n_tiles, pair, rank, cl;
+  __device__ __forceinline__ explicit TileWalk(int n, int cluster = 1) : n_tiles(n), cl(cluster) {
+    const int first = blockIdx.x / cluster, stride = gridDim.x / cluster;
+    rank = cluster > 1 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+    pair = first / n;
+    nb = first - pair * n;
+    step_m = stride / n;
+    step_n = stride - step_m * n;
+    mb = pair * cluster + rank;
   }
   __device__ __forceinline__ void next() {
-    mb += step_m;
+    pair += step_m;
     nb += step_n;
     if (nb >= n_tiles) {
       nb -= n_tiles;
-      ++mb;
+      ++pair;
     }
+    mb = pair * cl + rank;
   }
 };
 
@@ -613,6 +620,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int win_cblocks = (args.C + 63) / 64;  // kWindow: 64-channel K blocks
   const int win_taps = args.R * args.S;
   const int tiles = n_tiles * m_blocks;
+  // (cluster mode: the loops below walk units = (M-block pair, N block))
+  const int cl = args.cluster > 1 ? args.cluster : 1;
+  const int walk_first = blockIdx.x / cl, walk_stride = gridDim.x / cl;
+  const int walk_count = cl == 1 ? tiles : n_tiles * ((m_blocks + cl - 1) / cl);
+  const uint16_t cl_mask = static_cast<uint16_t>((1u << cl) - 1u);
   const int n_acc = args.n_acc;  // power of two
   const int acc_log2 = __ffs(n_acc) - 1;
   const uint32_t acc_stride = args.tmem_cols / n_acc;
@@ -626,7 +638,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                        ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
         ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
-        ptx::mbar_init(&empty[s], 1);
+        ptx::mbar_init(&empty[s], cl);  // (cluster: both CTAs' MMAs consume a multicast B slot)
         ptx::mbar_init(&box_full[s], 1);
       }
       ptx::mbar_init(b_full, 1);
@@ -650,6 +662,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (cl > 1) ptx::cluster_sync();  // peers' barriers exist before any multicast lands
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
@@ -664,8 +677,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;
     const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
     uint32_t j = 0, groups = 0;
-    TileWalk tw(n_tiles);
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j, tw.next()) {
+    TileWalk tw(n_tiles, cl);
+    for (int tile = walk_first; tile < walk_count; tile += walk_stride, ++j, tw.next()) {
       if (static_cast<int>(j & (args.teams - 1)) != team) continue;  // teams: power of two
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
@@ -908,8 +921,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0) + (kDw ? 1u : 0u);
       uint32_t j = 0;
       RingPos rp;
-      TileWalk tw(n_tiles);
-      for (int tile = blockIdx.x; tile < (tx ? tiles : 0); tile += gridDim.x, ++j, tw.next()) {
+      TileWalk tw(n_tiles, cl);
+      for (int tile = walk_first; tile < (tx ? walk_count : 0); tile += walk_stride, ++j, tw.next()) {
         const int m0 = tw.mb * tile_rows;
         const int n0 = tw.nb * args.BN;
         for (int kb = 0; kb < args.num_kb; ++kb) {
@@ -939,9 +952,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (b_res) continue;
           }
           ptx::mbar_arrive_expect_tx(&full[s], tx - (kDw ? 1u : 0u));
-          if (!b_res)
+          if (!b_res && cl > 1) {  // this CTA's half of the B block, to both CTAs
+            const uint32_t half = b_bytes / cl;
+            ptx::tma_load_2d_mc(ptx::smem_u32(smem + L.b_off + s * b_bytes + tw.rank * half),
+                                &args.tmap_b, &full[s], kb * kConvBK,
+                                n0 + tw.rank * (args.BN / cl), cl_mask);
+          } else if (!b_res) {
             ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                              kb * kConvBK, n0);
+          }
           if constexpr (kTmaA)
             for (int q = 0; q < mt; ++q)  // (rows past M arrive as zeros)
               ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes),
@@ -1040,7 +1059,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (args.b_res > 0) ptx::mbar_wait(b_full, 0);
       uint32_t j = 0;
       RingPos rp;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+      for (int tile = walk_first; tile < walk_count; tile += walk_stride, ++j) {
         const uint32_t acc = j & (n_acc - 1);
         if (j >= static_cast<uint32_t>(n_acc))
           ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
@@ -1069,7 +1088,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               ptx::umma_bf16(d + q * args.BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             }
           }
-          ptx::umma_commit(&empty[s]);
+          if (cl > 1)
+            ptx::umma_commit_mc(&empty[s], cl_mask);  // both CTAs read this B slot
+          else
+            ptx::umma_commit(&empty[s]);
         }
         ptx::umma_commit(&tmem_full[acc]);
       }
@@ -1079,6 +1101,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (cl > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == kTmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, args.tmem_cols);
@@ -1372,6 +1395,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     return !(e && e[0] == '0');
   }();
   args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
+  if (args.cluster > 1) args.b_res = 0;  // (multicast B streams through the ring)
   const int bres = args.b_res;
   args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, bres, args.mt);
   const bool dw = mode == ConvLoadMode::kDwFused;
@@ -1441,6 +1465,15 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
   const int per_sm = std::max(1, std::min(by_smem, by_tmem));
+  if (args.cluster > 1) {  // pairs of CTAs over (M-block pair, N block) units
+    if (mode != ConvLoadMode::kTmaA || args.b_res > 0 || args.cluster != 2) return cudaErrorInvalidValue;
+    const int m_blocks = (args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt);
+    const int units = n_tiles * ((m_blocks + 1) / 2);
+    const int ctas = std::min(2 * units, conv_gemm_sm_count() * per_sm) / 2 * 2;
+    return launch_pdl_cluster(conv_gemm_kernel<2>, dim3(ctas), dim3(kConvThreads), smem, stream, 2,
+                              args);
+  }
+  args.cluster = 1;
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
   switch (mode) {
     case ConvLoadMode::kGather16:

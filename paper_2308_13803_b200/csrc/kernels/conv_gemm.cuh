@@ -43,6 +43,8 @@ struct ConvGemmArgs {
   int teams, n_acc;
   int b_res;  // > 0: all num_kb weight blocks resident in smem (one N tile)
   int mt;     // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
+  int cluster;  // kTmaA: 2 = CTA pairs share (multicast) every weight block; tmap_b box
+                // rows are then BN / 2 (each CTA loads one half for both)
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;

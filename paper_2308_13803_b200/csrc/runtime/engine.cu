@@ -51,6 +51,18 @@ bool s2d_window() {
   return on;
 }
 
+// DS_CONV_CLUSTER=1: CTA pairs multicast the weight blocks of the 256-wide
+// TMA-A layers. Opt-in: measured no faster on B200 (L2 already merges the two
+// CTAs' near-simultaneous reads of a block; these layers are bound by shared-
+// memory traffic per MMA at 128 x 256 tiles, which 2-SM MMAs would halve).
+bool cluster_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DS_CONV_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool window_on() {
   static const bool on = [] {
     const char* e = std::getenv("DS_CONV_WINDOW");
@@ -285,11 +297,14 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }
+    // wide TMA-A layers: CTA pairs may multicast each weight block (opt-in)
+    const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
+    a.cluster = pl.mode == ConvLoadMode::kTmaA && a.BN == 256 && !b_resident && cluster_on() ? 2 : 1;
     if (static_cast<int>(i) == s2d_.op) {
       if (!encode_tmap_2d_bf16(&a.tmap_b, d_stem_w_, p.cout, s2d_.kpad, s2d_.kpad, a.BN))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem weights)");
     } else if (!encode_tmap_2d_bf16(&a.tmap_b, d_w_ + hp.w_off.at(op.param), p.cout, kpad, kpad,
-                                    a.BN)) {
+                                    a.BN / a.cluster)) {
       throw CudaError("cuTensorMapEncodeTiled failed (weights)");
     }
     if (pl.mode == ConvLoadMode::kTmaA) {

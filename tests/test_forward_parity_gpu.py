@@ -111,6 +111,21 @@ def test_window_conv_matches_im2col_gather(monkeypatch, model, bs):
     assert row_rel_err(win, gather).max() <= 2e-3
 
 
+@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 5), ("resnet50_v1", 3)])
+def test_cluster_multicast_matches_single_cta(monkeypatch, model, bs):
+    """CTA pairs sharing multicast weight blocks (DS_CONV_CLUSTER=1: each CTA
+    loads half of every B block for both, empty slots need both MMAs'
+    commits) compute exactly the single-CTA tiles: bit-identical logits."""
+    imgs = generate_images(model, 13, bs)
+    monkeypatch.setenv("DS_CONV_CLUSTER", "1")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        pair = be.forward(imgs)
+    monkeypatch.setenv("DS_CONV_CLUSTER", "0")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        single = be.forward(imgs)
+    assert np.array_equal(pair, single)
+
+
 @pytest.mark.parametrize("model", ["synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"])
 def test_fused_stem_matches_staged_input(monkeypatch, model):
     """The stem conv reading u8 images directly (kStemU8: the staging
