@@ -848,6 +848,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int blk = tw.mb - img * dw_blocks_per_img;
         const int by = blk / args.dw_tiles_x;
         const int bx = blk - by * args.dw_tiles_x;
+        if (args.win_iw > 0) {  // one halo box per block holds every tap's window
+          const uint32_t s = rp.slot;
+          if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&full[s], args.win_box_bytes);
+          asm volatile(
+              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + L.a_off + s * a_stage)),
+              "l"(&args.tmap_a), "r"(ptx::smem_u32(&full[s])), "r"(0), "r"(bx * args.dw_tw),
+              "r"(by * args.dw_th), "r"(img)
+              : "memory");
+          rp.next(args.stages);
+          continue;
+        }
         for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
           const uint32_t s = rp.slot;
           if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
@@ -982,6 +995,28 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
+        if (args.win_iw > 0) {  // windows of the block's halo box: tap (dr, dc) starts at
+                                // pixel (16 q + dr) * IW + dc, pixel rows sbo = IW * 32 B apart
+          const uint32_t s = rp.slot;
+          ptx::mbar_wait(&full[s], rp.lap & 1);
+          ptx::tc_fence_after();
+          const uint32_t box = ptx::smem_u32(smem + L.a_off + s * a_stage);
+          const uint32_t sbo = static_cast<uint32_t>(args.win_iw) * 32;
+          for (int t = 0; t < taps && !(args.debug_flags & 16); ++t) {
+            const int dr = t / args.S, dc = t - (t / args.S) * args.S;
+            const uint64_t db = ptx::umma_desc_sw128_kmajor(
+                ptx::smem_u32(smem + L.b_off + (t >> 2) * b_bytes));
+            for (int q = 0; q < mt; ++q) {
+              const uint64_t da = ptx::umma_desc_sw32_kmajor_sbo(
+                  box + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 32, sbo);
+              ptx::umma_bf16(d + q * args.BN, da, db + 2 * (t & 3), idesc, t != 0);
+            }
+          }
+          ptx::umma_commit(&empty[s]);
+          rp.next(args.stages);
+          ptx::umma_commit(&tmem_full[acc]);
+          continue;
+        }
         for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
           const uint32_t s = rp.slot;
           ptx::mbar_wait(&full[s], rp.lap & 1);

@@ -298,6 +298,20 @@ __device__ __forceinline__ uint64_t umma_desc_sw32_kmajor(uint32_t smem_addr) {
   return d;
 }
 
+// SWIZZLE_32B K-major with an explicit 8-row-group stride: a window of a
+// wider 32 B-swizzled box (rows of the window are 32 B apart within a group,
+// groups sbo apart); the swizzle is a function of the absolute smem address,
+// so a window may start at any 32 B row of a 1 KiB-aligned TMA box.
+__device__ __forceinline__ uint64_t umma_desc_sw32_kmajor_sbo(uint32_t smem_addr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(6) << 61;
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);

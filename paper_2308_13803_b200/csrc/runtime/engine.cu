@@ -63,6 +63,18 @@ bool cluster_on() {
   return on;
 }
 
+// DS_STEM_S2D_MODE=box: the kS2D stem with one halo box per 32 x 8 block
+// (every tap an MMA window of it) instead of one TMA box per tap. Bit-exact
+// and a third of the TMA bytes, but the windows' unaligned 32 B-swizzle rows
+// cost more shared-memory wavefronts per MMA: slower on B200 (A/B switch).
+bool s2d_tap_boxes() {
+  static const bool on = [] {
+    const char* e = std::getenv("DS_STEM_S2D_MODE");
+    return !(e && (std::string(e) == "box" || std::string(e) == "window"));
+  }();
+  return on;
+}
+
 bool window_on() {
   static const bool on = [] {
     const char* e = std::getenv("DS_CONV_WINDOW");
@@ -252,8 +264,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (!encode_tmap_nhwc(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, a.win_iw,
                             a.win_ih, 1))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem halo boxes)");
-    } else if (static_cast<int>(i) == s2d_.op) {
-      // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input
+    } else if (static_cast<int>(i) == s2d_.op && s2d_tap_boxes()) {
+      // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input,
+      // one 16 x 16 TMA box per tap
       pl.mode = ConvLoadMode::kS2D;
       a.R = s2d_.dr;
       a.S = s2d_.ds;
@@ -265,9 +278,30 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.dw_rw = 2;
       a.dw_tiles_y = (out.h + 15) / 16;
       a.dw_tiles_x = (out.w + 15) / 16;
+      a.win_iw = 0;
       a.win_box_bytes = 16 * 16 * 32;
       if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, 16))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem boxes)");
+    } else if (static_cast<int>(i) == s2d_.op) {
+      // the same, with one halo box per 32 x 8 block: every tap is a window of
+      // it (8-pixel rows = the MMA's 8-row groups, SBO = box row pitch)
+      pl.mode = ConvLoadMode::kS2D;
+      a.R = s2d_.dr;
+      a.S = s2d_.ds;
+      a.C = 16;
+      a.taps = s2d_.dr * s2d_.ds;
+      a.num_kb = s2d_.kpad / kConvBK;
+      a.dw_th = 32;
+      a.dw_tw = 8;
+      a.dw_rw = 4;
+      a.dw_tiles_y = (out.h + 31) / 32;
+      a.dw_tiles_x = (out.w + 7) / 8;
+      a.win_iw = 8 + a.S - 1;
+      a.win_ih = 32 + a.R - 1;
+      a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * 32);
+      if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, a.win_iw,
+                                 a.win_ih))
+        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem halo boxes)");
     } else if (static_cast<int>(i) == stem_) {
       pl.mode = ConvLoadMode::kStemU8;  // a.img is bound per launch (input slot)
     } else if (in.c == 4) {

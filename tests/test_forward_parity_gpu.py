@@ -145,7 +145,7 @@ def test_fused_stem_matches_staged_input(monkeypatch, model):
     assert k_staged == k_fused + 1
 
 
-@pytest.mark.parametrize("mode", ["tap", "window"])
+@pytest.mark.parametrize("mode", ["box", "tap", "window"])
 @pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2), ("inception_v3", 2)])
 def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
     """Stride-2 stems over the space-to-depth input (kS2D: per-tap TMA boxes in
@@ -153,7 +153,7 @@ def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
     bf16 input + im2col gather: identical products, K summed in another
     order, so logits agree to fp32-accumulation rounding."""
     imgs = generate_images(model, 9, bs)
-    monkeypatch.setenv("DS_STEM_S2D_MODE", mode)  # kS2D tap boxes | kWindow halo box
+    monkeypatch.setenv("DS_STEM_S2D_MODE", mode)  # kS2D halo box | kS2D tap boxes | kWindow
     with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
         s2d = be.forward(imgs)
     monkeypatch.setenv("DS_STEM_STAGED", "1")
@@ -161,6 +161,22 @@ def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
         staged = be.forward(imgs)
     assert np.isfinite(s2d).all()
     assert row_rel_err(s2d, staged).max() <= 2e-3
+
+
+@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2)])
+def test_s2d_halo_box_windows_match_tap_boxes(monkeypatch, model, bs):
+    """kS2D with one 32 B-swizzled halo box per 32 x 8 block, each tap an MMA
+    window starting at an arbitrary 32 B row of it (explicit SBO = box row
+    pitch), against one TMA box per tap: same operands, same MMA order, so
+    bit-identical logits."""
+    imgs = generate_images(model, 21, bs)
+    monkeypatch.setenv("DS_STEM_S2D_MODE", "box")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        box = be.forward(imgs)
+    monkeypatch.setenv("DS_STEM_S2D_MODE", "tap")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        tap = be.forward(imgs)
+    assert np.array_equal(box, tap)
 
 
 def test_softmax_probs():
