@@ -603,13 +603,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
   uint64_t* b_full = tmem_empty + kMaxAcc;    // resident B landed (b_res)
   uint64_t* box_full = b_full + 1;            // [stages] kDwFused halo box landed
+  // kWindow barriers [8]: transposing mode raw_full[2] raw_free[2] cm_full[2]
+  // cm_empty[2]; direct mode (128 B-swizzled box read in place) slot_full[4]
+  // slot_free[4]
   uint64_t* raw_full = box_full + args.stages;  // [2] kWindow: pixel-major box landed
   uint64_t* raw_free = raw_full + 2;            // [2] ... transposed (gather warps)
   uint64_t* cm_full = raw_free + 2;             // [2] chunk-major box ready
   uint64_t* cm_empty = cm_full + 2;             // [2] all taps of its K block consumed
+  uint64_t* slot_full = raw_full;               // [4] direct mode: box landed
+  uint64_t* slot_free = raw_full + 4;           // [4] direct mode: all taps consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cm_empty + 2);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index via a shuffle: provably warp-uniform, so role branches are
+  // uniform and the MMA-issue loops keep their operands in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
   const int tile_rows = kConvBM * mt;
@@ -644,8 +651,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       ptx::mbar_init(b_full, 1);
       for (int b = 0; b < 2; ++b) {
         ptx::mbar_init(&raw_full[b], 1);
-        ptx::mbar_init(&raw_free[b], kGatherWarps);
-        ptx::mbar_init(&cm_full[b], kGatherWarps);
+        ptx::mbar_init(&raw_free[b], args.win_direct ? 1 : kGatherWarps);
+        ptx::mbar_init(&cm_full[b], args.win_direct ? 1 : kGatherWarps);
         ptx::mbar_init(&cm_empty[b], 1);
       }
       for (int b = 0; b < n_acc; ++b) {
@@ -780,7 +787,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int cb = args.C < 64 ? args.C : 64;
       const int raw_chunks = cb / 8;  // 16 B chunks per raw pixel row
       uint32_t u = 0;                  // box uses so far (slot u & 1, phase u >> 1)
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      // (direct mode: the MMA reads the TMA's 128 B-swizzled box itself)
+      for (int tile = blockIdx.x; tile < (args.win_direct ? 0 : tiles); tile += gridDim.x) {
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
           const uint32_t b = u & 1, ph = (u >> 1) & 1;
           ptx::mbar_wait(&raw_full[b], ph);
@@ -900,9 +908,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int by = blk / args.dw_tiles_x;
         const int bx = blk - by * args.dw_tiles_x;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
-          const uint32_t b = u & 1, ph = (u >> 1) & 1;
-          if (u >= 2) ptx::mbar_wait(&raw_free[b], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&raw_full[b], args.win_box_bytes);
+          // (direct mode: 4 box slots, the MMA frees them; else 2 + 2 transposed)
+          const uint32_t nb_slots = args.win_direct ? 4u : 2u;
+          const uint32_t b = u % nb_slots, ph = (u / nb_slots) & 1;
+          if (u >= nb_slots) ptx::mbar_wait(args.win_direct ? &slot_free[b] : &raw_free[b], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&raw_full[b], args.win_box_bytes);  // (== slot_full[b])
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
@@ -982,7 +992,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else if (kS2) {  // kMmaWarp: per tap, sub-tile q reads its 128 rows of the tap box
-    if (lane == 0) {
+    {  // (whole warp: uniform descriptors, elected issue)
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
       ptx::mbar_wait(b_full, 0);
@@ -1002,19 +1012,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tc_fence_after();
           const uint32_t box = ptx::smem_u32(smem + L.a_off + s * a_stage);
           const uint32_t sbo = static_cast<uint32_t>(args.win_iw) * 32;
-          for (int t = 0; t < taps && !(args.debug_flags & 16); ++t) {
-            const int dr = t / args.S, dc = t - (t / args.S) * args.S;
+          for (int t = 0, dr = 0, dc = 0; t < taps && !(args.debug_flags & 16);
+               ++t, dc = dc + 1 == args.S ? 0 : dc + 1, dr = dc == 0 ? dr + 1 : dr) {
             const uint64_t db = ptx::umma_desc_sw128_kmajor(
                 ptx::smem_u32(smem + L.b_off + (t >> 2) * b_bytes));
             for (int q = 0; q < mt; ++q) {
               const uint64_t da = ptx::umma_desc_sw32_kmajor_sbo(
                   box + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 32, sbo);
-              ptx::umma_bf16(d + q * args.BN, da, db + 2 * (t & 3), idesc, t != 0);
+              ptx::umma_bf16_warp(d + q * args.BN, da, db + 2 * (t & 3), idesc, t != 0);
             }
           }
-          ptx::umma_commit(&empty[s]);
+          ptx::umma_commit_warp(&empty[s]);
           rp.next(args.stages);
-          ptx::umma_commit(&tmem_full[acc]);
+          ptx::umma_commit_warp(&tmem_full[acc]);
           continue;
         }
         for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
@@ -1027,16 +1037,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int q = 0; q < mt; ++q) {
               const uint64_t da = ptx::umma_desc_sw32_kmajor(ptx::smem_u32(
                   smem + L.a_off + s * a_stage + tl * args.win_box_bytes + q * kConvBM * 32));
-              ptx::umma_bf16(d + q * args.BN, da, db + 2 * tl, idesc, (kb | tl) != 0);
+              ptx::umma_bf16_warp(d + q * args.BN, da, db + 2 * tl, idesc, (kb | tl) != 0);
             }
-          ptx::umma_commit(&empty[s]);
+          ptx::umma_commit_warp(&empty[s]);
         }
-        ptx::umma_commit(&tmem_full[acc]);
+        ptx::umma_commit_warp(&tmem_full[acc]);
       }
     }
     __syncwarp();
-  } else if (kWin) {  // kMmaWarp, shifted-window MMAs
-    if (lane == 0) {
+  } else if (kWin) {  // kMmaWarp, shifted-window MMAs (whole warp, elected issue)
+    {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
       const bool b_res = args.b_res > 0;
@@ -1045,19 +1055,31 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t lbo = npix * 16, sbo = static_cast<uint32_t>(args.win_iw) * 16;
       uint32_t j = 0, u = 0;
       RingPos rp;
+      unsigned long long t_acc = 0, t_box = 0, t_all = clock64();  // (flag 32: probe)
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
         const uint32_t acc = j & (n_acc - 1);
+        unsigned long long t0 = clock64();
         if (j >= static_cast<uint32_t>(n_acc))
           ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
+        t_acc += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
         bool first = true;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
-          const uint32_t b = u & 1;
-          ptx::mbar_wait(&cm_full[b], (u >> 1) & 1);
+          const bool direct = args.win_direct != 0;
+          const uint32_t b = direct ? u & 3 : u & 1;
+          t0 = clock64();
+          if (direct) {
+            ptx::mbar_wait(&slot_full[b], (u >> 2) & 1);
+          } else {
+            ptx::mbar_wait(&cm_full[b], (u >> 1) & 1);
+          }
+          t_box += clock64() - t0;
           ptx::tc_fence_after();
-          const uint32_t cm = ptx::smem_u32(smem + L.win_off + (2 + b) * win_stride);
+          const uint32_t cm =
+              ptx::smem_u32(smem + L.win_off + (direct ? b : 2 + b) * win_stride);
           const int ksteps = min(8, (args.C - kb * 64) / 8) / 2;
+          int tap_r = 0, tap_c = 0;
           for (int t = 0; t < win_taps; ++t) {
             uint32_t s = 0;
             if (!b_res) {
@@ -1065,30 +1087,49 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               ptx::mbar_wait(&full[s], rp.lap & 1);
               ptx::tc_fence_after();
             }
-            const int dr = t / args.S, dc = t - (t / args.S) * args.S;
+            const int dr = tap_r, dc = tap_c;  // (tap t = dr * S + dc, advanced below)
+            if (++tap_c == args.S) {
+              tap_c = 0;
+              ++tap_r;
+            }
             const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(
                 smem + L.b_off + (b_res ? kb * win_taps + t : static_cast<int>(s)) * b_bytes));
             for (int q = 0; q < mt; ++q) {  // sub-tile q: pixel rows 16q .. 16q+15 of the block
-              const uint64_t da = ptx::umma_desc_none_kmajor(
-                  cm + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 16, lbo, sbo);
-              for (int k = 0; k < ksteps; ++k)  // next K=16 step: two chunk planes further
-                ptx::umma_bf16(d + q * args.BN, da + static_cast<uint64_t>(2 * k) * (lbo >> 4),
-                               db + 2 * k, idesc, first && k == 0 ? 0u : 1u);
+              const uint32_t pix = static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc);
+              if (direct) {  // 128 B-swizzled pixel rows; K=16 steps are +32 B in the row
+                const uint64_t da = ptx::umma_desc_sw128_kmajor_sbo(
+                    cm + pix * 128, static_cast<uint32_t>(args.win_iw) * 128);
+                if (ksteps == 4) {
+                  ptx::umma_bf16_warp_k64(d + q * args.BN, da, db, idesc, first ? 0u : 1u);
+                } else {
+                  for (int k = 0; k < ksteps; ++k)
+                    ptx::umma_bf16_warp(d + q * args.BN, da + 2 * k, db + 2 * k, idesc,
+                                        first && k == 0 ? 0u : 1u);
+                }
+              } else {
+                const uint64_t da = ptx::umma_desc_none_kmajor(cm + pix * 16, lbo, sbo);
+                for (int k = 0; k < ksteps; ++k)  // next K=16 step: two chunk planes further
+                  ptx::umma_bf16_warp(d + q * args.BN, da + static_cast<uint64_t>(2 * k) * (lbo >> 4),
+                                 db + 2 * k, idesc, first && k == 0 ? 0u : 1u);
+              }
             }
             first = false;
             if (!b_res) {
-              ptx::umma_commit(&empty[s]);
+              ptx::umma_commit_warp(&empty[s]);
               rp.next(args.stages);
             }
           }
-          ptx::umma_commit(&cm_empty[b]);
+          ptx::umma_commit_warp(direct ? &slot_free[b] : &cm_empty[b]);
         }
-        ptx::umma_commit(&tmem_full[acc]);
+        ptx::umma_commit_warp(&tmem_full[acc]);
       }
+      if ((args.debug_flags & 32) && blockIdx.x < 2 && lane == 0)
+        printf("kWindow MMA cta %d: tiles %u, cycles %llu, waiting box %llu, waiting acc %llu\n",
+               blockIdx.x, j, clock64() - t_all, t_box, t_acc);
     }
     __syncwarp();
-  } else {  // kMmaWarp: MMA issuer
-    if (lane == 0) {
+  } else {  // kMmaWarp: MMA issuer (whole warp: uniform descriptors, elected issue)
+    {
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
       if (args.b_res > 0) ptx::mbar_wait(b_full, 0);
@@ -1117,18 +1158,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int q = 0; q < mt && !(args.debug_flags & 16); ++q) {  // (flag 16: bring-up)
             const uint64_t da = ptx::umma_desc_sw128_kmajor(
                 ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes));
-#pragma unroll
-            for (int k = 0; k < kConvBK / 16; ++k) {
-              // +32 B along K inside the swizzle row = +2 in the >>4 start field.
-              ptx::umma_bf16(d + q * args.BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-            }
+            // the K block's four K=16 steps (+32 B in the swizzle row each)
+            ptx::umma_bf16_warp_k64(d + q * args.BN, da, db, idesc, kb != 0);
           }
           if (cl > 1)
-            ptx::umma_commit_mc(&empty[s], cl_mask);  // both CTAs read this B slot
+            ptx::umma_commit_mc_warp(&empty[s], cl_mask);  // both CTAs read this B slot
           else
-            ptx::umma_commit(&empty[s]);
+            ptx::umma_commit_warp(&empty[s]);
         }
-        ptx::umma_commit(&tmem_full[acc]);
+        ptx::umma_commit_warp(&tmem_full[acc]);
       }
     }
     __syncwarp();
@@ -1228,7 +1266,7 @@ bool encode_tmap_out4d(CUtensorMap* map, void* base, int n, int h, int w, int co
 }
 
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
-                      int box_w, int box_h, int box_n) {
+                      int box_w, int box_h, int box_n, bool sw128) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn || (static_cast<uint64_t>(c) * 2) % 16 != 0) return false;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
@@ -1240,7 +1278,8 @@ bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, i
                              static_cast<cuuint32_t>(box_h), static_cast<cuuint32_t>(box_n)};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

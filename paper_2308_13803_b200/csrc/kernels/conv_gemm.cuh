@@ -71,6 +71,8 @@ struct ConvGemmArgs {
   // at pixel offset r*win_iw + s (K-major, no swizzle).
   int win_iw, win_ih;
   uint32_t win_box_bytes;
+  int win_direct;  // 1: C % 64 == 0, the 128 B-swizzled pixel-major box is read in place
+                   // (4 box slots, no transpose); 0: transposed to chunk-major
   // kStemU8: A gathered straight from the u8 images [n][H][W][3]; the
   // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
   // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
@@ -107,7 +109,7 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
 // box_h, 1} box, no swizzle (used by the depthwise halo loads). Negative or
 // past-the-edge box coordinates read zeros (the convolution's padding).
 bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int c, int box_c,
-                      int box_w, int box_h, int box_n = 1);
+                      int box_w, int box_h, int box_n = 1, bool sw128 = false);
 
 size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps = 8, int b_res_blocks = 0,
                             int mt = 1);

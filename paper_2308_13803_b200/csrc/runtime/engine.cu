@@ -321,8 +321,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.win_ih = 16 + op.r - 1;
       const int cb = in.c < 64 ? in.c : 64;
       a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * cb * 2);
+      a.win_direct = in.c % 64 == 0 ? 1 : 0;  // 128 B pixel rows: windows read in place
       if (!encode_tmap_nhwc(&a.tmap_a, bufs_[op.in], max_bs, in.h, in.w, in.c, cb, a.win_iw,
-                            a.win_ih, 1))
+                            a.win_ih, 1, a.win_direct != 0))
         throw CudaError("cuTensorMapEncodeTiled failed (window halo boxes)");
     } else if (op.r == 1 && op.s == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 && op.pw == 0) {
       // A is a plain [pixels][C] matrix; for C < 64 the TMA box runs past
