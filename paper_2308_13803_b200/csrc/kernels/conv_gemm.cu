@@ -274,10 +274,37 @@ __device__ __forceinline__ uint4 relu_pack8(const float (&v)[8]) {
                     pack2_bf16(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
 }
 
+// A producer thread's depthwise items (fixed for every tile and K block: the
+// tile shape is fixed): two horizontally adjacent outputs x one 8-channel group
+// each, as the uint4 offset of the items' top-left input in the box and the
+// A row of the first output.
+struct DwItems {
+  int n;
+  int box_off[2];
+  int row_a[2];
+};
+
+__device__ __forceinline__ DwItems dw_items(const ConvGemmArgs& a, int tid, int S) {
+  DwItems d{0, {0, 0}, {0, 0}};
+  const int groups = a.dw_cb >> 3;
+  const int g = tid & (groups - 1);
+  const int half_tw = a.dw_tw >> 1;
+  const int items = a.dw_th * half_tw * groups;
+  for (int it = tid; it < items && d.n < 2; it += kGatherWarps * 32, ++d.n) {
+    const int strip = it / groups;
+    const int ty = strip / half_tw;
+    const int tx = (strip - ty * half_tw) * 2;
+    d.box_off[d.n] = (ty * S * a.dw_iw + tx * S) * groups + g;
+    // A row of pixel (ty, tx): warp ty / rw, lane (ty % rw) * tw + tx
+    d.row_a[d.n] = (ty / a.dw_rw) * 32 + (ty % a.dw_rw) * a.dw_tw + tx;
+  }
+  return d;
+}
+
 // One K block of one tile: box (smem, [IH][IW][groups] uint4) -> A stage.
 template <int S>
 __device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* box, uint32_t a_stage,
-                                            int kb, int tid) {
+                                            int kb, int tid, const DwItems& di) {
   constexpr int XN = S + 3;  // input columns of two adjacent outputs
   const int groups = a.dw_cb >> 3;
   const int g = tid & (groups - 1);  // fixed per thread (groups divides the thread count)
@@ -288,12 +315,9 @@ __device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* 
   for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(a.dw_w) + k * cg_all + gg);
   const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg);
   const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg + 1);
-  const int half_tw = a.dw_tw >> 1;
-  const int items = a.dw_th * half_tw * groups;
-  for (int it = tid; it < items; it += kGatherWarps * 32) {
-    const int strip = it / groups;
-    const int ty = strip / half_tw;
-    const int tx = (strip - ty * half_tw) * 2;
+  const int row_stride = a.dw_iw * groups;  // uint4 per box row
+#pragma unroll 2
+  for (int i = 0; i < di.n; ++i) {
     float acc[2][8];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -302,7 +326,7 @@ __device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* 
     }
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      const uint4* row = box + ((ty * S + r) * a.dw_iw + tx * S) * groups + g;
+      const uint4* row = box + di.box_off[i] + r * row_stride;
       uint4 xv[XN];
 #pragma unroll
       for (int u = 0; u < XN; ++u) xv[u] = row[u * groups];
@@ -311,11 +335,9 @@ __device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* 
 #pragma unroll
         for (int c = 0; c < 3; ++c) dw_fma8(acc[q], xv[q * S + c], w[r * 3 + c]);
     }
-    // A row of pixel (ty, tx): warp ty / rw, lane (ty % rw) * tw + tx
-    const int row_base = (ty / a.dw_rw) * 32 + (ty % a.dw_rw) * a.dw_tw + tx;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int row_a = row_base + q;
+      const int row_a = di.row_a[i] + q;
       const uint32_t rowp = a_stage + row_a * 128;
       ptx::sts128(rowp + ((g ^ (row_a & 7)) << 4), relu_pack8(acc[q]));
       if (groups == 4)  // 32-channel layer: the K block's upper half is zero
@@ -814,6 +836,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     } else if constexpr (kDw) {
       const int tid = threadIdx.x - kGatherWarp0 * 32;
+      const DwItems di = dw_items(args, tid, args.dw_stride);
       RingPos rp;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
@@ -823,9 +846,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint4* box = reinterpret_cast<const uint4*>(smem + L.box_off + s * box_stride);
           const uint32_t a_st = ptx::smem_u32(smem + L.a_off) + s * a_stage;
           if (args.dw_stride == 1)
-            dw_box_to_a<1>(args, box, a_st, kb, tid);
+            dw_box_to_a<1>(args, box, a_st, kb, tid, di);
           else
-            dw_box_to_a<2>(args, box, a_st, kb, tid);
+            dw_box_to_a<2>(args, box, a_st, kb, tid, di);
           ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core reads
           ptx::mbar_arrive(&full[s]);
         }

@@ -1,5 +1,3 @@
-mkdir -p gpurun_out/dbg15
-for f in 0 1 16 17; do
-  DS_CONV_DEBUG=3:$f timeout 300 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:128 --steps 3 --warmup 3 --max-converge 1 > gpurun_out/dbg15/g$f.json 2>/dev/null
-  DS_CONV_WINDOW=1 DS_CONV_DEBUG=3:$f timeout 300 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:128 --steps 3 --warmup 3 --max-converge 1 > gpurun_out/dbg15/w$f.json 2>/dev/null
-done
+mkdir -p gpurun_out/fu3
+DS_DW_FUSION=1 timeout 300 python bench.py --no-cpu-baseline --kernel-table --knob batching:128 --steps 3 --warmup 3 --max-converge 1 > gpurun_out/fu3/f.json 2>gpurun_out/fu3/f.err
+DS_DW_FUSION=1 timeout 300 python -m pytest tests -m gpu -q -k "depthwise_fusion" --timeout=150 --timeout-method=thread > gpurun_out/fu3/pt.txt 2>&1
