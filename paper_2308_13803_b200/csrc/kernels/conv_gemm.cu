@@ -616,8 +616,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t a_stage = static_cast<uint32_t>(mt) * kABytes;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
-  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x)
-    bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
   if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + args.stages;
@@ -701,6 +699,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31);
     // team w/4 takes every teams-th tile of this CTA, all its column groups,
     // so up to `teams` tiles drain concurrently.
+    // The epilogue warps stage the bias themselves (named barrier 1), off the
+    // critical path of the first tile's loads and MMAs.
+    for (int i = threadIdx.x; i < cout_pad; i += epi_warps * 32)
+      bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
+    asm volatile("bar.sync 1, %0;" ::"r"(epi_warps * 32) : "memory");
     const int quarter = warp & 3;
     const int team = warp >> 2;
     uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;

@@ -252,23 +252,32 @@ __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ 
   y[opix * ldo_g + coff_g + g] = pack8(acc);
 }
 
+// Global average pool: four threads (adjacent lanes) per (image, 8-channel
+// group), each summing every 4th pixel with all its loads in flight; the four
+// partial sums combine in a fixed order (p0+p1)+(p2+p3), so results are
+// deterministic (and within fp32 rounding of the oracle's sequential sum).
+constexpr int kGapParts = 4;
+
 __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int hw,
                                       int cg, long long work) {
   pdl_trigger();
   pdl_wait();
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= work) return;
-  const int g = static_cast<int>(i % cg);
-  const long long n = i / cg;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long i = t / kGapParts;
+  const int part = static_cast<int>(t % kGapParts);
+  const bool live = i < work;
+  const int g = live ? static_cast<int>(i % cg) : 0;
+  const long long n = live ? i / cg : 0;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint4* p = x + n * hw * cg + g;
-  // pixels in order (the oracle's summation order), loads issued 8 ahead
-  constexpr int U = 8;
-  int q = 0;
-  for (; q + U <= hw; q += U) {
+  constexpr int U = 13;  // 49 / 4 pixels per part in one batch of loads
+  for (int q0 = part; live && q0 < hw; q0 += U * kGapParts) {
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldg(p + static_cast<long long>(q + u) * cg);
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * kGapParts;
+      v[u] = q < hw ? __ldg(p + static_cast<long long>(q) * cg) : make_uint4(0u, 0u, 0u, 0u);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float xv[8];
@@ -277,12 +286,12 @@ __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __rest
       for (int e = 0; e < 8; ++e) acc[e] += xv[e];
     }
   }
-  for (; q < hw; ++q) {
-    float xv[8];
-    unpack8(__ldg(p + static_cast<long long>(q) * cg), xv);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] += xv[e];
+  for (int e = 0; e < 8; ++e) {
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);  // (p0+p1), (p2+p3)
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);  // (p0+p1)+(p2+p3)
   }
+  if (!live || part != 0) return;
   const float inv = static_cast<float>(hw);
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = acc[e] / inv;
@@ -398,7 +407,7 @@ cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int 
                                   cudaStream_t stream) {
   const int cg = c / 8;
   const long long work = static_cast<long long>(n) * cg;
-  return launch_pdl(global_avgpool_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
+  return launch_pdl(global_avgpool_kernel, dim3(grid_for(work * kGapParts)), dim3(kBlock), 0, stream,
                     reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, work);
   return cudaGetLastError();
 }
