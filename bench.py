@@ -249,8 +249,8 @@ def run_ours(args, rank, world, local, dist):
     be = GpuBackend(model, Config(max_bs, max_mtl), seed=42 + rank, device=local)
     l1, catalog = build_catalog(be, model, m, n)
     slo = SLO_FACTOR[model] * l1
-    sc = C.Scenario(controller="dnnscaler", seed=42, alpha=0.85, m=m, n=n, abs_max_bs=max_bs,
-                    max_mtl=max_mtl, window=window)
+    sc = C.Scenario(controller=args.controller, seed=42, alpha=0.85, m=m, n=n,
+                    abs_max_bs=max_bs, max_mtl=max_mtl, window=window)
     if args.knob:  # static knob (profiling runs): skips the Profiler/Scaler search
         kind, value = args.knob.split(":")
         sc.controller = "static"
@@ -327,7 +327,8 @@ def run_ours(args, rank, world, local, dist):
         "dtype": "bf16",
         "data": "synthetic (seeded u8 images, seeded He-init weights with folded BN; DESIGN.md)",
         "config": {
-            "workload": f"{model} {info.in_h}x{info.in_w}, DNNScaler Profiler+Scaler, "
+            "workload": f"{model} {info.in_h}x{info.in_w}, "
+                        f"{'DNNScaler Profiler+Scaler' if args.controller == 'dnnscaler' else 'Clipper AIMD'}, "
                         f"SLO = {SLO_FACTOR[model]} x L(BS=1)",
             "model": model,
             "global_batch": knob[1] if knob[0] == 0 else knob[1] * world,
@@ -336,11 +337,14 @@ def run_ours(args, rank, world, local, dist):
             "l1_ms": round(l1, 4),
             "p95_ms_timed": round(nearest_rank_p95(timed_lat), 4),
             "p95_within_slo": bool(nearest_rank_p95(timed_lat) <= slo),
-            "profiler": {"ti_batching": round(rep["ti_batching"], 2), "ti_mt": round(rep["ti_mt"], 2),
+            "profiler": {"ti_batching": round(rep.get("ti_batching", 0.0), 2),
+                         "ti_mt": round(rep.get("ti_mt", 0.0), 2),
                          "approach": res.summary["approach_kind"] and "multi-tenancy" or "batching",
-                         "tput_base": round(rep["tput_base"], 1),
-                         "tput_batching": round(rep["tput_batching"], 1),
-                         "tput_mt": round(rep["tput_mt"], 1)},
+                         "tput_base": round(rep.get("tput_base", 0.0), 1),
+                         "tput_batching": round(rep.get("tput_batching", 0.0), 1),
+                         "tput_mt": round(rep.get("tput_mt", 0.0), 1)}
+            if args.controller == "dnnscaler" else None,
+            "controller": args.controller,
             "knob_trajectory": [list(k) for k in knobs],
             "scenario": {"m": m, "n": n, "abs_max_bs": max_bs, "max_mtl": max_mtl,
                          "window": window, "alpha": 0.85},
@@ -388,6 +392,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-table", action="store_true")
     ap.add_argument("--knob", default="", help="static knob, e.g. batching:128 (profiling only)")
+    ap.add_argument("--controller", default="dnnscaler", choices=["dnnscaler", "clipper"],
+                    help="clipper: the paper's baseline controller on the same backend "
+                         "(Table 5 comparison; the headline is dnnscaler)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

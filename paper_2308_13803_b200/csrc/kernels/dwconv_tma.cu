@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "conv_gemm.cuh"
 #include "pdl.cuh"
@@ -237,6 +238,15 @@ int sm_count() {
   return n;
 }
 
+// (bring-up knob: DS_DW14_ROWS overrides the 14x14 tile height)
+int dw14_rows() {
+  static const int r = [] {
+    const char* e = std::getenv("DS_DW14_ROWS");
+    return e ? std::max(1, std::atoi(e)) : 14;
+  }();
+  return r;
+}
+
 // Tile shape per layer (output width, stride, channels): a strip of Q outputs
 // per thread, TW | wo, and (TW/Q)*TH*NB*groups close to a multiple of 32 <= 256.
 struct DwPlan {
@@ -255,7 +265,7 @@ DwPlan dw_plan(int ho, int wo, int c, int stride) {
     if (wo % 16 == 0 && wo >= 64) set(4, 16, cb >= 64 ? 8 : 16, 1);  // 112x112
     else if (wo % 8 == 0 && wo >= 48) set(4, 8, 14, 1);              // 56x56
     else if (wo % 4 == 0 && wo >= 20) set(4, wo, 4, 1);              // 28x28
-    else if (wo % 7 == 0 && wo >= 14) set(7, wo, std::min(ho, 14), 1);  // 14x14
+    else if (wo % 7 == 0 && wo >= 14) set(7, wo, std::min(ho, dw14_rows()), 1);  // 14x14
     else if (wo == 7) set(7, 7, 7, 4);                                // 7x7
   } else {
     if (wo % 8 == 0 && wo >= 48) set(2, 8, 8, 1);                     // 112 -> 56

@@ -98,16 +98,21 @@ def _device_catalog(be, model, m, n):
     return l1, [row] + C.load_catalog(DONORS)
 
 
-@pytest.mark.parametrize("model,m,n,max_bs,max_mtl,c,steps", [
-    ("synthetic_cnn", 32, 4, 32, 4, 4.15, []),
-    ("mobilenet_v1", 32, 8, 128, 10, 13.44, []),
-    ("mobilenet_v1", 32, 8, 128, 10, 13.44, [(0.4, 0.5)]),  # SLO step-down mid-job
+@pytest.mark.parametrize("model,m,n,max_bs,max_mtl,c,steps,controller", [
+    ("synthetic_cnn", 32, 4, 32, 4, 4.15, [], "dnnscaler"),
+    ("mobilenet_v1", 32, 8, 128, 10, 13.44, [], "dnnscaler"),
+    ("mobilenet_v1", 32, 8, 128, 10, 13.44, [(0.4, 0.5)], "dnnscaler"),  # SLO step-down
+    # the Clipper baseline (clipper.cpp:17-35, AIMD on the
+    # batch size) driving the same B200 backend, replayed through the reference
+    ("mobilenet_v1", 32, 8, 128, 10, 13.44, [], "clipper"),
 ])
-def test_device_job_replays_bit_exact(model, m, n, max_bs, max_mtl, c, steps, tmp_path):
+def test_device_job_replays_bit_exact(model, m, n, max_bs, max_mtl, c, steps, controller,
+                                      tmp_path):
     with GpuBackend(model, Config(max_bs, max_mtl)) as be:
         l1, catalog = _device_catalog(be, model, m, n)
         slo = c * l1
-        sc = C.Scenario(m=m, n=n, abs_max_bs=max_bs, max_mtl=max_mtl, window=100)
+        sc = C.Scenario(controller=controller, m=m, n=n, abs_max_bs=max_bs, max_mtl=max_mtl,
+                        window=100)
         sched = [(t, slo * f) for t, f in steps]
         job = C.JobSpec(7, model, slo, 0.8, slo_schedule=sched)
         dev = C.run_job(sc, job, catalog, "device", backend=be)
@@ -131,6 +136,8 @@ def test_device_job_replays_bit_exact(model, m, n, max_bs, max_mtl, c, steps, tm
         assert float(dev.summary[k]) == theirs["summary"][k], k
     assert dev.summary["steady_knob"] == (int(theirs["summary"]["steady_kind"]),
                                           int(theirs["summary"]["steady_value"]))
+    if controller != "dnnscaler":
+        return  # (no Profiler probe in Clipper's tape)
     # and the reference's profile() on the probe prefix of the tape
     rep, appr = refo.profile_tape(dev.tape, m, n, 10, max_bs, max_mtl)
     for k, v in rep.items():

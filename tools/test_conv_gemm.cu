@@ -138,6 +138,7 @@ static int run(const Case& cs) {
 
 int main(int argc, char** argv) {
   const Case cases[] = {
+      {"tiny 1x1 (fixed cost)", 1, 8, 16, 64, 1, 1, 1, 1, 0, 0, 64, 64, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"1x1 s1 tmaA", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"1x1 s1 gather", 2, 14, 14, 256, 1, 1, 1, 1, 0, 0, 512, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"3x3 s1 p1", 1, 28, 28, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
