@@ -134,6 +134,29 @@ class ClockSampler:
                 "power_w_median": float(np.median(power)) if power else None}
 
 
+class EnergyMeter:
+    """NVML board energy counter across the timed region (SURVEY §8(f) row 1:
+    measured power for the paper's throughput-per-watt comparison, Table 5)."""
+
+    def __init__(self, device):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        except Exception:  # noqa: BLE001 - no NVML: report null
+            self.h = None
+
+    def read_mj(self):
+        if self.h is None:
+            return None
+        try:
+            return self.nvml.nvmlDeviceGetTotalEnergyConsumption(self.h)  # millijoules
+        except Exception:  # noqa: BLE001
+            return None
+
+
 def nearest_rank_p95(x):
     x = np.sort(np.asarray(x))
     rank = int(np.ceil(0.95 * len(x) - 1e-9))
@@ -287,9 +310,18 @@ def run_ours(args, rank, world, local, dist):
         return items, ms, recs, st0, st1
 
     sampler = ClockSampler(local)
+    meter = EnergyMeter(local)
     sampler.start()
+    e_start = meter.read_mj()
     items, ms, recs, st0, st1 = timed(args.steps, "timed")
+    e_end = meter.read_mj()
     clocks = sampler.stop()
+    energy = None
+    if e_start is not None and e_end is not None and e_end > e_start:
+        joules = (e_end - e_start) / 1000.0
+        energy = {"joules": round(joules, 3), "avg_power_w": round(joules / (ms * 1e-3), 1),
+                  "inferences_per_joule": round(items / joules, 1),
+                  "source": "NVML total energy counter over the timed periods (board power)"}
     # e2e through host buffers, same session (the Scaler keeps control)
     be.set_host_io(True)
     e_warm = max(1, args.warmup // 2)
@@ -361,6 +393,7 @@ def run_ours(args, rank, world, local, dist):
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
         "roofline": rl,
         "clocks": clocks,
+        "energy": energy,
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(model, args.cpu_seconds)

@@ -81,6 +81,13 @@ ds_config ds_get_config(const ds_backend* b);
 ds_status ds_run_batches(ds_backend* b, int bs, int count, double* latencies_ms);
 ds_status ds_run_mt_requests(ds_backend* b, int count, double* latencies_ms);
 
+/* B x MT combination (the device counterpart of the reference's analytic
+ * combination_sweep cell, harness.cpp:356-386): `mtl` full-size instances on
+ * their own streams, each serving batches of `bs` concurrently; `count`
+ * completed-batch latencies, round robin over the instances; clock advances
+ * by latency / mtl. Device-resident inputs only. */
+ds_status ds_run_combo_requests(ds_backend* b, int bs, int mtl, int count, double* latencies_ms);
+
 /* Parity path: u8 NHWC images [bs][h][w][3] (host memory) through the full
  * network; fp32 logits [bs][classes] and softmax probs (either may be NULL). */
 ds_status ds_forward(ds_backend* b, const uint8_t* images, int bs, float* logits, float* probs);

@@ -76,6 +76,7 @@ SIGNATURES = {
     "ds_get_config": (DsConfig, [_vp]),
     "ds_run_batches": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp]),
     "ds_run_mt_requests": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    "ds_run_combo_requests": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]),
     "ds_forward": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
     "ds_set_host_io": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ds_drain": (ctypes.c_int, [_vp]),

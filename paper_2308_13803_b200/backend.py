@@ -123,6 +123,37 @@ class GpuBackend:
         _lib.check(self._lib.ds_run_mt_requests(self._h, count, out.ctypes.data))
         return out
 
+    def run_combo_requests(self, bs: int, mtl: int, count: int) -> np.ndarray:
+        """B x MT: mtl instances each serving bs-batches concurrently."""
+        out = np.empty(count, dtype=np.float64)
+        _lib.check(self._lib.ds_run_combo_requests(self._h, bs, mtl, count, out.ctypes.data))
+        return out
+
+    def combination_sweep(self, bs_list, mtl_list, samples_per_cell: int = 50) -> list:
+        """Device counterpart of the reference combination_sweep
+        (harness.cpp:356-386): per (bs, mtl) cell the mean and nearest-rank p95
+        of the per-instance batch latency and throughput = bs * mtl * 1000 /
+        mean (the reference's formula), plus the throughput measured on the
+        device clock over the cell."""
+        from . import control as C
+        if not bs_list or not mtl_list:
+            raise ValueError("empty sweep grid")
+        if samples_per_cell < 1:
+            raise ValueError("samples_per_cell must be positive")
+        cells = []
+        for bs in bs_list:
+            for mtl in mtl_list:
+                self.run_combo_requests(bs, mtl, 2 * mtl)  # warm-up (instances, graphs)
+                self.timer_start()
+                lat = self.run_combo_requests(bs, mtl, samples_per_cell)
+                ms = self.timer_stop()
+                mean = float(lat.mean())
+                cells.append({"bs": bs, "mtl": mtl, "mean_ms": mean,
+                              "p95_ms": C.percentile(lat, 0.95),
+                              "throughput": bs * mtl * 1000.0 / mean,
+                              "measured_throughput": bs * samples_per_cell * 1000.0 / ms})
+        return cells
+
     def forward(self, images: np.ndarray, probs: bool = False):
         images = np.ascontiguousarray(images, dtype=np.uint8)
         bs = images.shape[0]

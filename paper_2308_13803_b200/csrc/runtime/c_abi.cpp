@@ -131,6 +131,15 @@ ds_status ds_run_mt_requests(ds_backend* b, int count, double* latencies_ms) {
   return guard([&] { b->impl->run_mt_requests(count, latencies_ms); });
 }
 
+ds_status ds_run_combo_requests(ds_backend* b, int bs, int mtl, int count, double* latencies_ms) {
+  if (!b) return null_handle();
+  if (count < 0 || (count > 0 && !latencies_ms)) {
+    g_last_error = "invalid window";
+    return DS_EINVAL;
+  }
+  return guard([&] { b->impl->run_combo_requests(bs, mtl, count, latencies_ms); });
+}
+
 ds_status ds_forward(ds_backend* b, const uint8_t* images, int bs, float* logits, float* probs) {
   if (!b) return null_handle();
   if (!images) {

@@ -532,11 +532,14 @@ Backend::Backend(const std::string& model_id, BackendConfig cfg, uint64_t seed, 
   const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
   host_images_.resize(img_bytes * pool_images_);
   generate_images(model_.in_h, model_.in_w, seed_, 0, pool_images_, host_images_.data());
-  inst_.resize(cfg_.max_mtl);
-  inflight_.resize(cfg_.max_mtl);
-  io_cursor_.assign(cfg_.max_mtl, 0);
-  io_seq_.assign(cfg_.max_mtl, 0);
-  pinned_logits_.assign(cfg_.max_mtl, nullptr);
+  // instances [0, max_mtl): the batching instance and the MT (bs = 1)
+  // instances; [max_mtl, 2 max_mtl - 1): full-size instances 1.. of the
+  // B x MT combination (combo instance 0 is the batching instance)
+  inst_.resize(2 * cfg_.max_mtl);
+  inflight_.resize(2 * cfg_.max_mtl);
+  io_cursor_.assign(2 * cfg_.max_mtl, 0);
+  io_seq_.assign(2 * cfg_.max_mtl, 0);
+  pinned_logits_.assign(2 * cfg_.max_mtl, nullptr);
   instance(0);
 }
 
@@ -557,10 +560,11 @@ Backend::~Backend() {
 
 Instance& Backend::instance(int i) {
   if (!inst_.at(i)) {
-    const int max_bs = (i == 0) ? cfg_.abs_max_bs : 1;
+    const bool full = i == 0 || i >= cfg_.max_mtl;
+    const int max_bs = full ? cfg_.abs_max_bs : 1;
     inst_[i] = std::make_unique<Instance>(model_, max_bs, device_);
     const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
-    const int first = (i == 0) ? 0 : (i % pool_images_);
+    const int first = full ? 0 : (i % pool_images_);
     check_cuda(cudaMemcpy(inst_[i]->images(), host_images_.data() + img_bytes * first,
                           img_bytes * max_bs, cudaMemcpyHostToDevice),
                "upload images");
@@ -662,6 +666,32 @@ void Backend::run_batches(int bs, int count, double* lat_out) {
     clock_ms_ += lat;  // reference gpu_sim.cpp:16
     lat_out[j] = lat;
   }
+}
+
+void Backend::run_combo_requests(int bs, int mtl, int count, double* lat_out) {
+  // B x MT combination (reference combination_sweep, harness.cpp:356-386, on
+  // the analytic model): mtl full-size instances, each on its own stream,
+  // each keeping kDepth batches of bs in flight; latencies of completed
+  // batches round robin over the instances; clock += latency / mtl as for MT.
+  if (bs < 1 || bs > cfg_.abs_max_bs) throw std::invalid_argument("invalid batch size");
+  if (mtl < 1 || mtl > cfg_.max_mtl) throw std::invalid_argument("invalid instance count");
+  if (host_io_) throw std::invalid_argument("combination requests run device-resident");
+  drain();
+  auto idx = [&](int k) { return k == 0 ? 0 : cfg_.max_mtl + k - 1; };
+  for (int k = 0; k < mtl; ++k) instance(idx(k));  // (created outside the timed calls)
+  // exactly `count` batches are issued (request j on instance j % mtl), so
+  // every batch run between the drains is one of the returned latencies
+  int issued = 0;
+  for (int j = 0; j < count; ++j) {
+    while (issued < count && static_cast<int>(inflight_[idx(issued % mtl)].size()) < kDepth) {
+      enqueue_request(idx(issued % mtl), bs);
+      ++issued;
+    }
+    const double lat = complete_oldest(idx(j % mtl));
+    clock_ms_ += lat / static_cast<double>(mtl);
+    lat_out[j] = lat;
+  }
+  drain();
 }
 
 void Backend::run_mt_requests(int count, double* lat_out) {

@@ -124,6 +124,9 @@ class Backend {
   // One control window: `count` consecutive seam calls at a fixed knob.
   void run_batches(int bs, int count, double* lat_out);
   void run_mt_requests(int count, double* lat_out);
+  // B x MT combination: mtl full-size instances each serving bs-batches
+  // concurrently (reference combination_sweep).
+  void run_combo_requests(int bs, int mtl, int count, double* lat_out);
   // Parity path: host u8 NHWC images in, fp32 logits (and probs) out.
   void forward(const uint8_t* host_images, int bs, float* host_logits, float* host_probs);
   // End-to-end mode: every request copies its images from a pinned host pool

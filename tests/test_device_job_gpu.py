@@ -143,3 +143,30 @@ def test_device_job_replays_bit_exact(model, m, n, max_bs, max_mtl, c, steps, co
     for k, v in rep.items():
         assert float(dev.report[k]) == v, k
     assert appr == dev.summary["approach_kind"]
+
+
+def test_combination_sweep_on_device():
+    """the B x MT combination on the device (several
+    full-size instances, each serving batches concurrently), reported per
+    cell like the reference's combination_sweep (harness.cpp:356-386): mean,
+    nearest-rank p95, throughput = bs * mtl * 1000 / mean."""
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=32, max_mtl=3)) as be:
+        c0 = be.clock_ms()
+        lat = be.run_combo_requests(8, 2, 6)
+        assert lat.shape == (6,) and (lat > 0).all()
+        assert be.clock_ms() == pytest.approx(c0 + lat.sum() / 2, rel=1e-12)
+        with pytest.raises(ValueError, match="invalid instance count"):
+            be.run_combo_requests(8, 4, 1)
+        with pytest.raises(ValueError, match="invalid batch size"):
+            be.run_combo_requests(33, 1, 1)
+        cells = be.combination_sweep([8, 32], [1, 2], samples_per_cell=20)
+        # the batching path is unaffected afterwards
+        assert be.run_batch(32) > 0
+    assert [(c["bs"], c["mtl"]) for c in cells] == [(8, 1), (8, 2), (32, 1), (32, 2)]
+    for c in cells:
+        assert c["p95_ms"] >= c["mean_ms"] * 0.5 and c["throughput"] > 0
+        assert c["throughput"] == pytest.approx(c["bs"] * c["mtl"] * 1000.0 / c["mean_ms"])
+        assert c["measured_throughput"] > 0
+    by = {(c["bs"], c["mtl"]): c for c in cells}
+    # two concurrent instances deliver more than one (or at worst about the same)
+    assert by[(8, 2)]["measured_throughput"] > 0.8 * by[(8, 1)]["measured_throughput"]
