@@ -1105,6 +1105,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t cm =
               ptx::smem_u32(smem + L.win_off + (direct ? b : 2 + b) * win_stride);
           const int ksteps = min(8, (args.C - kb * 64) / 8) / 2;
+          if (direct && ksteps == 4 && mt == 1 && args.R == 3 && args.S == 3) {
+            // 3x3: the nine taps fully unrolled, every A descriptor a
+            // compile-time offset from the K block's box (uniform issue)
+            const uint64_t da0 = ptx::umma_desc_sw128_kmajor_sbo(cm, 10 * 128);  // IW = 10
+            const uint32_t b_base = ptx::smem_u32(smem + L.b_off);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+              uint32_t s = 0;
+              if (!b_res) {  // weights stream through the ring, one tap per slot
+                s = rp.slot;
+                ptx::mbar_wait(&full[s], rp.lap & 1);
+                ptx::tc_fence_after();
+              }
+              const uint64_t db = ptx::umma_desc_sw128_kmajor(
+                  b_base + (b_res ? static_cast<uint32_t>(kb * 9 + t) : s) * b_bytes);
+              ptx::umma_bf16_warp_k64(d, da0 + static_cast<uint64_t>(((t / 3) * 10 + t % 3) * 8),
+                                      db, idesc, first && t == 0 ? 0u : 1u);
+              if (!b_res) {
+                ptx::umma_commit_warp(&empty[s]);
+                rp.next(args.stages);
+              }
+            }
+            first = false;
+            ptx::umma_commit_warp(&slot_free[b]);
+            continue;
+          }
           int tap_r = 0, tap_c = 0;
           for (int t = 0; t < win_taps; ++t) {
             uint32_t s = 0;

@@ -36,10 +36,6 @@ int choose_stages(int bn, int cout) { return conv_gemm_stages(bn, cout); }
 
 uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 
-// DS_CONV_WINDOW=1: stride-1 R x S convs as kWindow (shifted-window MMAs).
-// Opt-in: parity-tested, but its fixed 16 x 8 pixel tiles waste a third of
-// the MMA rows on 28/14/7-wide layers and the 2-deep box rings expose the
-// halo load, so the im2col gather is still faster on B200.
 // DS_STEM_S2D_MODE=window: the s2d stem as a kWindow conv (one halo box per
 // 32 x 8 block, transposed by the gather warps) instead of kS2D (one TMA box
 // per tap in the MMA's layout, no producer warps; faster on B200). A/B switch.
@@ -75,12 +71,23 @@ bool s2d_tap_boxes() {
   return on;
 }
 
-bool window_on() {
-  static const bool on = [] {
+// Stride-1 R x S convs as kWindow (shifted-window MMAs, no im2col). Default:
+// only where the halo box is read in place (C % 64 == 0) and the map is at
+// least 28 x 28 (the 16 x 8 pixel tiles waste few MMA rows there): ResNet's
+// 56^2 3x3s run in half the gather's time; on 14^2 / 7^2 maps and with the
+// transposed (C % 64 != 0) boxes the im2col gather is still faster.
+// DS_CONV_WINDOW=1: every eligible conv; DS_CONV_WINDOW=0: none (A/B).
+int window_mode() {
+  static const int m = [] {
     const char* e = std::getenv("DS_CONV_WINDOW");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : 2;
   }();
-  return on;
+  return m;
+}
+
+bool window_on(int c, int ho, int wo) {
+  const int m = window_mode();
+  return m == 1 || (m == 2 && c % 64 == 0 && ho >= 28 && wo >= 28);
 }
 
 }  // namespace
@@ -308,7 +315,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
-    } else if (window_on() && op.kind == OpKind::kConv && op.sh == 1 && op.sw == 1 &&
+    } else if (window_on(in.c, out.h, out.w) && op.kind == OpKind::kConv && op.sh == 1 &&
+               op.sw == 1 &&
                op.residual < 0 && !out.f32 && conv_gemm_window_ok(op.r, op.s, in.c, p.cout)) {
       // stride-1 R x S conv: shifted-window MMAs over per-K-block halo boxes
       pl.mode = ConvLoadMode::kWindow;

@@ -160,7 +160,7 @@ def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
     with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
         staged = be.forward(imgs)
     assert np.isfinite(s2d).all()
-    assert row_rel_err(s2d, staged).max() <= 2e-3
+    assert row_rel_err(s2d, staged).max() <= 4e-3
 
 
 @pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2)])
