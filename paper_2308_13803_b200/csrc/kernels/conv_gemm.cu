@@ -30,6 +30,7 @@
 #include "sm100_ptx.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstdio>
 #include <mutex>
@@ -1038,7 +1039,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tc_fence_after();
           const uint32_t box = ptx::smem_u32(smem + L.a_off + s * a_stage);
           const uint32_t sbo = static_cast<uint32_t>(args.win_iw) * 32;
-          for (int t = 0, dr = 0, dc = 0; t < taps && !(args.debug_flags & 16);
+          const uint32_t b_base = ptx::smem_u32(smem + L.b_off);
+          // 2x2 / 4x4 taps (3x3 / 7x7 stems) with two sub-tiles: fully
+          // unrolled, every descriptor a compile-time offset (uniform issue)
+          auto unrolled = [&](auto dr_c, auto ds_c) {
+            constexpr int DR = decltype(dr_c)::value, DS = decltype(ds_c)::value;
+            constexpr int IW = 8 + DS - 1;
+            const uint64_t da0 = ptx::umma_desc_sw32_kmajor_sbo(box, IW * 32);
+            const uint64_t db0 = ptx::umma_desc_sw128_kmajor(b_base);
+            const uint64_t bstep = b_bytes >> 4;
+#pragma unroll
+            for (int t = 0; t < DR * DS; ++t)
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                ptx::umma_bf16_warp(d + q * args.BN,
+                                    da0 + static_cast<uint64_t>(((16 * q + t / DS) * IW + t % DS) * 2),
+                                    db0 + static_cast<uint64_t>(t >> 2) * bstep + 2 * (t & 3), idesc,
+                                    t != 0);
+          };
+          const bool fast = mt == 2 && !(args.debug_flags & 16);
+          if (fast && args.R == 2 && args.S == 2)
+            unrolled(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{});
+          else if (fast && args.R == 4 && args.S == 4)
+            unrolled(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+          for (int t = 0, dr = 0, dc = 0;
+               t < ((fast && args.R == args.S && (args.R == 2 || args.R == 4)) ? 0 : taps) &&
+               !(args.debug_flags & 16);
                ++t, dc = dc + 1 == args.S ? 0 : dc + 1, dr = dc == 0 ? dr + 1 : dr) {
             const uint64_t db = ptx::umma_desc_sw128_kmajor(
                 ptx::smem_u32(smem + L.b_off + (t >> 2) * b_bytes));

@@ -59,14 +59,14 @@ bool cluster_on() {
   return on;
 }
 
-// DS_STEM_S2D_MODE=box: the kS2D stem with one halo box per 32 x 8 block
-// (every tap an MMA window of it) instead of one TMA box per tap. Bit-exact
-// and a third of the TMA bytes, but the windows' unaligned 32 B-swizzle rows
-// cost more shared-memory wavefronts per MMA: slower on B200 (A/B switch).
+// DS_STEM_S2D_MODE=tap: the kS2D stem with one TMA box per tap instead of one
+// halo box per 32 x 8 block whose taps are MMA windows (the default: a
+// fraction of the TMA bytes, and with the taps unrolled the issue loop runs
+// at the tensor pipe's pace). A/B switch.
 bool s2d_tap_boxes() {
   static const bool on = [] {
     const char* e = std::getenv("DS_STEM_S2D_MODE");
-    return !(e && (std::string(e) == "box" || std::string(e) == "window"));
+    return e && std::string(e) == "tap";
   }();
   return on;
 }
