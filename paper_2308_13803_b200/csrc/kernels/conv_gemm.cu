@@ -1211,6 +1211,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
       if (args.b_res > 0) ptx::mbar_wait(b_full, 0);
+      // operand descriptors = per-CTA bases + slot / sub-tile offsets in the
+      // 16 B start-address units (addresses stay below 2^18, so the 14-bit
+      // start field never carries)
+      const uint64_t da_base = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.a_off));
+      const uint64_t db_base = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off));
+      const uint64_t a_step = a_stage >> 4, b_step = b_bytes >> 4;
       uint32_t j = 0;
       RingPos rp;
       for (int tile = walk_first; tile < walk_count; tile += walk_stride, ++j) {
@@ -1231,13 +1237,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::mbar_wait(&full[s], use & 1);
           ptx::tc_fence_after();
           const uint64_t db =
-              ptx::umma_desc_sw128_kmajor(
-                  ptx::smem_u32(smem + L.b_off + (args.b_res > 0 ? kb : static_cast<int>(s)) * b_bytes));
-          for (int q = 0; q < mt && !(args.debug_flags & 16); ++q) {  // (flag 16: bring-up)
-            const uint64_t da = ptx::umma_desc_sw128_kmajor(
-                ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes));
-            // the K block's four K=16 steps (+32 B in the swizzle row each)
-            ptx::umma_bf16_warp_k64(d + q * args.BN, da, db, idesc, kb != 0);
+              db_base + static_cast<uint64_t>(args.b_res > 0 ? static_cast<uint32_t>(kb) : s) * b_step;
+          const uint64_t da = da_base + static_cast<uint64_t>(s) * a_step;
+          // the K block's four K=16 steps (+32 B in the swizzle row each), per sub-tile
+          if (mt == 2) {
+            ptx::umma_bf16_warp_k64(d, da, db, idesc, kb != 0);
+            ptx::umma_bf16_warp_k64(d + args.BN, da + (kABytes >> 4), db, idesc, kb != 0);
+          } else {
+            for (int q = 0; q < mt; ++q)
+              ptx::umma_bf16_warp_k64(d + q * args.BN, da + static_cast<uint64_t>(q) * (kABytes >> 4),
+                                      db, idesc, kb != 0);
           }
           if (cl > 1)
             ptx::umma_commit_mc_warp(&empty[s], cl_mask);  // both CTAs read this B slot
