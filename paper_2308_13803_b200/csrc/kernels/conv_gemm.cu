@@ -44,6 +44,9 @@ constexpr int kABytes = kConvBM * kConvBK * 2;  // 16 KiB per stage
 // Output staging for the TMA-store epilogue: per epilogue warp two buffers
 // of 32 rows x 128 B (64 bf16 or 32 fp32 columns, 128 B-swizzled).
 constexpr int kYStageBytes = 32 * 128;
+// Staging buffers per epilogue warp: two (the next group fills while the
+// last one's TMA store reads), one when sixteen warps drain (smem for the ring).
+__host__ __device__ constexpr int y_bufs(int epi_warps) { return epi_warps > 8 ? 1 : 2; }
 
 // Warp roles (kConvThreads = 18 warps).
 constexpr int kEpiWarps = 8;      // warps 0-7: epilogue (two teams of four)
@@ -74,13 +77,22 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
   // kWindow: raw[2] + chunk-major[2] halo boxes
   L.win_off = L.y_off;
   L.y_off += 4 * static_cast<uint32_t>((win_bytes + 1023) / 1024 * 1024);
-  L.bar_off = L.y_off + epi_warps * 2 * kYStageBytes;
+  L.bar_off = L.y_off + epi_warps * y_bufs(epi_warps) * kYStageBytes;
   // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
   // box_full[stages], win barriers[8], tmem slot
   L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2 + 8) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
   L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
+}
+
+// Bring-up timeline stamps (args.ts, tools/test_conv_gemm TS=1): slot k of
+// this CTA's 64 = clock64() - entry clock. Slots: 0 entry globaltimer (ns),
+// 1 pdl_wait done, 2 MMA loop done, 3 exit; per tile j < 8: 8+j first A/B
+// stage landed (MMA), 16+j tile committed (MMA), 24+j epilogue got the
+// accumulator, 32+j epilogue stores issued, 40+j TMA first load issued.
+__device__ __forceinline__ void ts_mark(unsigned long long* ts, int k, long long t0) {
+  if (ts) ts[blockIdx.x * 64 + k] = static_cast<unsigned long long>(clock64() - t0);
 }
 
 // In-order position on the operand ring (iteration it = lap * stages + slot),
@@ -595,19 +607,23 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
 template <int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_gemm_kernel(const __grid_constant__ ConvGemmArgs args) {
-  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA);
+  // kPairTmaA: a TMA-A conv on CTA pairs, one M = 256 pair MMA per K step
+  // (cta_group::2 throughout), each CTA holding half of every B block
+  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA);
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
   // (offsetting smem_raw, rather than masking the generic address, keeps the
   // pointer in the shared window so accesses through it compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const long long ts0 = clock64();
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
   constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
   constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D);
   constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
   // (kWindow's A operands live in the halo boxes: its ring stages carry B only)
-  const SmemLayout L = smem_layout(args.BN, args.stages, args.Cout, epi_warps, args.b_res,
+  const SmemLayout L = smem_layout(kPair ? args.BN / 2 : args.BN, args.stages, args.Cout, epi_warps, args.b_res,
                                    kWin ? 1 : args.mt,
                                    kDw ? static_cast<int>(args.dw_box_bytes) : 0,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0);
@@ -666,7 +682,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                        ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
         ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
-        ptx::mbar_init(&empty[s], cl);  // (cluster: both CTAs' MMAs consume a multicast B slot)
+        // (cluster multicast: both CTAs' MMAs consume a B slot; pairs: the
+        // leader's commit arrives in both CTAs once)
+        ptx::mbar_init(&empty[s], kPair ? 1 : cl);
         ptx::mbar_init(&box_full[s], 1);
       }
       ptx::mbar_init(b_full, 1);
@@ -678,15 +696,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
-        ptx::mbar_init(&tmem_empty[b], 4);  // one arrival per warp of the owning team
+        // one arrival per warp of the owning teams (pairs: of both CTAs' teams)
+        ptx::mbar_init(&tmem_empty[b], 4 * (args.teams > n_acc ? args.teams / n_acc : 1) * (kPair ? 2 : 1));
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
       if (kTmaA || kBlk) ptx::tma_prefetch_desc(&args.tmap_a);  // (A / halo / tap boxes)
     }
     __syncwarp();
-    ptx::tmem_alloc(tmem_slot, args.tmem_cols);
-    ptx::tmem_relinquish();
+    if constexpr (kPair) {
+      ptx::tmem_alloc_pair(tmem_slot, args.tmem_cols);
+      ptx::tmem_relinquish_pair();
+    } else {
+      ptx::tmem_alloc(tmem_slot, args.tmem_cols);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -695,6 +719,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // activations (and the residual) come from earlier layers
+  if (args.ts && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.ts[blockIdx.x * 64] = gt;
+    ts_mark(args.ts, 1, ts0);
+  }
 
   if (warp < epi_warps) {
     // Epilogue: warp w reads TMEM lane quarter w%4 (tile rows 32*(w%4)..+31);
@@ -706,17 +736,25 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
     asm volatile("bar.sync 1, %0;" ::"r"(epi_warps * 32) : "memory");
     const int quarter = warp & 3;
-    const int team = warp >> 2;
-    uint8_t* ystage = smem + L.y_off + warp * 2 * kYStageBytes;
+    // teams per accumulator: with more teams than accumulators, tpa teams
+    // share each tile, team t taking column part t % tpa
+    const int tpa = args.teams > n_acc ? args.teams / n_acc : 1;
+    const int team = (warp >> 2) / tpa;
+    const int part = (warp >> 2) % tpa;
+    const int tile_teams = args.teams / tpa;
+    const int part_cols = args.BN / tpa;
+    const int ybufs = y_bufs(epi_warps);
+    uint8_t* ystage = smem + L.y_off + warp * ybufs * kYStageBytes;
     const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
     uint32_t j = 0, groups = 0;
     TileWalk tw(n_tiles, cl);
     for (int tile = walk_first; tile < walk_count; tile += walk_stride, ++j, tw.next()) {
-      if (static_cast<int>(j & (args.teams - 1)) != team) continue;  // teams: power of two
+      if (static_cast<int>(j & (tile_teams - 1)) != team) continue;  // teams: power of two
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
       ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
       ptx::tc_fence_after();
+      if (args.ts && quarter == 0 && lane == 0 && j < 8) ts_mark(args.ts, 24 + j, ts0);
       // pixel block of this tile (kBlk): image, block row / column
       int b_img = 0, b_y = 0, b_x = 0;
       if constexpr (kBlk) {
@@ -742,13 +780,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (args.debug_flags & 1) {
           // release only
         } else if (args.y_tma) {
-          for (int g0 = 0; g0 < args.BN && n0 + g0 < args.Cout; g0 += group_cols) {
-            uint8_t* group = ystage + (groups & 1) * kYStageBytes;
-            if (groups >= 2) {  // the store issued two groups ago must have read `group`
-              if (lane == 0) ptx::bulk_wait_read<1>();
+          const int g_end = (part + 1) * part_cols;
+          for (int g0 = part * part_cols; g0 < g_end && n0 + g0 < args.Cout; g0 += group_cols) {
+            uint8_t* group = ystage + (ybufs == 2 ? (groups & 1) * kYStageBytes : 0);
+            if (groups >= static_cast<uint32_t>(ybufs)) {  // the store that used `group` has read it
+              if (lane == 0) {
+                if (ybufs == 2)
+                  ptx::bulk_wait_read<1>();
+                else
+                  ptx::bulk_wait_read<0>();
+              }
               __syncwarp();
             }
-            for (int c = 0; c < group_cols && g0 + c < args.BN; c += 32) {
+            for (int c = 0; c < group_cols && g0 + c < g_end; c += 32) {
               uint32_t raw[32];
               ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
               ptx::tmem_ld_wait();
@@ -770,7 +814,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             ++groups;
           }
         } else {
-          for (int c0 = 0; c0 < args.BN && n0 + c0 < args.Cout; c0 += 16) {
+          for (int c0 = part * part_cols; c0 < (part + 1) * part_cols && n0 + c0 < args.Cout; c0 += 16) {
             uint32_t raw[16];
             ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
             ptx::tmem_ld_wait();
@@ -780,7 +824,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if (kPair && tw.rank != 0)
+          ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);  // the leader's MMA reuses it
+        else
+          ptx::mbar_arrive(&tmem_empty[acc]);
+      }
+      if (args.ts && quarter == 0 && lane == 0 && j < 8) ts_mark(args.ts, 32 + j, ts0);
     }
     if (lane == 0) ptx::bulk_wait<0>();
   } else if (warp < kGatherWarp0) {
@@ -960,7 +1010,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
   } else if (warp == kTmaWarp) {
     if (lane == 0) {
-      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      const uint32_t b_bytes = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
       const bool b_res = args.b_res > 0;
       if (b_res) {  // the whole weight matrix, once
         ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
@@ -985,6 +1035,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             rp.next(args.stages);
           }
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
+          if (args.ts && kb == 0 && j < 8) ts_mark(args.ts, 40 + j, ts0);
           if constexpr (kDw) {  // the K block's halo box
             const int img = tw.mb / dw_blocks_per_img;
             const int blk = tw.mb - img * dw_blocks_per_img;
@@ -1000,6 +1051,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 "r"(img)
                 : "memory");
             if (b_res) continue;
+          }
+          if constexpr (kPair) {
+            // both CTAs' bytes count on the leader's full barrier
+            if (tw.rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * tx);
+            ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
+                                  kb * kConvBK, n0 + tw.rank * (args.BN / 2));
+            ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.a_off + s * a_stage), &args.tmap_a, &full[s],
+                                  kb * kConvBK, m0);
+            continue;
           }
           ptx::mbar_arrive_expect_tx(&full[s], tx - (kDw ? 1u : 0u));
           if (!b_res && cl > 1) {  // this CTA's half of the B block, to both CTAs
@@ -1207,9 +1267,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     __syncwarp();
   } else {  // kMmaWarp: MMA issuer (whole warp: uniform descriptors, elected issue)
-    {
-      const uint32_t idesc = ptx::umma_idesc_bf16_f32(kConvBM, args.BN);
-      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+    // (pairs: the leader CTA's MMA warp issues for both; the peer's idles)
+    if (!kPair || ptx::cluster_ctarank() == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16_f32(kPair ? 2 * kConvBM : kConvBM, args.BN);
+      const uint32_t b_bytes = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
       if (args.b_res > 0) ptx::mbar_wait(b_full, 0);
       // operand descriptors = per-CTA bases + slot / sub-tile offsets in the
       // 16 B start-address units (addresses stay below 2^18, so the 14-bit
@@ -1236,10 +1297,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
           ptx::mbar_wait(&full[s], use & 1);
           ptx::tc_fence_after();
+          if (args.ts && kb == 0 && lane == 0 && j < 8) ts_mark(args.ts, 8 + j, ts0);
           const uint64_t db =
               db_base + static_cast<uint64_t>(args.b_res > 0 ? static_cast<uint32_t>(kb) : s) * b_step;
           const uint64_t da = da_base + static_cast<uint64_t>(s) * a_step;
           // the K block's four K=16 steps (+32 B in the swizzle row each), per sub-tile
+          if constexpr (kPair) {
+            ptx::umma_bf16_pair_k64(d, da, db, idesc, kb != 0);
+            ptx::umma_commit_pair_warp(&empty[s], 3);  // both CTAs' slots
+            continue;
+          }
           if (mt == 2) {
             ptx::umma_bf16_warp_k64(d, da, db, idesc, kb != 0);
             ptx::umma_bf16_warp_k64(d + args.BN, da + (kABytes >> 4), db, idesc, kb != 0);
@@ -1253,18 +1320,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           else
             ptx::umma_commit_warp(&empty[s]);
         }
-        ptx::umma_commit_warp(&tmem_full[acc]);
+        if constexpr (kPair)
+          ptx::umma_commit_pair_warp(&tmem_full[acc], 3);
+        else
+          ptx::umma_commit_warp(&tmem_full[acc]);
+        if (args.ts && lane == 0 && j < 8) ts_mark(args.ts, 16 + j, ts0);
       }
+      if (args.ts && lane == 0) ts_mark(args.ts, 2, ts0);
     }
     __syncwarp();
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (args.ts && threadIdx.x == 0) ts_mark(args.ts, 3, ts0);
   if (cl > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == kTmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, args.tmem_cols);
+    if constexpr (kPair)
+      ptx::tmem_dealloc_pair(tmem_base, args.tmem_cols);
+    else
+      ptx::tmem_dealloc(tmem_base, args.tmem_cols);
   }
 }
 
@@ -1500,6 +1576,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -1518,6 +1597,12 @@ int conv_gemm_sm_count() {
 cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cudaStream_t stream) {
   // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
   ConvGemmArgs args = in_args;
+  const bool pair = mode == ConvLoadMode::kPairTmaA;
+  if (pair) {
+    // CTA pairs: each CTA's B half is BN / 2 rows of 128 B swizzle atoms
+    if (args.BN % 16 != 0 || args.BN > 256) return cudaErrorInvalidValue;
+    args.cluster = 2;
+  }
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
   // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
@@ -1545,9 +1630,18 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const uint32_t acc_cols = pow2_at_least(args.mt * args.BN);
   args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / acc_cols)));
   args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(acc_cols));
-  args.teams = std::min(mode == ConvLoadMode::kTmaA && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
+  args.teams = std::min((mode == ConvLoadMode::kTmaA || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
   if (args.teams == 3) args.teams = 2;  // a power of two
+  // wide TMA-A tiles with two accumulators: the idle gather warps join and
+  // two teams split each tile's columns (DS_CONV_TPA=0: off)
+  static const bool tpa_on = [] {
+    const char* e = std::getenv("DS_CONV_TPA");
+    return !(e && e[0] == '0');
+  }();
+  if (tpa_on && (mode == ConvLoadMode::kTmaA || pair) && args.BN >= 128 && args.n_acc == 2 &&
+      args.BN % (2 * group_cols) == 0)
+    args.teams = 4;
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
@@ -1558,7 +1652,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
   if (args.cluster > 1) args.b_res = 0;  // (multicast B streams through the ring)
   const int bres = args.b_res;
-  args.stages = conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, bres, args.mt);
+  args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, bres, args.mt);
   const bool dw = mode == ConvLoadMode::kDwFused;
   const int box = dw ? static_cast<int>(args.dw_box_bytes) : 0;
   if (dw) {
@@ -1617,7 +1711,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       dw ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres, 1, box).total + 1024
       : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
                           static_cast<int>(args.win_box_bytes)).total + 1024
-            : conv_gemm_smem_bytes(args.BN, args.stages, args.Cout, 4 * args.teams, bres, args.mt);
+            : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
+                                   bres, args.mt);
   const bool blk = dw || win || mode == ConvLoadMode::kS2D;
   const int tiles =
       blk ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
@@ -1627,12 +1722,14 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
   const int per_sm = std::max(1, std::min(by_smem, by_tmem));
   if (args.cluster > 1) {  // pairs of CTAs over (M-block pair, N block) units
-    if (mode != ConvLoadMode::kTmaA || args.b_res > 0 || args.cluster != 2) return cudaErrorInvalidValue;
+    if ((mode != ConvLoadMode::kTmaA && !pair) || args.b_res > 0 || args.cluster != 2 ||
+        (pair && args.mt != 1))
+      return cudaErrorInvalidValue;
     const int m_blocks = (args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt);
     const int units = n_tiles * ((m_blocks + 1) / 2);
     const int ctas = std::min(2 * units, conv_gemm_sm_count() * per_sm) / 2 * 2;
-    return launch_pdl_cluster(conv_gemm_kernel<2>, dim3(ctas), dim3(kConvThreads), smem, stream, 2,
-                              args);
+    return launch_pdl_cluster(pair ? conv_gemm_kernel<7> : conv_gemm_kernel<2>, dim3(ctas),
+                              dim3(kConvThreads), smem, stream, 2, args);
   }
   args.cluster = 1;
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
@@ -1651,6 +1748,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kS2D:
       return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kPairTmaA:
+      break;  // (launched above)
   }
   return cudaGetLastError();
 }

@@ -52,6 +52,9 @@ struct ConvGemmArgs {
   int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
   int out_f32, relu;
   int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
+  // bring-up timeline (tools/test_conv_gemm TS=1): per CTA 64 clock64 stamps
+  // relative to kernel entry, see conv_gemm.cu ts_mark(); nullptr in the runtime
+  unsigned long long* ts;
   // kDwFused: A[m, c] = relu(dw3x3(x)[m, c] + dw_b[c]), computed in the
   // producer from the depthwise input x ([H][W][C], pad 1, stride dw_stride);
   // Ho/Wo are the depthwise output dims, R = S = 1. Tiles are dw_th x dw_tw
@@ -91,6 +94,8 @@ enum class ConvLoadMode : int {
   kWindow = 5,    // stride-1 R x S conv as shifted-window MMAs over a per-K-block halo box
   kS2D = 6,       // stride-2 stem over its space-to-depth input: per tap one TMA box, no
                   // producer warps (A arrives in the MMA's 32 B-swizzled layout)
+  kPairTmaA = 7,  // kTmaA on CTA pairs: one M = 256 cta_group::2 MMA per K step, each CTA
+                  // loading its 128 A rows and half of the B block (tmap_b box rows BN / 2)
 };
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in

@@ -59,6 +59,18 @@ bool cluster_on() {
   return on;
 }
 
+// DS_CONV_PAIR: TMA-A layers whose weights stream (not resident) run on CTA
+// pairs with M = 256 cta_group::2 MMAs, each CTA staging half of every B
+// block (a third less shared-memory traffic per MMA at 128 x 256 tiles).
+// 1 (default): BN >= 128; 0: off.
+bool pair_on(int bn) {
+  static const int m = [] {
+    const char* e = std::getenv("DS_CONV_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m == 1 && bn >= 128;
+}
+
 // DS_STEM_S2D_MODE=tap: the kS2D stem with one TMA box per tap instead of one
 // halo box per 32 x 8 block whose taps are MMA windows (the default: a
 // fraction of the TMA bytes, and with the taps unrolled the issue loop runs
@@ -343,6 +355,10 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     // wide TMA-A layers: CTA pairs may multicast each weight block (opt-in)
     const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
     a.cluster = pl.mode == ConvLoadMode::kTmaA && a.BN == 256 && !b_resident && cluster_on() ? 2 : 1;
+    if (pl.mode == ConvLoadMode::kTmaA && a.cluster == 1 && !b_resident && pair_on(a.BN)) {
+      pl.mode = ConvLoadMode::kPairTmaA;
+      a.cluster = 2;  // (tmap_b boxes of BN / 2 rows: each CTA's half)
+    }
     if (static_cast<int>(i) == s2d_.op) {
       if (!encode_tmap_2d_bf16(&a.tmap_b, d_stem_w_, p.cout, s2d_.kpad, s2d_.kpad, a.BN))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem weights)");
@@ -350,7 +366,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                                     a.BN / a.cluster)) {
       throw CudaError("cuTensorMapEncodeTiled failed (weights)");
     }
-    if (pl.mode == ConvLoadMode::kTmaA) {
+    if (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA) {
       const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
       if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
         throw CudaError("cuTensorMapEncodeTiled failed (activations)");

@@ -186,3 +186,22 @@ def test_softmax_probs():
     ref = np.exp(logits - logits.max(1, keepdims=True))
     ref /= ref.sum(1, keepdims=True)
     np.testing.assert_allclose(probs, ref, rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 5), ("resnet50_v1", 3), ("inception_v3", 2)])
+def test_pair_mma_matches_single_cta(monkeypatch, model, bs):
+    """1x1 convs on CTA pairs (kPairTmaA: one M = 256 cta_group::2 MMA per K
+    step, each CTA holding its 128 A rows and half of the B block; two
+    epilogue teams per tile when the gather warps idle) against single-CTA
+    M = 128 MMAs: the same products summed in the same K order, so
+    bit-identical logits."""
+    imgs = generate_images(model, 17, bs)
+    monkeypatch.setenv("DS_CONV_PAIR", "1")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        pair = be.forward(imgs)
+    monkeypatch.setenv("DS_CONV_PAIR", "0")
+    monkeypatch.setenv("DS_CONV_TPA", "0")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        single = be.forward(imgs)
+    assert np.isfinite(pair).all()
+    assert np.array_equal(pair, single)

@@ -62,7 +62,13 @@ static int run(const Case& cs) {
   cudaMemset(dy, 0xFF, ybytes);  // NaN-fill so unwritten outputs are caught
 
   ConvGemmArgs a{};
-  if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad, cs.BN)) {
+  a.cluster = getenv("CLUSTER") ? atoi(getenv("CLUSTER")) : 1;  // 2: CTA pairs multicast B
+  ConvLoadMode mode = cs.mode;
+  if (getenv("PAIR") && mode == ConvLoadMode::kTmaA) {  // cta_group::2 pair MMAs
+    mode = ConvLoadMode::kPairTmaA;
+    a.cluster = 2;
+  }
+  if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad, cs.BN / a.cluster)) {
     printf("%s: tmap_b encode failed\n", cs.name);
     return 1;
   }
@@ -87,7 +93,7 @@ static int run(const Case& cs) {
   a.y = dy; a.ldy = ldy; a.c_off = cs.c_off; a.out_f32 = cs.f32; a.relu = cs.relu;
   // channels [c_off, c_off+Cout) of an ldy-wide buffer; keep Cout+c_off <= ldy
   conv_gemm_init();
-  cudaError_t e = launch_conv_gemm(a, cs.mode, 0);
+  cudaError_t e = launch_conv_gemm(a, mode, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("%s: CUDA error %s\n", cs.name, cudaGetErrorString(e));
@@ -96,11 +102,50 @@ static int run(const Case& cs) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int i = 0; i < 20; ++i) launch_conv_gemm(a, cs.mode, 0);
+  for (int i = 0; i < 20; ++i) launch_conv_gemm(a, mode, 0);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
   ms /= 20;
+
+  if (getenv("TS")) {  // per-CTA timeline of one launch (3rd of 3 back to back)
+    unsigned long long* dts;
+    const int nct = 148 * 2;
+    cudaMalloc(&dts, nct * 64 * 8);
+    cudaMemset(dts, 0, nct * 64 * 8);
+    a.ts = dts;
+    for (int i = 0; i < 3; ++i) launch_conv_gemm(a, mode, 0);
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> h(nct * 64);
+    cudaMemcpy(h.data(), dts, h.size() * 8, cudaMemcpyDeviceToHost);
+    a.ts = nullptr;
+    cudaFree(dts);
+    unsigned long long g0 = ~0ull, g1 = 0;
+    int ctas = 0;
+    for (int c = 0; c < nct; ++c)
+      if (h[c * 64]) { g0 = std::min(g0, h[c * 64]); g1 = std::max(g1, h[c * 64]); ++ctas; }
+    printf("  timeline: %d CTAs, entry spread %.2f us (globaltimer)\n", ctas, (g1 - g0) * 1e-3);
+    auto stat = [&](int k, const char* name) {
+      std::vector<double> v;
+      for (int c = 0; c < ctas; ++c)
+        if (h[c * 64 + k]) v.push_back(h[c * 64 + k] / 1965.0);
+      if (v.empty()) return;
+      std::sort(v.begin(), v.end());
+      printf("  %-22s n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", name, v.size(), v[0],
+             v[v.size() / 2], v.back());
+    };
+    stat(1, "pdl_wait done");
+    for (int j = 0; j < 8; ++j) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "tile%d TMA issue", j); stat(40 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d MMA first", j); stat(8 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d MMA commit", j); stat(16 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d epi start", j); stat(24 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d epi end", j); stat(32 + j, nm);
+    }
+    stat(2, "MMA loop done");
+    stat(3, "exit barrier");
+  }
 
   std::vector<uint8_t> hy(ybytes);
   cudaMemcpy(hy.data(), dy, ybytes, cudaMemcpyDeviceToHost);
