@@ -58,12 +58,13 @@ __global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restr
                                  int w, int hs, int ws, int pad, long long pixels) {
   pdl_trigger();
   pdl_wait();
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // (32-bit index arithmetic: the launcher keeps pixels below 2^31)
+  const int i = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= pixels) return;
-  const int X = static_cast<int>(i % ws);
-  const long long t = i / ws;
-  const int Y = static_cast<int>(t % hs);
-  const long long n = t / hs;
+  const int t = i / ws;
+  const int X = i - t * ws;
+  const int n = t / hs;
+  const int Y = t - n * hs;
   uint32_t v[8];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -76,7 +77,7 @@ __global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restr
       // p + 0.5 minus (2^22 + 128), exactly and without the conversion pipe
       float f[3] = {0.f, 0.f, 0.f};
       if (y >= 0 && y < h && x >= 0 && x < w) {
-        const uint8_t* src = img + ((n * h + y) * w + x) * 3;
+        const uint8_t* src = img + ((static_cast<long long>(n) * h + y) * w + x) * 3;
 #pragma unroll
         for (int c = 0; c < 3; ++c)
           f[c] = __fmul_rn(__fsub_rn(__uint_as_float(0x4A800001u + 2u * __ldg(src + c)), 4194432.0f),
@@ -360,6 +361,7 @@ cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, in
 cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w, int hs,
                              int ws, int pad, cudaStream_t stream) {
   const long long pixels = static_cast<long long>(n) * hs * ws;
+  if (pixels >= (1LL << 31)) return cudaErrorInvalidValue;
   return launch_pdl(stage_s2d_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
                     reinterpret_cast<uint4*>(out), h, w, hs, ws, pad, pixels);
 }
