@@ -554,7 +554,7 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
 // offset inside its staging group.
 __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const float* bias_s, int m,
                                                    int n, const uint32_t (&raw)[32], uint8_t* group,
-                                                   int col, int lane) {
+                                                   int col, int lane, const uint4 (&res)[4]) {
   float v[32];
   const float4* b4 = reinterpret_cast<const float4*>(bias_s + n);  // n % 32 == 0
 #pragma unroll
@@ -567,11 +567,10 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
   }
   if (a.residual && m < a.M) {
     const __nv_bfloat16* rrow = a.residual + static_cast<size_t>(m) * a.ld_res + n;
-    if (n + 32 <= a.Cout) {
-      const uint4* rp = reinterpret_cast<const uint4*>(rrow);
+    if (n + 32 <= a.Cout) {  // (loaded by the caller before the TMEM load)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 rr = __ldg(rp + q);
+        const uint4 rr = res[q];
         const uint32_t w[4] = {rr.x, rr.y, rr.z, rr.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -752,6 +751,29 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (static_cast<int>(j & (tile_teams - 1)) != team) continue;  // teams: power of two
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
+      if (!kBlk && args.residual) {
+        // pull this lane's residual rows (its column part) into L2 a tile
+        // ahead — this team's next tile (and, the first time, this one) — so
+        // the epilogue's loads do not each wait on HBM
+        auto prefetch_res = [&](const TileWalk& w) {
+          for (int q = 0; q < mt; ++q) {
+            const int m = w.mb * tile_rows + q * kConvBM + quarter * 32 + lane;
+            const int c0 = w.nb * args.BN + part * part_cols;
+            if (m >= args.M || c0 >= args.Cout) break;
+            const char* rrow =
+                reinterpret_cast<const char*>(args.residual + static_cast<size_t>(m) * args.ld_res + c0);
+            const int bytes = min(part_cols, args.Cout - c0) * 2;
+            for (int c = 0; c < bytes; c += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rrow + c));
+          }
+        };
+        if (args.res_prefetch == 1 || (args.res_prefetch == 2 && j < static_cast<uint32_t>(tile_teams)))
+          prefetch_res(tw);
+        if (args.res_prefetch == 2 && tile + tile_teams * walk_stride < walk_count) {
+          TileWalk ahead = tw;
+          for (int k = 0; k < tile_teams; ++k) ahead.next();
+          prefetch_res(ahead);
+        }
+      }
       ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
       ptx::tc_fence_after();
       if (args.ts && quarter == 0 && lane == 0 && j < 8) ts_mark(args.ts, 24 + j, ts0);
@@ -793,10 +815,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               __syncwarp();
             }
             for (int c = 0; c < group_cols && g0 + c < g_end; c += 32) {
+              // residual slice first: its global load overlaps the TMEM load
+              uint4 res[4];
+              if (args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
+                const uint4* rp = reinterpret_cast<const uint4*>(
+                    args.residual + static_cast<size_t>(m) * args.ld_res + n0 + g0 + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) res[q] = __ldg(rp + q);
+              }
               uint32_t raw[32];
               ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
               ptx::tmem_ld_wait();
-              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane);
+              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res);
             }
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
@@ -1635,6 +1665,11 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   if (args.teams == 3) args.teams = 2;  // a power of two
   // wide TMA-A tiles with two accumulators: the idle gather warps join and
   // two teams split each tile's columns (DS_CONV_TPA=0: off)
+  static const int res_prefetch = [] {  // bring-up A/B: 0 none, 1 this tile, 2 a tile ahead
+    const char* e = std::getenv("DS_RES_PREFETCH");
+    return e ? std::atoi(e) : 1;
+  }();
+  args.res_prefetch = res_prefetch;
   static const bool tpa_on = [] {
     const char* e = std::getenv("DS_CONV_TPA");
     return !(e && e[0] == '0');

@@ -48,6 +48,7 @@ struct ConvGemmArgs {
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;
+  int res_prefetch;  // epilogue L2 prefetch of residual rows (launch_conv_gemm sets it)
   void* y;
   int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
   int out_f32, relu;
