@@ -87,13 +87,30 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
 }
 
 // Bring-up timeline stamps (args.ts, tools/test_conv_gemm TS=1): slot k of
-// this CTA's 64 = clock64() - entry clock. Slots: 0 entry globaltimer (ns),
+// this CTA's 64 = clock64() (slot 4: at entry). Slots: 0 entry globaltimer (ns),
 // 1 pdl_wait done, 2 MMA loop done, 3 exit; per tile j < 8: 8+j first A/B
 // stage landed (MMA), 16+j tile committed (MMA), 24+j epilogue got the
 // accumulator, 32+j epilogue stores issued, 40+j TMA first load issued.
-__device__ __forceinline__ void ts_mark(unsigned long long* ts, int k, long long t0) {
-  if (ts) ts[blockIdx.x * 64 + k] = static_cast<unsigned long long>(clock64() - t0);
+// (raw clocks; slot 4 holds the entry clock, which the tool subtracts, so no
+// register stays live for it)
+__device__ __forceinline__ void ts_mark(unsigned long long* ts, int k, long long = 0) {
+  if (ts) ts[blockIdx.x * 64 + k] = static_cast<unsigned long long>(clock64());
 }
+
+// floor(a / d) for a < 2^24 through a float reciprocal computed once per
+// kernel, corrected to exact (the per-tile pixel-block decode would otherwise
+// run two ~40-instruction integer divisions on every tile).
+struct SmallDiv {
+  int d;
+  float rcp;
+  __device__ __forceinline__ explicit SmallDiv(int dv) : d(dv), rcp(1.0f / static_cast<float>(dv)) {}
+  __device__ __forceinline__ int div(int a) const {
+    int q = __float2int_rz(__int2float_rz(a) * rcp);
+    if (q * d > a) --q;
+    if ((q + 1) * d <= a) ++q;
+    return q;
+  }
+};
 
 // In-order position on the operand ring (iteration it = lap * stages + slot),
 // advanced incrementally: the single-thread MMA/TMA loops are latency-bound,
@@ -615,7 +632,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // (offsetting smem_raw, rather than masking the generic address, keeps the
   // pointer in the shared window so accesses through it compile to LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  const long long ts0 = clock64();
+  if (threadIdx.x == 0) ts_mark(args.ts, 4);
+  constexpr long long ts0 = 0;
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
   constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
@@ -737,12 +755,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int quarter = warp & 3;
     // teams per accumulator: with more teams than accumulators, tpa teams
     // share each tile, team t taking column part t % tpa
-    const int tpa = args.teams > n_acc ? args.teams / n_acc : 1;
+    const int tpa = kTmaA && args.teams > n_acc ? args.teams / n_acc : 1;
     const int team = (warp >> 2) / tpa;
     const int part = (warp >> 2) % tpa;
     const int tile_teams = args.teams / tpa;
     const int part_cols = args.BN / tpa;
     const int ybufs = y_bufs(epi_warps);
+    const int sub_rows = kBlk ? kConvBM / args.dw_tw : 0;  // block rows per 128-row sub-tile
     uint8_t* ystage = smem + L.y_off + warp * ybufs * kYStageBytes;
     const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
     uint32_t j = 0, groups = 0;
@@ -780,9 +799,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       // pixel block of this tile (kBlk): image, block row / column
       int b_img = 0, b_y = 0, b_x = 0;
       if constexpr (kBlk) {
-        b_img = tw.mb / dw_blocks_per_img;
+        b_img = SmallDiv(dw_blocks_per_img).div(tw.mb);
         const int blk = tw.mb - b_img * dw_blocks_per_img;
-        b_y = blk / args.dw_tiles_x;
+        b_y = SmallDiv(args.dw_tiles_x).div(blk);
         b_x = blk - b_y * args.dw_tiles_x;
       }
       for (int q = 0; q < mt; ++q) {  // sub-tile q: rows m0 .. m0+127, columns q*BN ..
@@ -832,7 +851,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             __syncwarp();
             if (lane == 0) {
               if constexpr (kBlk) {  // this warp's rw pixel rows of the TH x TW block
-                const int yq = q * (kConvBM / args.dw_tw) + quarter * args.dw_rw;  // in-block row
+                const int yq = q * sub_rows + quarter * args.dw_rw;  // in-block row
                 if (yq < args.dw_th)
                   ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, b_x * args.dw_tw,
                                     b_y * args.dw_th + yq, b_img);
@@ -959,9 +978,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
-        const int img = tw.mb / dw_blocks_per_img;
+        const int img = SmallDiv(dw_blocks_per_img).div(tw.mb);
         const int blk = tw.mb - img * dw_blocks_per_img;
-        const int by = blk / args.dw_tiles_x;
+        const int by = SmallDiv(args.dw_tiles_x).div(blk);
         const int bx = blk - by * args.dw_tiles_x;
         if (args.win_iw > 0) {  // one halo box per block holds every tap's window
           const uint32_t s = rp.slot;
@@ -1010,9 +1029,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       uint32_t u = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
         const int n0 = tw.nb * args.BN;
-        const int img = tw.mb / dw_blocks_per_img;
+        const int img = SmallDiv(dw_blocks_per_img).div(tw.mb);
         const int blk = tw.mb - img * dw_blocks_per_img;
-        const int by = blk / args.dw_tiles_x;
+        const int by = SmallDiv(args.dw_tiles_x).div(blk);
         const int bx = blk - by * args.dw_tiles_x;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
           // (direct mode: 4 box slots, the MMA frees them; else 2 + 2 transposed)
@@ -1067,9 +1086,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
           if (args.ts && kb == 0 && j < 8) ts_mark(args.ts, 40 + j, ts0);
           if constexpr (kDw) {  // the K block's halo box
-            const int img = tw.mb / dw_blocks_per_img;
+            const int img = SmallDiv(dw_blocks_per_img).div(tw.mb);
             const int blk = tw.mb - img * dw_blocks_per_img;
-            const int by = blk / args.dw_tiles_x;
+            const int by = SmallDiv(args.dw_tiles_x).div(blk);
             const int bx = blk - by * args.dw_tiles_x;
             ptx::mbar_arrive_expect_tx(&box_full[s], args.dw_box_bytes);
             asm volatile(

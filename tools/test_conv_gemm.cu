@@ -128,7 +128,7 @@ static int run(const Case& cs) {
     auto stat = [&](int k, const char* name) {
       std::vector<double> v;
       for (int c = 0; c < ctas; ++c)
-        if (h[c * 64 + k]) v.push_back(h[c * 64 + k] / 1965.0);
+        if (h[c * 64 + k]) v.push_back((h[c * 64 + k] - h[c * 64 + 4]) / 1965.0);
       if (v.empty()) return;
       std::sort(v.begin(), v.end());
       printf("  %-22s n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", name, v.size(), v[0],
