@@ -44,6 +44,9 @@ constexpr int kABytes = kConvBM * kConvBK * 2;  // 16 KiB per stage
 // Output staging for the TMA-store epilogue: per epilogue warp two buffers
 // of 32 rows x 128 B (64 bf16 or 32 fp32 columns, 128 B-swizzled).
 constexpr int kYStageBytes = 32 * 128;
+// kPwDw: per epilogue team one zero-bordered halo buffer of up to 16 x 16
+// pixels x 64 channels (the two fill the sixteen warps' output staging)
+constexpr int kPdHaloBytes = 16 * 16 * 128;
 // Staging buffers per epilogue warp: two (the next group fills while the
 // last one's TMA store reads), one when sixteen warps drain (smem for the ring).
 __host__ __device__ constexpr int y_bufs(int epi_warps) { return epi_warps > 8 ? 1 : 2; }
@@ -620,13 +623,173 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
   }
 }
 
+// Depthwise 3x3 (+bias, ReLU) of one 64-channel round from the halo buffer:
+// items are (output row, strip of kPdQ outputs, 4-channel group g4); each
+// input vector of a strip row is loaded once and feeds up to three outputs,
+// in the standalone kernels' per-output fma order (row r outer, tap s inner).
+constexpr int kPdQ = 7;
+
+__device__ __forceinline__ void dw_fma4(float (&acc)[4], const uint2& x, const uint2& w) {
+  acc[0] = dw_fma_lo(x.x, w.x, acc[0]);
+  acc[1] = dw_fma_hi(x.x, w.x, acc[1]);
+  acc[2] = dw_fma_lo(x.y, w.y, acc[2]);
+  acc[3] = dw_fma_hi(x.y, w.y, acc[3]);
+}
+
+template <int S>
+__device__ __forceinline__ void pwdw_strips(uint32_t halo, uint32_t wp, uint32_t bp, int cout, int hp_w,
+                                            int hd, int wd, int g4, int tid, __nv_bfloat16* yimg, int ldy) {
+  const int strips = wd / kPdQ;
+  const int items = hd * strips * 16;
+  const int chunk = g4 >> 1, half = (g4 & 1) * 8;  // 8 B half of a 16 B halo chunk
+  for (int it = tid; it < items; it += 256) {
+    const int rest = it >> 4;
+    const int oy = rest / strips, strip = rest - (rest / strips) * strips;
+    float a[kPdQ][4];
+    {
+      uint4 b;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(bp));
+#pragma unroll
+      for (int q = 0; q < kPdQ; ++q) {
+        a[q][0] = __uint_as_float(b.x); a[q][1] = __uint_as_float(b.y);
+        a[q][2] = __uint_as_float(b.z); a[q][3] = __uint_as_float(b.w);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      uint2 w[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[c] = ptx::lds64(wp + (r * 3 + c) * cout * 2);
+      const int h0 = (oy * S + r) * hp_w + strip * kPdQ * S;
+#pragma unroll
+      for (int u = 0; u < (kPdQ - 1) * S + 3; ++u) {
+        const int hq = h0 + u;
+        const uint2 x = ptx::lds64(halo + hq * 128 + ((chunk ^ (hq & 7)) << 4) + half);
+        // outputs q with q * S + c == u, taps c in ascending order
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if ((u - c) >= 0 && (u - c) % S == 0 && (u - c) / S < kPdQ) dw_fma4(a[(u - c) / S], x, w[c]);
+      }
+    }
+    __nv_bfloat16* yp = yimg + (static_cast<size_t>(oy) * wd + strip * kPdQ) * ldy;
+#pragma unroll
+    for (int q = 0; q < kPdQ; ++q)
+      *reinterpret_cast<uint2*>(yp + q * ldy) =
+          make_uint2(pack2_bf16(fmaxf(a[q][0], 0.f), fmaxf(a[q][1], 0.f)),
+                     pack2_bf16(fmaxf(a[q][2], 0.f), fmaxf(a[q][3], 0.f)));
+  }
+}
+
+// kPwDw epilogue. Two teams of eight warps take alternate tiles (tile j ->
+// team j % 2, accumulator j % n_acc); a tile is one image's Ho x Wo pixels
+// (mt 128-row sub-tiles) x BN pointwise channels. Per 64-channel round the
+// team's warps move TMEM (warp: lane quarter w % 4 of sub-tile (w / 4) % 2,
+// two 32-column slices) + bias, ReLU, bf16 into the team's zero-bordered halo
+// buffer [(Ho + 2) x (Wo + 2) pixels][64 ch] (16 B chunk c of pixel p at
+// c ^ (p & 7): conflict-free), then compute the depthwise 3x3 (stride
+// dw_stride, pad 1) + bias + ReLU of those 64 channels straight to HBM with
+// the standalone kernels' fma order, so the result is bit-identical to the
+// two-kernel path. The pointwise output never leaves shared memory.
+__device__ __forceinline__ void pwdw_epilogue(const ConvGemmArgs& args, uint8_t* halo_base, uint32_t dwp,
+                                           const float* bias_s, uint32_t tmem_base, uint32_t acc_stride,
+                                           uint64_t* tmem_full, uint64_t* tmem_empty, int n_acc,
+                                           int acc_log2, int n_tiles, int warp, int lane) {
+  const int team = warp >> 3;
+  const int quarter = warp & 3;
+  const int sub = (warp >> 2) & 1;
+  const int tid = threadIdx.x & 255;  // thread index in the team
+  const int hw = args.Ho * args.Wo;
+  const int hp_w = args.Wo + 2;  // halo row pitch (pixels)
+  const int S = args.dw_stride;
+  const int hd = (args.Ho - 1) / S + 1, wd = (args.Wo - 1) / S + 1;
+  const uint32_t halo = ptx::smem_u32(halo_base) + team * kPdHaloBytes;
+  const int barrier_id = 2 + team;
+  // depthwise weights [9][Cout] bf16 then bias [Cout] fp32, staged in smem at dwp
+  const uint32_t dw_bias = dwp + 9 * args.Cout * 2;
+  const int p = sub * kConvBM + quarter * 32 + lane;  // this lane's pixel in the image
+  const bool row_ok = sub < args.mt && p < hw;
+  const int py = p / args.Wo, px = p - (p / args.Wo) * args.Wo;
+  const int hpix = (py + 1) * hp_w + px + 1;
+  // (CTA pairs: units of (image pair, N block); this CTA's image is 2 * pair + rank)
+  const int cl = args.cluster > 1 ? 2 : 1;
+  const int images = args.M / hw;
+  TileWalk tw(n_tiles, cl);
+  const int walk_count = n_tiles * ((images + cl - 1) / cl);
+  uint32_t j = 0;
+  for (int tile = blockIdx.x / cl; tile < walk_count; tile += gridDim.x / cl, ++j, tw.next()) {
+    if (static_cast<int>(j & 1) != team) continue;
+    const bool img_ok = tw.mb < images;
+    const int n0 = tw.nb * args.BN;
+    const uint32_t acc = j & (n_acc - 1);
+    ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
+    ptx::tc_fence_after();
+    const bool stamp = args.ts && (warp & 7) == 0 && lane == 0 && j < 8;
+    if (stamp) ts_mark(args.ts, 24 + j);
+    const int rounds = args.BN / 64;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int c0 = n0 + rd * 64;  // first pointwise / depthwise channel of the round
+      if (sub < args.mt && img_ok) {
+        const uint32_t t_row = tmem_base + acc * acc_stride + sub * args.BN + rd * 64 +
+                               (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          uint32_t raw[32];
+          ptx::tmem_ld_32x32b_x32(t_row + sl * 32, raw);
+          ptx::tmem_ld_wait();
+          if (row_ok) {
+            const float* b = bias_s + c0 + sl * 32;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(raw[8 * k + e]) + b[8 * k + e];
+              ptx::sts128(halo + hpix * 128 + (((sl * 4 + k) ^ (hpix & 7)) << 4), relu_pack8(v));
+            }
+          }
+        }
+      }
+      if (rd == rounds - 1) {  // this warp's TMEM reads of the tile are done
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (cl > 1 && tw.rank != 0)
+            ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);  // the leader's MMA reuses it
+          else
+            ptx::mbar_arrive(&tmem_empty[acc]);
+        }
+      }
+      if (!img_ok) continue;  // (odd image count: the pair's second CTA has no image)
+      asm volatile("bar.sync %0, 256;" ::"r"(barrier_id) : "memory");  // halo complete
+      if (stamp && rd == 0) ts_mark(args.ts, 48 + j);
+      const int g4 = tid & 15;    // this thread's 4-channel group of the round
+      const int ch = c0 + g4 * 4;
+      __nv_bfloat16* yimg = static_cast<__nv_bfloat16*>(args.y) +
+                            static_cast<size_t>(tw.mb) * hd * wd * args.ldy + ch;
+      if (S == 1)
+        pwdw_strips<1>(halo, dwp + ch * 2, dw_bias + ch * 4, args.Cout, hp_w, hd, wd, g4, tid, yimg,
+                       args.ldy);
+      else
+        pwdw_strips<2>(halo, dwp + ch * 2, dw_bias + ch * 4, args.Cout, hp_w, hd, wd, g4, tid, yimg,
+                       args.ldy);
+      asm volatile("bar.sync %0, 256;" ::"r"(barrier_id) : "memory");  // halo reads done
+    }
+    if (stamp) ts_mark(args.ts, 32 + j);
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_gemm_kernel(const __grid_constant__ ConvGemmArgs args) {
   // kPairTmaA: a TMA-A conv on CTA pairs, one M = 256 pair MMA per K step
   // (cta_group::2 throughout), each CTA holding half of every B block
-  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA);
-  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair;
+  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA) ||
+                        MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
+  // kPwDw: a 1x1 conv whose tile is one whole image (<= 256 pixels) x BN
+  // channels, and whose epilogue runs the following depthwise 3x3 on it
+  constexpr bool kPD = MODE == static_cast<int>(ConvLoadMode::kPwDw) ||
+                      MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kPD;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
   // (offsetting smem_raw, rather than masking the generic address, keeps the
@@ -673,7 +836,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
-  const int tile_rows = kConvBM * mt;
+  const int tile_rows = kPD ? args.Ho * args.Wo : kConvBM * mt;
   // kDwFused: M blocks are TH x TW pixel blocks of one image
   const int dw_blocks_per_img = args.dw_tiles_y * args.dw_tiles_x;
   const int m_blocks = kBlk ? (args.M / (args.Ho * args.Wo)) * dw_blocks_per_img
@@ -714,7 +877,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
         // one arrival per warp of the owning teams (pairs: of both CTAs' teams)
-        ptx::mbar_init(&tmem_empty[b], 4 * (args.teams > n_acc ? args.teams / n_acc : 1) * (kPair ? 2 : 1));
+        ptx::mbar_init(&tmem_empty[b], (kPD ? 8 : 4 * (args.teams > n_acc ? args.teams / n_acc : 1)) *
+                                           (kPair ? 2 : 1));
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
@@ -751,7 +915,26 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // critical path of the first tile's loads and MMAs.
     for (int i = threadIdx.x; i < cout_pad; i += epi_warps * 32)
       bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
+    if constexpr (kPD) {  // zero the halo buffers once: their borders are the padding
+      for (int i = threadIdx.x; i < 2 * kPdHaloBytes / 16; i += epi_warps * 32)
+        ptx::sts128(ptx::smem_u32(smem + L.y_off) + i * 16, make_uint4(0, 0, 0, 0));
+      // depthwise weights [9][Cout] and bias [Cout] after the layout
+      const uint32_t dwp = ptx::smem_u32(smem + L.total);
+      for (int i = threadIdx.x; i < 9 * args.Cout / 8; i += epi_warps * 32)
+        ptx::sts128(dwp + i * 16, __ldg(reinterpret_cast<const uint4*>(args.dw_w) + i));
+      for (int i = threadIdx.x; i < args.Cout / 4; i += epi_warps * 32) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(args.dw_b) + i);
+        ptx::sts128(dwp + 9 * args.Cout * 2 + i * 16,
+                    make_uint4(__float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z),
+                               __float_as_uint(b.w)));
+      }
+    }
     asm volatile("bar.sync 1, %0;" ::"r"(epi_warps * 32) : "memory");
+    if constexpr (kPD) {
+      pwdw_epilogue(args, smem + L.y_off, ptx::smem_u32(smem + L.total), bias_s, tmem_base, acc_stride,
+                    tmem_full, tmem_empty, n_acc,
+                    acc_log2, n_tiles, warp, lane);
+    } else {
     const int quarter = warp & 3;
     // teams per accumulator: with more teams than accumulators, tpa teams
     // share each tile, team t taking column part t % tpa
@@ -882,6 +1065,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (args.ts && quarter == 0 && lane == 0 && j < 8) ts_mark(args.ts, 32 + j, ts0);
     }
     if (lane == 0) ptx::bulk_wait<0>();
+    }  // (not kPD)
   } else if (warp < kGatherWarp0) {
     // (with a single epilogue team, warps 4-7 have no role)
   } else if (warp < kGatherWarp0 + kGatherWarps) {
@@ -1106,8 +1290,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (tw.rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * tx);
             ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                                   kb * kConvBK, n0 + tw.rank * (args.BN / 2));
-            ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.a_off + s * a_stage), &args.tmap_a, &full[s],
-                                  kb * kConvBK, m0);
+            for (int q = 0; q < mt; ++q)
+              ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes), &args.tmap_a,
+                                    &full[s], kb * kConvBK, m0 + q * kConvBM);
             continue;
           }
           ptx::mbar_arrive_expect_tx(&full[s], tx - (kDw ? 1u : 0u));
@@ -1353,6 +1538,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // the K block's four K=16 steps (+32 B in the swizzle row each), per sub-tile
           if constexpr (kPair) {
             ptx::umma_bf16_pair_k64(d, da, db, idesc, kb != 0);
+            if (mt == 2)  // (kPairPwDw: both CTAs' second image sub-tile)
+              ptx::umma_bf16_pair_k64(d + args.BN, da + (kABytes >> 4), db, idesc, kb != 0);
             ptx::umma_commit_pair_warp(&empty[s], 3);  // both CTAs' slots
             continue;
           }
@@ -1522,6 +1709,16 @@ size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_r
   return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt).total + 1024;  // + alignment slack
 }
 
+bool conv_gemm_pwdw_ok(int ho, int wo, int cout, int bn, int dw_stride) {
+  // whole image per tile (<= 2 sub-tiles, halo <= 16 x 16), 64-channel
+  // rounds, two accumulators for the two epilogue teams
+  const int acc_cols = static_cast<int>(pow2_at_least(((ho * wo + kConvBM - 1) / kConvBM) * bn));
+  const int wd = (wo - 1) / dw_stride + 1;  // depthwise output width: strips of kPdQ
+  return ho * wo <= 2 * kConvBM && (ho + 2) * (wo + 2) * 128 <= kPdHaloBytes && bn % 64 == 0 &&
+         wd % kPdQ == 0 &&
+         bn <= 256 && cout % bn == 0 && 512 / acc_cols >= 2 && (dw_stride == 1 || dw_stride == 2);
+}
+
 bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
                        int& box_bytes) {
   if (c < 32 || (c & (c - 1)) != 0 || (stride != 1 && stride != 2)) return false;
@@ -1628,6 +1825,12 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -1646,9 +1849,13 @@ int conv_gemm_sm_count() {
 cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cudaStream_t stream) {
   // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
   ConvGemmArgs args = in_args;
-  const bool pair = mode == ConvLoadMode::kPairTmaA;
+  const bool pair = mode == ConvLoadMode::kPairTmaA || mode == ConvLoadMode::kPairPwDw;
+  const bool pd = mode == ConvLoadMode::kPwDw || mode == ConvLoadMode::kPairPwDw;
+  if (pd && !conv_gemm_pwdw_ok(args.Ho, args.Wo, args.Cout, args.BN, args.dw_stride))
+    return cudaErrorInvalidValue;
   if (pair) {
     // CTA pairs: each CTA's B half is BN / 2 rows of 128 B swizzle atoms
+    // (kPairPwDw: each CTA of the pair takes its own image)
     if (args.BN % 16 != 0 || args.BN > 256) return cudaErrorInvalidValue;
     args.cluster = 2;
   }
@@ -1672,6 +1879,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.mt = 1;
   while (args.mt * 2 <= mt_cap && args.mt * 2 * static_cast<int>(pow2_at_least(args.BN)) <= 256)
     args.mt *= 2;
+  if (pd) args.mt = (args.Ho * args.Wo + kConvBM - 1) / kConvBM;  // one image per tile
   // TMEM: as many accumulators as 512 columns hold (2..kMaxAcc), so the MMA
   // runs ahead of the epilogue; epilogue teams: 2, or 4 when the gather warps
   // are idle (TMA-A) and tiles are single small ones, never more than the
@@ -1682,6 +1890,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.teams = std::min((mode == ConvLoadMode::kTmaA || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
   if (args.teams == 3) args.teams = 2;  // a power of two
+  if (pd) args.teams = 4;  // sixteen epilogue warps = two teams of eight (pwdw_epilogue)
   // wide TMA-A tiles with two accumulators: the idle gather warps join and
   // two teams split each tile's columns (DS_CONV_TPA=0: off)
   static const int res_prefetch = [] {  // bring-up A/B: 0 none, 1 this tile, 2 a tile ahead
@@ -1761,29 +1970,44 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return cudaErrorInvalidValue;
   }
   const int bres2 = args.b_res;
+  // kPwDw: the depthwise weights and bias sit after the layout
+  const size_t pd_extra = pd ? static_cast<size_t>(args.Cout) * (9 * 2 + 4) : 0;
+  if (pd) {
+    const int bn_s = pair ? args.BN / 2 : args.BN;  // B rows staged per CTA
+    const int per_stage = args.mt * kABytes + (bres > 0 ? 0 : bn_s * kConvBK * 2);
+    const int fixed = static_cast<int>(smem_layout(bn_s, 0, args.Cout, 16, bres, args.mt).total +
+                                       pd_extra) + 64 * 8 + 1024;
+    args.stages = std::min(kConvMaxStages, (227 * 1024 - fixed) / per_stage);
+    if (args.stages < 2) return cudaErrorInvalidValue;
+  }
   const size_t smem =
       dw ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres, 1, box).total + 1024
       : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
                           static_cast<int>(args.win_box_bytes)).total + 1024
             : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
-                                   bres, args.mt);
+                                   bres, args.mt) +
+              pd_extra;
   const bool blk = dw || win || mode == ConvLoadMode::kS2D;
   const int tiles =
-      blk ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
-                : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
+      blk  ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
+      : pd ? n_tiles * (args.M / (args.Ho * args.Wo))
+           : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
   const int per_sm = std::max(1, std::min(by_smem, by_tmem));
   if (args.cluster > 1) {  // pairs of CTAs over (M-block pair, N block) units
     if ((mode != ConvLoadMode::kTmaA && !pair) || args.b_res > 0 || args.cluster != 2 ||
-        (pair && args.mt != 1))
+        (pair && !pd && args.mt != 1))
       return cudaErrorInvalidValue;
-    const int m_blocks = (args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt);
+    const int m_blocks = pd ? args.M / (args.Ho * args.Wo)  // (images)
+                            : (args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt);
     const int units = n_tiles * ((m_blocks + 1) / 2);
     const int ctas = std::min(2 * units, conv_gemm_sm_count() * per_sm) / 2 * 2;
-    return launch_pdl_cluster(pair ? conv_gemm_kernel<7> : conv_gemm_kernel<2>, dim3(ctas),
-                              dim3(kConvThreads), smem, stream, 2, args);
+    return launch_pdl_cluster(mode == ConvLoadMode::kPairPwDw ? conv_gemm_kernel<9>
+                              : pair                          ? conv_gemm_kernel<7>
+                                                              : conv_gemm_kernel<2>,
+                              dim3(ctas), dim3(kConvThreads), smem, stream, 2, args);
   }
   args.cluster = 1;
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
@@ -1803,6 +2027,10 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     case ConvLoadMode::kS2D:
       return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kPairTmaA:
+      break;  // (launched above)
+    case ConvLoadMode::kPwDw:
+      return launch_pdl(conv_gemm_kernel<8>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kPairPwDw:
       break;  // (launched above)
   }
   return cudaGetLastError();

@@ -97,7 +97,14 @@ enum class ConvLoadMode : int {
                   // producer warps (A arrives in the MMA's 32 B-swizzled layout)
   kPairTmaA = 7,  // kTmaA on CTA pairs: one M = 256 cta_group::2 MMA per K step, each CTA
                   // loading its 128 A rows and half of the B block (tmap_b box rows BN / 2)
+  kPwDw = 8,      // 1x1 conv + the following depthwise 3x3 (dw_w / dw_b / dw_stride): a
+                  // tile is one image x BN channels; y / ldy are the depthwise output
+  kPairPwDw = 9,  // kPwDw on CTA pairs (two images per pair MMA, B halves as kPairTmaA)
 };
+
+// Whether a 1x1 conv (ho x wo output, cout channels, N tile bn) and its
+// depthwise successor can run as one kPwDw launch.
+bool conv_gemm_pwdw_ok(int ho, int wo, int cout, int bn, int dw_stride);
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
 // elements) with a {64, box_rows} box and 128 B swizzle.

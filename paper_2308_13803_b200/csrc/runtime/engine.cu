@@ -182,12 +182,13 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
 
   plans_.resize(m.ops.size());
   fused_ = fused_depthwise(m);
+  absorbed_ = pwdw_absorbed(m);
   stem_ = fused_stem(m);
   kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (input or s2d staging +) softmax
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
-    if (!fused_[i]) ++kernels_per_forward_;
-    if (op.kind == OpKind::kDwConv && !fused_[i]) {
+    if (!fused_[i] && !absorbed_[i]) ++kernels_per_forward_;
+    if (op.kind == OpKind::kDwConv && !fused_[i] && !absorbed_[i]) {
       const BufferSpec& din = m.buffers.at(op.in);
       dw_maps_.resize(m.ops.size());
       dw_tma_.resize(m.ops.size(), false);
@@ -352,9 +353,27 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }
+    if (pl.mode == ConvLoadMode::kTmaA && i + 1 < m.ops.size() && absorbed_[i + 1]) {
+      // 1x1 conv + the following depthwise in one launch: a tile is one image
+      // x BN channels; the depthwise output is this launch's output
+      const OpSpec& dw = m.ops[i + 1];
+      const BufferSpec& dw_out = m.buffers.at(dw.out);
+      pl.mode = ConvLoadMode::kPwDw;
+      a.BN = pwdw_bn(p.cout);
+      a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
+      a.dw_b = d_b_ + hp.b_off.at(dw.param);
+      a.dw_stride = dw.sh;
+      a.y = bufs_[dw.out];
+      a.ldy = dw_out.c;
+      a.c_off = 0;
+    }
     // wide TMA-A layers: CTA pairs may multicast each weight block (opt-in)
     const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
     a.cluster = pl.mode == ConvLoadMode::kTmaA && a.BN == 256 && !b_resident && cluster_on() ? 2 : 1;
+    if (pl.mode == ConvLoadMode::kPwDw && pair_on(a.BN)) {
+      pl.mode = ConvLoadMode::kPairPwDw;  // two images per pair MMA, B halves
+      a.cluster = 2;
+    }
     if (pl.mode == ConvLoadMode::kTmaA && a.cluster == 1 && !b_resident && pair_on(a.BN)) {
       pl.mode = ConvLoadMode::kPairTmaA;
       a.cluster = 2;  // (tmap_b boxes of BN / 2 rows: each CTA's half)
@@ -366,7 +385,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                                     a.BN / a.cluster)) {
       throw CudaError("cuTensorMapEncodeTiled failed (weights)");
     }
-    if (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA) {
+    if (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA ||
+        pl.mode == ConvLoadMode::kPwDw || pl.mode == ConvLoadMode::kPairPwDw) {
       const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
       if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
         throw CudaError("cuTensorMapEncodeTiled failed (activations)");
@@ -377,7 +397,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       const size_t esz = out.f32 ? 4 : 2;
       void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
-      if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow ||
+      if (pl.mode == ConvLoadMode::kPwDw || pl.mode == ConvLoadMode::kPairPwDw)  // (direct stores)
+        a.y_tma = 0;
+      else if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow ||
           pl.mode == ConvLoadMode::kS2D)  // pixel-row boxes
         a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
                                                 a.dw_tw, a.dw_rw)
@@ -426,7 +448,7 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
     record_mark();
   }
   for (size_t i = 0; i < m.ops.size(); ++i) {
-    if (fused_[i]) continue;  // computed inside the next conv's producer
+    if (fused_[i] || absorbed_[i]) continue;  // computed inside a neighbouring conv
     const OpSpec& op = m.ops[i];
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out = m.buffers[op.out];

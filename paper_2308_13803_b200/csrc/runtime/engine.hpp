@@ -89,6 +89,7 @@ class Instance {
   std::vector<void*> bufs_;
   std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
   std::vector<bool> fused_;      // depthwise ops folded into the next conv
+  std::vector<bool> absorbed_;   // depthwise ops computed in the previous conv's epilogue (kPwDw)
   int stem_ = -1;                // stem conv reading the u8 images (kStemU8), or -1
   S2dPlan s2d_;                  // stride-2 stem over the space-to-depth input (kS2D)
   __nv_bfloat16* d_s2d_ = nullptr;     // [max_bs][hs][ws][16]

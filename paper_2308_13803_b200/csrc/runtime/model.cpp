@@ -338,6 +338,41 @@ std::vector<bool> fused_depthwise(const ModelSpec& m) {
   return fused;
 }
 
+int pwdw_bn(int cout) { return cout % 128 == 0 ? 128 : 64; }
+
+std::vector<bool> pwdw_absorbed(const ModelSpec& m) {
+  std::vector<bool> absorbed(m.ops.size(), false);
+  // Opt-in (DS_PWDW=1): bit-exact, but on B200 about break-even with the two
+  // launches — one image per tile wastes 23 % of the 14 x 14 maps' MMA rows
+  // (196 of 256), and the depthwise phase's shared-memory traffic slows the
+  // MMA side, which is already shared-memory-bound at N = 128.
+  const char* e = std::getenv("DS_PWDW");
+  if (!e || e[0] != '1') return absorbed;
+  const std::vector<bool> fused = fused_depthwise(m);
+  for (size_t i = 1; i < m.ops.size(); ++i) {
+    const OpSpec& pw = m.ops[i - 1];
+    const OpSpec& dw = m.ops[i];
+    if (dw.kind != OpKind::kDwConv || pw.kind != OpKind::kConv || dw.in != pw.out || fused[i]) continue;
+    if (i >= 2 && fused[i - 2]) continue;  // (the 1x1 already consumes a fused depthwise)
+    if (pw.r != 1 || pw.s != 1 || pw.sh != 1 || pw.sw != 1 || pw.ph != 0 || pw.pw != 0 ||
+        pw.residual >= 0 || pw.c_off != 0 || !pw.relu || !dw.relu || dw.ph != 1 || dw.sh != dw.sw)
+      continue;
+    const BufferSpec& mid = m.buffers[pw.out];
+    const BufferSpec& in = m.buffers[pw.in];
+    if (mid.f32 || in.c % 8 != 0 || m.buffers[dw.out].c != mid.c) continue;
+    bool other_reader = false;
+    for (size_t j = 0; j < m.ops.size(); ++j)
+      if (j != i && (m.ops[j].in == pw.out || m.ops[j].residual == pw.out)) other_reader = true;
+    const int cout = m.params[pw.param].cout;
+    // (maps of at most 128 pixels waste most of the 128-row MMA tile: the two
+    // launches are faster there)
+    if (!other_reader && cout == mid.c && cout % 64 == 0 && mid.h * mid.w > 128 &&
+        conv_gemm_pwdw_ok(mid.h, mid.w, cout, pwdw_bn(cout), dw.sh))
+      absorbed[i] = true;
+  }
+  return absorbed;
+}
+
 namespace {
 // The op that reads the staged input (buffer 0), when it is a conv and its only reader.
 int stem_op(const ModelSpec& m) {
@@ -396,6 +431,7 @@ int fused_stem(const ModelSpec& m) {
 
 std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
   const std::vector<bool> fused = fused_depthwise(m);
+  const std::vector<bool> absorbed = pwdw_absorbed(m);
   const int stem = fused_stem(m);
   const S2dPlan s2d = stem_s2d(m);
   std::vector<KernelCost> out;
@@ -453,6 +489,15 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
       k.flops_per_image += dw.flops_per_image;
       k.bytes_per_image += static_cast<double>(dw_in.h) * dw_in.w * dw_in.c * 2 - in_elems * 2;
       k.fixed_bytes += dw.fixed_bytes;
+    }
+    if (absorbed[i]) {
+      // one launch with the 1x1 before it: its output stays in shared memory
+      const KernelCost pw = out.back();
+      out.pop_back();
+      k.kind = KernelKind::kConvGemm;
+      k.flops_per_image += pw.flops_per_image;
+      k.bytes_per_image += pw.bytes_per_image - 2.0 * in_elems * 2;
+      k.fixed_bytes += pw.fixed_bytes;
     }
     out.push_back(k);
   }

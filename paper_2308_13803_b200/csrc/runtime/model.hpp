@@ -73,6 +73,14 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m);
 // correct (parity-tested) but its producer is still latency-bound.
 std::vector<bool> fused_depthwise(const ModelSpec& m);
 
+// Depthwise ops computed in the epilogue of the 1x1 conv before them (conv_gemm
+// kPwDw: one whole image x 128 or 64 channels per tile, the 1x1 output kept in
+// shared memory): true for op i when op i is a depthwise 3x3 whose input is
+// the output of op i-1, a 1x1 stride-1 conv read by nothing else, on maps of
+// at most 14 x 14 and more than 128 pixels. Opt-in: DS_PWDW=1. pwdw_bn: the conv's N tile.
+std::vector<bool> pwdw_absorbed(const ModelSpec& m);
+int pwdw_bn(int cout);
+
 // Index of the stem conv when it reads the u8 images directly (ConvLoadMode
 // kStemU8: staging fused into its producer), -1 when the staged bf16 input is
 // used (DS_STEM_STAGED=1, or buffer 0 has another reader).

@@ -205,3 +205,27 @@ def test_pair_mma_matches_single_cta(monkeypatch, model, bs):
         single = be.forward(imgs)
     assert np.isfinite(pair).all()
     assert np.array_equal(pair, single)
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("bs", [1, 3, 6])
+def test_pwdw_fusion_matches_two_kernels(monkeypatch, bs, pair):
+    """1x1 conv + depthwise in one launch on the 14 x 14 maps (kPwDw: a tile
+    is one image x 128 channels, the 1x1 output rounded to bf16 into a
+    shared-memory halo buffer, the depthwise in strips with the standalone
+    kernels' per-output fma order; stride 1 and the stride-2 14 -> 7 layer)
+    against the two launches: bit-identical logits, and six launches fewer
+    per MobileNet forward. pair=1: kPairPwDw, two images per cta_group::2
+    MMA (odd batches leave the last pair's second CTA without an image)."""
+    imgs = generate_images("mobilenet_v1", 23, bs)
+    monkeypatch.setenv("DS_CONV_PAIR", pair)
+    monkeypatch.setenv("DS_PWDW", "1")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        fused = be.forward(imgs)
+        k_fused = be.stats()["kernels_per_forward"]
+    monkeypatch.setenv("DS_PWDW", "0")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        plain = be.forward(imgs)
+        k_plain = be.stats()["kernels_per_forward"]
+    assert np.array_equal(fused, plain)
+    assert k_plain - k_fused == 6

@@ -64,11 +64,26 @@ static int run(const Case& cs) {
   ConvGemmArgs a{};
   a.cluster = getenv("CLUSTER") ? atoi(getenv("CLUSTER")) : 1;  // 2: CTA pairs multicast B
   ConvLoadMode mode = cs.mode;
+  const bool pd = getenv("PWDW") && mode == ConvLoadMode::kTmaA;  // + depthwise epilogue (timing only)
+  if (pd) {
+    mode = ConvLoadMode::kPwDw;
+    a.BN = cs.Cout % 128 == 0 ? 128 : 64;
+    a.dw_stride = 1;
+    __nv_bfloat16* dww;
+    float* dwb;
+    cudaMalloc(&dww, 9 * cs.Cout * 2);
+    cudaMalloc(&dwb, cs.Cout * 4);
+    cudaMemset(dww, 0, 9 * cs.Cout * 2);
+    cudaMemset(dwb, 0, cs.Cout * 4);
+    a.dw_w = dww;
+    a.dw_b = dwb;
+  }
   if (getenv("PAIR") && mode == ConvLoadMode::kTmaA) {  // cta_group::2 pair MMAs
     mode = ConvLoadMode::kPairTmaA;
     a.cluster = 2;
   }
-  if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad, cs.BN / a.cluster)) {
+  if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad,
+                           (getenv("PWDW") ? (cs.Cout % 128 == 0 ? 128 : 64) : cs.BN) / a.cluster)) {
     printf("%s: tmap_b encode failed\n", cs.name);
     return 1;
   }
@@ -80,7 +95,7 @@ static int run(const Case& cs) {
   a.x = dx; a.H = cs.H; a.W = cs.W; a.C = cs.C; a.R = cs.R; a.S = cs.S;
   a.stride_h = cs.sh; a.stride_w = cs.sw; a.pad_h = cs.ph; a.pad_w = cs.pw;
   a.Ho = Ho; a.Wo = Wo; a.M = M; a.num_kb = Kpad / 64; a.taps = cs.R * cs.S;
-  a.Cout = cs.Cout; a.BN = cs.BN;
+  a.Cout = cs.Cout; a.BN = getenv("PWDW") ? (cs.Cout % 128 == 0 ? 128 : 64) : cs.BN;
   a.stages = conv_gemm_stages(cs.BN, cs.Cout);
   a.tmem_cols = conv_gemm_tmem_cols(cs.BN);
   a.y_tma = encode_tmap_out(&a.tmap_y, static_cast<uint8_t*>(dy) + cs.c_off * (cs.f32 ? 4 : 2), M,
@@ -141,12 +156,17 @@ static int run(const Case& cs) {
       snprintf(nm, sizeof nm, "tile%d MMA first", j); stat(8 + j, nm);
       snprintf(nm, sizeof nm, "tile%d MMA commit", j); stat(16 + j, nm);
       snprintf(nm, sizeof nm, "tile%d epi start", j); stat(24 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d halo0 done", j); stat(48 + j, nm);
       snprintf(nm, sizeof nm, "tile%d epi end", j); stat(32 + j, nm);
     }
     stat(2, "MMA loop done");
     stat(3, "exit barrier");
   }
 
+  if (pd) {
+    printf("%-28s pwdw: %.3f us\n", cs.name, ms * 1e3);
+    return 0;
+  }
   std::vector<uint8_t> hy(ybytes);
   cudaMemcpy(hy.data(), dy, ybytes, cudaMemcpyDeviceToHost);
   double max_err = 0, max_ref = 0;
