@@ -803,14 +803,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D);
   constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
   // (kWindow's A operands live in the halo boxes: its ring stages carry B only)
+  // (kS2D ring stages are sized for two sub-tiles: a halo box of a 64-row
+  // block is still under 32 KiB)
   const SmemLayout L = smem_layout(kPair ? args.BN / 2 : args.BN, args.stages, args.Cout, epi_warps, args.b_res,
-                                   kWin ? 1 : args.mt,
+                                   kWin ? 1 : kS2 ? 2 : args.mt,
                                    kDw ? static_cast<int>(args.dw_box_bytes) : 0,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0);
   const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   const uint32_t box_stride = (args.dw_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
-  const uint32_t a_stage = static_cast<uint32_t>(mt) * kABytes;
+  const uint32_t a_stage = static_cast<uint32_t>(kS2 ? 2 : mt) * kABytes;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
@@ -1334,10 +1336,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t box = ptx::smem_u32(smem + L.a_off + s * a_stage);
           const uint32_t sbo = static_cast<uint32_t>(args.win_iw) * 32;
           const uint32_t b_base = ptx::smem_u32(smem + L.b_off);
-          // 2x2 / 4x4 taps (3x3 / 7x7 stems) with two sub-tiles: fully
-          // unrolled, every descriptor a compile-time offset (uniform issue)
-          auto unrolled = [&](auto dr_c, auto ds_c) {
+          // 2x2 / 4x4 taps (3x3 / 7x7 stems) with two or four sub-tiles:
+          // fully unrolled, every descriptor a compile-time offset (uniform issue)
+          auto unrolled = [&](auto dr_c, auto ds_c, auto mt_c) {
             constexpr int DR = decltype(dr_c)::value, DS = decltype(ds_c)::value;
+            constexpr int MT = decltype(mt_c)::value;
             constexpr int IW = 8 + DS - 1;
             const uint64_t da0 = ptx::umma_desc_sw32_kmajor_sbo(box, IW * 32);
             const uint64_t db0 = ptx::umma_desc_sw128_kmajor(b_base);
@@ -1345,17 +1348,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
             for (int t = 0; t < DR * DS; ++t)
 #pragma unroll
-              for (int q = 0; q < 2; ++q)
+              for (int q = 0; q < MT; ++q)
                 ptx::umma_bf16_warp(d + q * args.BN,
                                     da0 + static_cast<uint64_t>(((16 * q + t / DS) * IW + t % DS) * 2),
                                     db0 + static_cast<uint64_t>(t >> 2) * bstep + 2 * (t & 3), idesc,
                                     t != 0);
           };
-          const bool fast = mt == 2 && !(args.debug_flags & 16);
-          if (fast && args.R == 2 && args.S == 2)
-            unrolled(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{});
-          else if (fast && args.R == 4 && args.S == 4)
-            unrolled(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+          const bool fast = (mt == 2 || mt == 4) && !(args.debug_flags & 16);
+          using I2 = std::integral_constant<int, 2>;
+          using I4 = std::integral_constant<int, 4>;
+          if (fast && args.R == 2 && args.S == 2) {
+            if (mt == 2) unrolled(I2{}, I2{}, I2{});
+            else unrolled(I2{}, I2{}, I4{});
+          } else if (fast && args.R == 4 && args.S == 4) {
+            if (mt == 2) unrolled(I4{}, I4{}, I2{});
+            else unrolled(I4{}, I4{}, I4{});
+          }
           for (int t = 0, dr = 0, dc = 0;
                t < ((fast && args.R == args.S && (args.R == 2 || args.R == 4)) ? 0 : taps) &&
                !(args.debug_flags & 16);
@@ -1872,7 +1880,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   static const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
                    teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
   const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
-                     : mode == ConvLoadMode::kS2D ? 2
+                     : mode == ConvLoadMode::kS2D ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
                      : mode == ConvLoadMode::kStemU8 ? mt_stem
                      : mode == ConvLoadMode::kTmaA ? mt_tma
                                                    : 1;
@@ -1948,14 +1956,17 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     }
   }
   if (mode == ConvLoadMode::kS2D) {
-    // 16 x 16 pixel blocks = two 128-row sub-tiles; all weights resident
-    args.mt = 2;
+    // pixel blocks of dw_th x 8 (halo box) or 16 x 16 (tap boxes) = dw_th / 16
+    // 128-row sub-tiles; all weights resident
+    args.mt = args.win_iw > 0 ? args.dw_th / 16 : 2;
+    if (args.mt != 2 && args.mt != 4) return cudaErrorInvalidValue;
     if (!args.y_tma || n_tiles != 1 || args.num_kb * args.BN * 128 > 64 * 1024)
       return cudaErrorInvalidValue;
     args.b_res = args.num_kb;
     // no producer warps: all sixteen non-TMA/MMA warps drain accumulators
     // (four epilogue teams) when their staging still leaves a 2-deep ring
     if (args.n_acc >= 4 && conv_gemm_stages(args.BN, args.Cout, 16, args.b_res, 2) >= 2) args.teams = 4;
+    if (args.win_box_bytes > 2u * kABytes) return cudaErrorInvalidValue;  // (ring stage = 2 sub-tiles)
     args.stages = std::min(6, conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, args.b_res, 2));
     if (args.stages < 2) return cudaErrorInvalidValue;
   }
@@ -1985,7 +1996,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
                           static_cast<int>(args.win_box_bytes)).total + 1024
             : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
-                                   bres, args.mt) +
+                                   bres, mode == ConvLoadMode::kS2D ? 2 : args.mt) +
               pd_extra;
   const bool blk = dw || win || mode == ConvLoadMode::kS2D;
   const int tiles =

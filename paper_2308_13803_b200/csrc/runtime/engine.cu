@@ -303,21 +303,24 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, 16))
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem boxes)");
     } else if (static_cast<int>(i) == s2d_.op) {
-      // the same, with one halo box per 32 x 8 block: every tap is a window of
-      // it (8-pixel rows = the MMA's 8-row groups, SBO = box row pitch)
+      // the same, with one halo box per dw_th x 8 block: every tap is a window
+      // of it (8-pixel rows = the MMA's 8-row groups, SBO = box row pitch);
+      // 64-row blocks (four sub-tiles per tile) for the narrow stems, whose
+      // epilogue is bound by per-tile work (DS_S2D_ROWS=32|64 overrides)
       pl.mode = ConvLoadMode::kS2D;
       a.R = s2d_.dr;
       a.S = s2d_.ds;
       a.C = 16;
       a.taps = s2d_.dr * s2d_.ds;
       a.num_kb = s2d_.kpad / kConvBK;
-      a.dw_th = 32;
+      const char* rows_env = std::getenv("DS_S2D_ROWS");
+      a.dw_th = rows_env ? (std::atoi(rows_env) == 64 ? 64 : 32) : (p.cout <= 32 ? 64 : 32);
       a.dw_tw = 8;
       a.dw_rw = 4;
-      a.dw_tiles_y = (out.h + 31) / 32;
+      a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
       a.dw_tiles_x = (out.w + 7) / 8;
       a.win_iw = 8 + a.S - 1;
-      a.win_ih = 32 + a.R - 1;
+      a.win_ih = a.dw_th + a.R - 1;
       a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * 32);
       if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, a.win_iw,
                                  a.win_ih))
