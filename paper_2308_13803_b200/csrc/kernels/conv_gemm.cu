@@ -1877,7 +1877,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const char* e = std::getenv(name);
     return e ? std::max(1, std::min(4, std::atoi(e))) : dflt;
   };
-  static const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
+  const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
                    teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
   const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
                      : mode == ConvLoadMode::kS2D ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
@@ -1901,12 +1901,12 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   if (pd) args.teams = 4;  // sixteen epilogue warps = two teams of eight (pwdw_epilogue)
   // wide TMA-A tiles with two accumulators: the idle gather warps join and
   // two teams split each tile's columns (DS_CONV_TPA=0: off)
-  static const int res_prefetch = [] {  // bring-up A/B: 0 none, 1 this tile, 2 a tile ahead
+  const int res_prefetch = [] {  // bring-up A/B: 0 none, 1 this tile, 2 a tile ahead
     const char* e = std::getenv("DS_RES_PREFETCH");
     return e ? std::atoi(e) : 1;
   }();
   args.res_prefetch = res_prefetch;
-  static const bool tpa_on = [] {
+  const bool tpa_on = [] {
     const char* e = std::getenv("DS_CONV_TPA");
     return !(e && e[0] == '0');
   }();
@@ -1916,7 +1916,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
-  static const bool b_res_on = [] {
+  const bool b_res_on = [] {
     const char* e = std::getenv("DS_B_RESIDENT");
     return !(e && e[0] == '0');
   }();

@@ -240,7 +240,7 @@ int sm_count() {
 
 // (bring-up knob: DS_DW14_ROWS overrides the 14x14 tile height)
 int dw14_rows() {
-  static const int r = [] {
+  const int r = [] {
     const char* e = std::getenv("DS_DW14_ROWS");
     return e ? std::max(1, std::atoi(e)) : 14;
   }();

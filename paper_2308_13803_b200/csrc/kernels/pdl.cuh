@@ -15,7 +15,7 @@
 namespace ds {
 
 inline bool pdl_enabled() {
-  static const bool on = [] {
+  const bool on = [] {
     const char* e = std::getenv("DS_PDL");
     return !(e && e[0] == '0');
   }();

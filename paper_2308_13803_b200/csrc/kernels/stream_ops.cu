@@ -8,6 +8,7 @@
 #include "pdl.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace ds {
 
@@ -253,6 +254,69 @@ __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ 
   y[opix * ldo_g + coff_g + g] = pack8(acc);
 }
 
+// 3x3 pooling, register-blocked: grid.y = output row (image, oy); a thread
+// owns one 8-channel group g of kPoolCols consecutive output columns, so each
+// loaded input vector serves up to three outputs; 32-bit index arithmetic.
+// Per output the taps are visited in the same order as pool3x3_kernel (row
+// outer, column inner, padding skipped) and averages divide the sum by 9, so
+// results are bit-identical to it (DS_POOL_LEGACY=1 selects the old kernel).
+template <int STRIDE, int kPoolCols>
+__global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
+                                    int cg, int ho, int wo, int pad, int is_max, int ldo_g, int coff_g,
+                                    int xq_per_row) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int xq = i / cg;
+  if (xq >= xq_per_row) return;
+  const int g = i - xq * cg;
+  const int row = blockIdx.y;
+  const int n = row / ho;
+  const int oy = row - n * ho;
+  const int ox0 = xq * kPoolCols;
+  constexpr int IN = (kPoolCols - 1) * STRIDE + 3;
+  const int ix0 = ox0 * STRIDE - pad;
+  float acc[kPoolCols][8];
+#pragma unroll
+  for (int q = 0; q < kPoolCols; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[q][e] = is_max ? -INFINITY : 0.0f;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int iy = oy * STRIDE - pad + r;
+    if (iy < 0 || iy >= h) continue;
+    const uint4* xrow = x + (static_cast<long long>(n) * h + iy) * w * cg + g;
+#pragma unroll
+    for (int u = 0; u < IN; ++u) {
+      const int ix = ix0 + u;
+      if (ix < 0 || ix >= w) continue;
+      float xv[8];
+      unpack8(__ldg(xrow + static_cast<long long>(ix) * cg), xv);
+      // outputs q with q * STRIDE + s == u (taps s ascending, as in the
+      // per-output order)
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if ((u - s) < 0 || (u - s) % STRIDE != 0) continue;
+        const int q = (u - s) / STRIDE;
+        if (q >= kPoolCols) continue;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          acc[q][e] = is_max ? fmaxf(acc[q][e], xv[e]) : acc[q][e] + xv[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kPoolCols; ++q) {
+    if (ox0 + q >= wo) break;
+    if (!is_max) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[q][e] = acc[q][e] / 9.0f;
+    }
+    const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox0 + q;
+    y[opix * ldo_g + coff_g + g] = pack8(acc[q]);
+  }
+}
+
 // Global average pool: four threads (adjacent lanes) per (image, 8-channel
 // group), each summing every 4th pixel with all its loads in flight; the four
 // partial sums combine in a fixed order (p0+p1)+(p2+p3), so results are
@@ -398,6 +462,29 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
                            cudaStream_t stream) {
   const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
   const int cg = c / 8;
+  const bool legacy = [] {
+    const char* e = std::getenv("DS_POOL_LEGACY");
+    return e && e[0] == '1';
+  }();
+  const int rows = n * ho;
+  const char* cols_env = std::getenv("DS_POOL_COLS");  // bring-up A/B: 1, 2 or 4
+  const int cols = cols_env ? std::atoi(cols_env) : 1;
+  if (!legacy && rows <= 65535 && (stride == 1 || stride == 2) && (cols == 1 || cols == 2 || cols == 4)) {
+    const int xq = (wo + cols - 1) / cols;
+    const int per_row = xq * cg;
+    const int bt = std::min(kBlock, (per_row + 31) / 32 * 32);
+    const dim3 grid((per_row + bt - 1) / bt, rows);
+    auto go = [&](auto kernel) {
+      return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
+                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, is_max ? 1 : 0, ldo / 8,
+                        c_off / 8, xq);
+    };
+    if (stride == 1)
+      return cols == 1 ? go(pool3x3_rows_kernel<1, 1>) : cols == 2 ? go(pool3x3_rows_kernel<1, 2>)
+                                                         : go(pool3x3_rows_kernel<1, 4>);
+    return cols == 1 ? go(pool3x3_rows_kernel<2, 1>) : cols == 2 ? go(pool3x3_rows_kernel<2, 2>)
+                                                       : go(pool3x3_rows_kernel<2, 4>);
+  }
   const long long work = static_cast<long long>(n) * ho * wo * cg;
   return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
                     reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho,

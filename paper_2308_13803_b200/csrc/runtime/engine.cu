@@ -40,7 +40,7 @@ uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 // 32 x 8 block, transposed by the gather warps) instead of kS2D (one TMA box
 // per tap in the MMA's layout, no producer warps; faster on B200). A/B switch.
 bool s2d_window() {
-  static const bool on = [] {
+  const bool on = [] {
     const char* e = std::getenv("DS_STEM_S2D_MODE");
     return e && std::string(e) == "window";
   }();
@@ -52,7 +52,7 @@ bool s2d_window() {
 // CTAs' near-simultaneous reads of a block; these layers are bound by shared-
 // memory traffic per MMA at 128 x 256 tiles, which 2-SM MMAs would halve).
 bool cluster_on() {
-  static const bool on = [] {
+  const bool on = [] {
     const char* e = std::getenv("DS_CONV_CLUSTER");
     return e && e[0] == '1';
   }();
@@ -64,7 +64,7 @@ bool cluster_on() {
 // block (a third less shared-memory traffic per MMA at 128 x 256 tiles).
 // 1 (default): BN >= 128; 0: off.
 bool pair_on(int bn) {
-  static const int m = [] {
+  const int m = [] {
     const char* e = std::getenv("DS_CONV_PAIR");
     return e ? std::atoi(e) : 1;
   }();
@@ -76,7 +76,7 @@ bool pair_on(int bn) {
 // fraction of the TMA bytes, and with the taps unrolled the issue loop runs
 // at the tensor pipe's pace). A/B switch.
 bool s2d_tap_boxes() {
-  static const bool on = [] {
+  const bool on = [] {
     const char* e = std::getenv("DS_STEM_S2D_MODE");
     return e && std::string(e) == "tap";
   }();
@@ -90,7 +90,7 @@ bool s2d_tap_boxes() {
 // transposed (C % 64 != 0) boxes the im2col gather is still faster.
 // DS_CONV_WINDOW=1: every eligible conv; DS_CONV_WINDOW=0: none (A/B).
 int window_mode() {
-  static const int m = [] {
+  const int m = [] {
     const char* e = std::getenv("DS_CONV_WINDOW");
     return e ? (e[0] == '1' ? 1 : 0) : 2;
   }();
