@@ -254,66 +254,92 @@ __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ 
   y[opix * ldo_g + coff_g + g] = pack8(acc);
 }
 
-// 3x3 pooling, register-blocked: grid.y = output row (image, oy); a thread
-// owns one 8-channel group g of kPoolCols consecutive output columns, so each
-// loaded input vector serves up to three outputs; 32-bit index arithmetic.
-// Per output the taps are visited in the same order as pool3x3_kernel (row
-// outer, column inner, padding skipped) and averages divide the sum by 9, so
-// results are bit-identical to it (DS_POOL_LEGACY=1 selects the old kernel).
-template <int STRIDE, int kPoolCols>
+// 3x3 pooling on a 2-D grid: grid.y = output row (image, oy), x = (output
+// column, 8-channel group); 32-bit index arithmetic (the column / group split
+// through an exact float-reciprocal division). Max pooling compares the
+// packed bf16 pairs directly (max is exact in any precision); average pooling
+// accumulates with fma.rn.f32.bf16(x, 1.0, acc) == acc + float(x), one
+// instruction per element. Per output the taps are visited in the same order
+// as pool3x3_kernel (row outer, column inner, padding skipped) and averages
+// divide the fp32 sum by 9, so results are bit-identical to it
+// (DS_POOL_LEGACY=1 selects the old kernel).
+__device__ __forceinline__ float add_bf16_lo(uint32_t x, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, one;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b16 one, 0x3F80;\n\t"
+      "fma.rn.f32.bf16 %0, xl, one, %2;}"
+      : "=f"(d)
+      : "r"(x), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ float add_bf16_hi(uint32_t x, float c) {
+  float d;
+  asm("{.reg .b16 xl, xh, one;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "mov.b16 one, 0x3F80;\n\t"
+      "fma.rn.f32.bf16 %0, xh, one, %2;}"
+      : "=f"(d)
+      : "r"(x), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t max_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+template <int STRIDE, bool IS_MAX>
 __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
-                                    int cg, int ho, int wo, int pad, int is_max, int ldo_g, int coff_g,
-                                    int xq_per_row) {
+                                    int cg, int ho, int wo, int pad, int ldo_g, int coff_g) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int xq = i / cg;
-  if (xq >= xq_per_row) return;
-  const int g = i - xq * cg;
+  int ox = __float2int_rz(__int2float_rz(i) * (1.0f / static_cast<float>(cg)));
+  if (ox * cg > i) --ox;
+  if ((ox + 1) * cg <= i) ++ox;
+  if (ox >= wo) return;
+  const int g = i - ox * cg;
   const int row = blockIdx.y;
   const int n = row / ho;
   const int oy = row - n * ho;
-  const int ox0 = xq * kPoolCols;
-  constexpr int IN = (kPoolCols - 1) * STRIDE + 3;
-  const int ix0 = ox0 * STRIDE - pad;
-  float acc[kPoolCols][8];
-#pragma unroll
-  for (int q = 0; q < kPoolCols; ++q)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[q][e] = is_max ? -INFINITY : 0.0f;
+  const int iy0 = oy * STRIDE - pad, ix0 = ox * STRIDE - pad;
+  uint4 mx = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // bf16 -inf pairs
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const int iy = oy * STRIDE - pad + r;
+    const int iy = iy0 + r;
     if (iy < 0 || iy >= h) continue;
     const uint4* xrow = x + (static_cast<long long>(n) * h + iy) * w * cg + g;
 #pragma unroll
-    for (int u = 0; u < IN; ++u) {
-      const int ix = ix0 + u;
+    for (int s = 0; s < 3; ++s) {
+      const int ix = ix0 + s;
       if (ix < 0 || ix >= w) continue;
-      float xv[8];
-      unpack8(__ldg(xrow + static_cast<long long>(ix) * cg), xv);
-      // outputs q with q * STRIDE + s == u (taps s ascending, as in the
-      // per-output order)
+      const uint4 v = __ldg(xrow + ix * cg);
+      if constexpr (IS_MAX) {
+        mx.x = max_bf16x2(mx.x, v.x);
+        mx.y = max_bf16x2(mx.y, v.y);
+        mx.z = max_bf16x2(mx.z, v.z);
+        mx.w = max_bf16x2(mx.w, v.w);
+      } else {
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        if ((u - s) < 0 || (u - s) % STRIDE != 0) continue;
-        const int q = (u - s) / STRIDE;
-        if (q >= kPoolCols) continue;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          acc[q][e] = is_max ? fmaxf(acc[q][e], xv[e]) : acc[q][e] + xv[e];
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] = add_bf16_lo(vw[k], acc[2 * k]);
+          acc[2 * k + 1] = add_bf16_hi(vw[k], acc[2 * k + 1]);
+        }
       }
     }
   }
+  const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox;
+  if constexpr (IS_MAX) {
+    y[opix * ldo_g + coff_g + g] = mx;
+  } else {
 #pragma unroll
-  for (int q = 0; q < kPoolCols; ++q) {
-    if (ox0 + q >= wo) break;
-    if (!is_max) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[q][e] = acc[q][e] / 9.0f;
-    }
-    const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox0 + q;
-    y[opix * ldo_g + coff_g + g] = pack8(acc[q]);
+    for (int e = 0; e < 8; ++e) acc[e] = acc[e] / 9.0f;
+    y[opix * ldo_g + coff_g + g] = pack8(acc);
   }
 }
 
@@ -467,23 +493,16 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
     return e && e[0] == '1';
   }();
   const int rows = n * ho;
-  const char* cols_env = std::getenv("DS_POOL_COLS");  // bring-up A/B: 1, 2 or 4
-  const int cols = cols_env ? std::atoi(cols_env) : 1;
-  if (!legacy && rows <= 65535 && (stride == 1 || stride == 2) && (cols == 1 || cols == 2 || cols == 4)) {
-    const int xq = (wo + cols - 1) / cols;
-    const int per_row = xq * cg;
+  if (!legacy && rows <= 65535 && (stride == 1 || stride == 2) && wo * cg < (1 << 24)) {
+    const int per_row = wo * cg;
     const int bt = std::min(kBlock, (per_row + 31) / 32 * 32);
     const dim3 grid((per_row + bt - 1) / bt, rows);
     auto go = [&](auto kernel) {
       return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
-                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, is_max ? 1 : 0, ldo / 8,
-                        c_off / 8, xq);
+                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8);
     };
-    if (stride == 1)
-      return cols == 1 ? go(pool3x3_rows_kernel<1, 1>) : cols == 2 ? go(pool3x3_rows_kernel<1, 2>)
-                                                         : go(pool3x3_rows_kernel<1, 4>);
-    return cols == 1 ? go(pool3x3_rows_kernel<2, 1>) : cols == 2 ? go(pool3x3_rows_kernel<2, 2>)
-                                                       : go(pool3x3_rows_kernel<2, 4>);
+    if (stride == 1) return is_max ? go(pool3x3_rows_kernel<1, true>) : go(pool3x3_rows_kernel<1, false>);
+    return is_max ? go(pool3x3_rows_kernel<2, true>) : go(pool3x3_rows_kernel<2, false>);
   }
   const long long work = static_cast<long long>(n) * ho * wo * cg;
   return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,

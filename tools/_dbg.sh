@@ -1,5 +1,4 @@
-mkdir -p gpurun_out/pool
-for c in 1 2 4; do
-  DS_POOL_COLS=$c timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/pool/i$c.json 2>gpurun_out/pool/i$c.err
-done
-DS_POOL_LEGACY=1 timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/pool/ileg.json 2>gpurun_out/pool/ileg.err
+mkdir -p gpurun_out/pool2
+timeout 600 python -m pytest tests -m gpu -x -q --timeout=150 --timeout-method=thread -k "pool or logits" > gpurun_out/pool2/pytest.log 2>&1; echo "exit $?" >> gpurun_out/pool2/pytest.log
+timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/pool2/i.json 2>gpurun_out/pool2/i.err
+timeout 600 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:193 --max-converge 1 > gpurun_out/pool2/r.json 2>gpurun_out/pool2/r.err
