@@ -800,7 +800,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
   constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
-  constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D);
+  // kS2DWide: kS2D over 16 or 32 channels (C / 16 boxes per block); its own
+  // instantiation keeps the single-box stem kernel's registers lean
+  constexpr bool kS2W = MODE == static_cast<int>(ConvLoadMode::kS2DWide);
+  constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D) || kS2W;
   constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
   // (kWindow's A operands live in the halo boxes: its ring stages carry B only)
   // (kS2D ring stages are sized for two sub-tiles: a halo box of a 64-row
@@ -813,6 +816,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t box_stride = (args.dw_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
   const uint32_t a_stage = static_cast<uint32_t>(kS2 ? 2 : mt) * kABytes;
+  // kS2D: per 16-channel block one halo box, 1 KiB apart in the stage
+  const uint32_t s2_box_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
@@ -1171,13 +1176,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (args.win_iw > 0) {  // one halo box per block holds every tap's window
           const uint32_t s = rp.slot;
           if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&full[s], args.win_box_bytes);
-          asm volatile(
-              "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + L.a_off + s * a_stage)),
-              "l"(&args.tmap_a), "r"(ptx::smem_u32(&full[s])), "r"(0), "r"(bx * args.dw_tw),
-              "r"(by * args.dw_th), "r"(img)
-              : "memory");
+          // one box per 16-channel block (C = 16 or 32), origin shifted by the
+          // padding (negative coordinates read zeros)
+          const int nc = kS2W ? args.C >> 4 : 1;
+          ptx::mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nc) * args.win_box_bytes);
+          for (int cb = 0; cb < nc; ++cb)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                    ptx::smem_u32(smem + L.a_off + s * a_stage + cb * s2_box_stride)),
+                "l"(&args.tmap_a), "r"(ptx::smem_u32(&full[s])), "r"(cb * 16),
+                "r"(bx * args.dw_tw - args.pad_w), "r"(by * args.dw_th - args.pad_h), "r"(img)
+                : "memory");
           rp.next(args.stages);
           continue;
         }
@@ -1338,42 +1348,65 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t b_base = ptx::smem_u32(smem + L.b_off);
           // 2x2 / 4x4 taps (3x3 / 7x7 stems) with two or four sub-tiles:
           // fully unrolled, every descriptor a compile-time offset (uniform issue)
-          auto unrolled = [&](auto dr_c, auto ds_c, auto mt_c) {
+          // (NC 16-channel boxes: K step of (tap t, block cb) = t * NC + cb)
+          auto unrolled = [&](auto dr_c, auto ds_c, auto mt_c, auto nc_c) {
             constexpr int DR = decltype(dr_c)::value, DS = decltype(ds_c)::value;
-            constexpr int MT = decltype(mt_c)::value;
+            constexpr int MT = decltype(mt_c)::value, NC = decltype(nc_c)::value;
             constexpr int IW = 8 + DS - 1;
             const uint64_t da0 = ptx::umma_desc_sw32_kmajor_sbo(box, IW * 32);
             const uint64_t db0 = ptx::umma_desc_sw128_kmajor(b_base);
             const uint64_t bstep = b_bytes >> 4;
+            const uint64_t cstep = s2_box_stride >> 4;
 #pragma unroll
             for (int t = 0; t < DR * DS; ++t)
 #pragma unroll
-              for (int q = 0; q < MT; ++q)
-                ptx::umma_bf16_warp(d + q * args.BN,
-                                    da0 + static_cast<uint64_t>(((16 * q + t / DS) * IW + t % DS) * 2),
-                                    db0 + static_cast<uint64_t>(t >> 2) * bstep + 2 * (t & 3), idesc,
-                                    t != 0);
+              for (int cb = 0; cb < NC; ++cb)
+#pragma unroll
+                for (int q = 0; q < MT; ++q) {
+                  const int k = t * NC + cb;
+                  ptx::umma_bf16_warp(d + q * args.BN,
+                                      da0 + cb * cstep +
+                                          static_cast<uint64_t>(((16 * q + t / DS) * IW + t % DS) * 2),
+                                      db0 + static_cast<uint64_t>(k >> 2) * bstep + 2 * (k & 3), idesc,
+                                      k != 0);
+                }
           };
           const bool fast = (mt == 2 || mt == 4) && !(args.debug_flags & 16);
+          using I1 = std::integral_constant<int, 1>;
           using I2 = std::integral_constant<int, 2>;
+          using I3 = std::integral_constant<int, 3>;
           using I4 = std::integral_constant<int, 4>;
-          if (fast && args.R == 2 && args.S == 2) {
-            if (mt == 2) unrolled(I2{}, I2{}, I2{});
-            else unrolled(I2{}, I2{}, I4{});
-          } else if (fast && args.R == 4 && args.S == 4) {
-            if (mt == 2) unrolled(I4{}, I4{}, I2{});
-            else unrolled(I4{}, I4{}, I4{});
+          bool done = false;
+          if constexpr (kS2W) {
+            if (fast && mt == 2 && args.R == 3 && args.S == 3 && (args.C == 16 || args.C == 32)) {
+              if (args.C == 16) unrolled(I3{}, I3{}, I2{}, I1{});
+              else unrolled(I3{}, I3{}, I2{}, I2{});
+              done = true;
+            }
+          } else {
+            if (fast && args.R == 2 && args.S == 2) {
+              if (mt == 2) unrolled(I2{}, I2{}, I2{}, I1{});
+              else unrolled(I2{}, I2{}, I4{}, I1{});
+              done = true;
+            } else if (fast && args.R == 4 && args.S == 4) {
+              if (mt == 2) unrolled(I4{}, I4{}, I2{}, I1{});
+              else unrolled(I4{}, I4{}, I4{}, I1{});
+              done = true;
+            }
           }
-          for (int t = 0, dr = 0, dc = 0;
-               t < ((fast && args.R == args.S && (args.R == 2 || args.R == 4)) ? 0 : taps) &&
-               !(args.debug_flags & 16);
+          const int ncb = kS2W ? args.C >> 4 : 1;
+          for (int t = 0, dr = 0, dc = 0; t < (done ? 0 : taps) && !(args.debug_flags & 16);
                ++t, dc = dc + 1 == args.S ? 0 : dc + 1, dr = dc == 0 ? dr + 1 : dr) {
-            const uint64_t db = ptx::umma_desc_sw128_kmajor(
-                ptx::smem_u32(smem + L.b_off + (t >> 2) * b_bytes));
-            for (int q = 0; q < mt; ++q) {
-              const uint64_t da = ptx::umma_desc_sw32_kmajor_sbo(
-                  box + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 32, sbo);
-              ptx::umma_bf16_warp(d + q * args.BN, da, db + 2 * (t & 3), idesc, t != 0);
+            for (int cb = 0; cb < ncb; ++cb) {
+              const int k = t * ncb + cb;
+              const uint64_t db = ptx::umma_desc_sw128_kmajor(
+                  ptx::smem_u32(smem + L.b_off + (k >> 2) * b_bytes));
+              for (int q = 0; q < mt; ++q) {
+                const uint64_t da = ptx::umma_desc_sw32_kmajor_sbo(
+                    box + cb * s2_box_stride + static_cast<uint32_t>((16 * q + dr) * args.win_iw + dc) * 32,
+                    sbo);
+                ptx::umma_bf16_warp(d + q * args.BN, da, db + 2 * (k & 3), idesc, k != 0);
+              }
             }
           }
           ptx::umma_commit_warp(&empty[s]);
@@ -1641,13 +1674,13 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
 bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int w, int c,
                            int box_w, int box_h) {
   EncodeTiledFn fn = get_encode_fn();
-  if (!fn || c * 2 != 32) return false;
+  if (!fn || c % 16 != 0) return false;  // (boxes of 16 channels = one 32 B swizzle row)
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
                               static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2,
                                  static_cast<cuuint64_t>(c) * 2 * w,
                                  static_cast<cuuint64_t>(c) * 2 * w * h};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(c), static_cast<cuuint32_t>(box_w),
+  const cuuint32_t box[4] = {16u, static_cast<cuuint32_t>(box_w),
                              static_cast<cuuint32_t>(box_h), 1u};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
@@ -1839,6 +1872,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -1880,7 +1916,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
                    teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
   const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
-                     : mode == ConvLoadMode::kS2D ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
+                     : (mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide)
+                         ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
                      : mode == ConvLoadMode::kStemU8 ? mt_stem
                      : mode == ConvLoadMode::kTmaA ? mt_tma
                                                    : 1;
@@ -1955,7 +1992,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       args.tap_info[t] = ((r * args.W + c) * 3) | (r << 24) | (c << 28);
     }
   }
-  if (mode == ConvLoadMode::kS2D) {
+  const bool s2 = mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide;
+  if (s2) {
     // pixel blocks of dw_th x 8 (halo box) or 16 x 16 (tap boxes) = dw_th / 16
     // 128-row sub-tiles; all weights resident
     args.mt = args.win_iw > 0 ? args.dw_th / 16 : 2;
@@ -1966,7 +2004,10 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     // no producer warps: all sixteen non-TMA/MMA warps drain accumulators
     // (four epilogue teams) when their staging still leaves a 2-deep ring
     if (args.n_acc >= 4 && conv_gemm_stages(args.BN, args.Cout, 16, args.b_res, 2) >= 2) args.teams = 4;
-    if (args.win_box_bytes > 2u * kABytes) return cudaErrorInvalidValue;  // (ring stage = 2 sub-tiles)
+    // (ring stage = 2 sub-tiles: C / 16 boxes, 1 KiB apart)
+    if ((args.C != 16 && args.C != 32) ||
+        static_cast<uint32_t>(args.C / 16) * ((args.win_box_bytes + 1023) / 1024 * 1024) > 2u * kABytes)
+      return cudaErrorInvalidValue;
     args.stages = std::min(6, conv_gemm_stages(args.BN, args.Cout, 4 * args.teams, args.b_res, 2));
     if (args.stages < 2) return cudaErrorInvalidValue;
   }
@@ -1996,9 +2037,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
                           static_cast<int>(args.win_box_bytes)).total + 1024
             : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
-                                   bres, mode == ConvLoadMode::kS2D ? 2 : args.mt) +
+                                   bres, s2 ? 2 : args.mt) +
               pd_extra;
-  const bool blk = dw || win || mode == ConvLoadMode::kS2D;
+  const bool blk = dw || win || s2;
   const int tiles =
       blk  ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
       : pd ? n_tiles * (args.M / (args.Ho * args.Wo))
@@ -2037,6 +2078,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kS2D:
       return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kS2DWide:
+      return launch_pdl(conv_gemm_kernel<10>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kPairTmaA:
       break;  // (launched above)
     case ConvLoadMode::kPwDw:

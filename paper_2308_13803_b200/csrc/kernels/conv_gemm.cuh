@@ -100,6 +100,8 @@ enum class ConvLoadMode : int {
   kPwDw = 8,      // 1x1 conv + the following depthwise 3x3 (dw_w / dw_b / dw_stride): a
                   // tile is one image x BN channels; y / ldy are the depthwise output
   kPairPwDw = 9,  // kPwDw on CTA pairs (two images per pair MMA, B halves as kPairTmaA)
+  kS2DWide = 10,  // kS2D window MMAs for 16 / 32-channel stride-1 3x3 convs (one halo box
+                  // per 16-channel block, padding as negative box coordinates)
 };
 
 // Whether a 1x1 conv (ho x wo output, cout channels, N tile bn) and its
@@ -148,8 +150,8 @@ bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int
 // operand rings fit in shared memory next to the epilogue staging.
 bool conv_gemm_window_ok(int r, int s, int c, int cout);
 
-// 4-D NHWC bf16 map with a {box_c, box_w, box_h, 1} box and 32 B swizzle
-// (box_c * 2 == 32): the kS2D per-tap A boxes.
+// 4-D NHWC bf16 map (c a multiple of 16) with a {16, box_w, box_h, 1} box and
+// 32 B swizzle: the kS2D A boxes (one per 16-channel block).
 bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int w, int c,
                            int box_w, int box_h);
 

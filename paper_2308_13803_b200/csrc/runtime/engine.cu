@@ -97,6 +97,13 @@ int window_mode() {
   return m;
 }
 
+// DS_CONV_NARROW=0: 16/32-channel stride-1 3x3 convs back on the im2col
+// gather (A/B); default: as kS2D window MMAs.
+bool narrow_window_on() {
+  const char* e = std::getenv("DS_CONV_NARROW");
+  return !(e && e[0] == '0');
+}
+
 bool window_on(int c, int ho, int wo) {
   const int m = window_mode();
   return m == 1 || (m == 2 && c % 64 == 0 && ho >= 28 && wo >= 28);
@@ -291,6 +298,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.R = s2d_.dr;
       a.S = s2d_.ds;
       a.C = 16;
+      a.pad_h = a.pad_w = 0;  // (the s2d buffer holds the stem's padding)
       a.taps = s2d_.dr * s2d_.ds;
       a.num_kb = s2d_.kpad / kConvBK;
       a.dw_th = 16;
@@ -311,6 +319,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.R = s2d_.dr;
       a.S = s2d_.ds;
       a.C = 16;
+      a.pad_h = a.pad_w = 0;  // (the s2d buffer holds the stem's padding)
       a.taps = s2d_.dr * s2d_.ds;
       a.num_kb = s2d_.kpad / kConvBK;
       const char* rows_env = std::getenv("DS_S2D_ROWS");
@@ -331,6 +340,25 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
+    } else if (narrow_window_on() && op.kind == OpKind::kConv && op.sh == 1 && op.sw == 1 &&
+               op.r == 3 && op.s == 3 && (in.c == 16 || in.c == 32) && op.residual < 0 && !out.f32 &&
+               p.cout <= 256 && out.h >= 28 && out.w >= 28 &&
+               kpad / kConvBK * ((p.cout + 15) / 16 * 16) * 128 <= 64 * 1024) {
+      // 3x3 stride-1 conv over 16 / 32 channels (Inception's 147^2 stem convs):
+      // kS2D's window MMAs over one 32 B-swizzled halo box per 16-channel block
+      // and 32 x 8 pixel block, instead of a 16 B-granule im2col gather
+      pl.mode = ConvLoadMode::kS2DWide;
+      a.dw_th = 32;
+      a.dw_tw = 8;
+      a.dw_rw = 4;
+      a.dw_tiles_y = (out.h + 31) / 32;
+      a.dw_tiles_x = (out.w + 7) / 8;
+      a.win_iw = 8 + op.s - 1;
+      a.win_ih = 32 + op.r - 1;
+      a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * 32);
+      if (!encode_tmap_nhwc_sw32(&a.tmap_a, bufs_[op.in], max_bs, in.h, in.w, in.c, a.win_iw,
+                                 a.win_ih))
+        throw CudaError("cuTensorMapEncodeTiled failed (narrow window boxes)");
     } else if (window_on(in.c, out.h, out.w) && op.kind == OpKind::kConv && op.sh == 1 &&
                op.sw == 1 &&
                op.residual < 0 && !out.f32 && conv_gemm_window_ok(op.r, op.s, in.c, p.cout)) {
@@ -403,7 +431,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (pl.mode == ConvLoadMode::kPwDw || pl.mode == ConvLoadMode::kPairPwDw)  // (direct stores)
         a.y_tma = 0;
       else if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow ||
-          pl.mode == ConvLoadMode::kS2D)  // pixel-row boxes
+          pl.mode == ConvLoadMode::kS2D || pl.mode == ConvLoadMode::kS2DWide)  // pixel-row boxes
         a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
                                                 a.dw_tw, a.dw_rw)
                       ? 1

@@ -248,3 +248,18 @@ def test_row_pool_kernel_matches_per_pixel_kernel(monkeypatch, model, bs):
     with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
         legacy = be.forward(imgs)
     assert np.array_equal(rows, legacy)
+
+
+def test_narrow_window_convs_match_gather(monkeypatch):
+    """Inception's 16/32-channel stride-1 3x3 convs as kS2D window MMAs (one
+    32 B-swizzled halo box per 16-channel block, padding as negative box
+    coordinates) against the im2col gather: the same K order (tap, channel),
+    so bit-identical logits."""
+    imgs = generate_images("inception_v3", 31, 2)
+    monkeypatch.setenv("DS_CONV_NARROW", "1")
+    with GpuBackend("inception_v3", Config(abs_max_bs=4, max_mtl=1)) as be:
+        win = be.forward(imgs)
+    monkeypatch.setenv("DS_CONV_NARROW", "0")
+    with GpuBackend("inception_v3", Config(abs_max_bs=4, max_mtl=1)) as be:
+        gather = be.forward(imgs)
+    assert np.array_equal(win, gather)

@@ -1,4 +1,4 @@
-mkdir -p gpurun_out/pool2
-timeout 600 python -m pytest tests -m gpu -x -q --timeout=150 --timeout-method=thread -k "pool or logits" > gpurun_out/pool2/pytest.log 2>&1; echo "exit $?" >> gpurun_out/pool2/pytest.log
-timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/pool2/i.json 2>gpurun_out/pool2/i.err
-timeout 600 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:193 --max-converge 1 > gpurun_out/pool2/r.json 2>gpurun_out/pool2/r.err
+mkdir -p gpurun_out/narrow
+timeout 900 python -m pytest tests -m gpu -q --timeout=200 --timeout-method=thread -k "narrow or logits or s2d or stem" > gpurun_out/narrow/pytest.log 2>&1; echo "exit $?" >> gpurun_out/narrow/pytest.log
+timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/narrow/i.json 2>gpurun_out/narrow/i.err
+timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/narrow/mb.json 2>gpurun_out/narrow/mb.err
