@@ -574,7 +574,8 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
 // offset inside its staging group.
 __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const float* bias_s, int m,
                                                    int n, const uint32_t (&raw)[32], uint8_t* group,
-                                                   int col, int lane, const uint4 (&res)[4]) {
+                                                   int col, int lane, const uint4 (&res)[4],
+                                                   bool narrow = false) {
   float v[32];
   const float4* b4 = reinterpret_cast<const float4*>(bias_s + n);  // n % 32 == 0
 #pragma unroll
@@ -605,6 +606,16 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
   if (a.relu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+  }
+  if (narrow) {  // 64 B rows, 64 B swizzle: 16 B chunk c of row r at c ^ ((r >> 1) & 3)
+    uint8_t* row64 = group + lane * 64;
+    const int sw64 = (lane >> 1) & 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<uint4*>(row64 + ((q ^ sw64) << 4)) =
+          make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    return;
   }
   uint8_t* row = group + lane * 128;
   const int sw = lane & 7;  // 128 B swizzle: 16 B chunk c lives at c ^ (row & 7)
@@ -953,7 +964,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int ybufs = y_bufs(epi_warps);
     const int sub_rows = kBlk ? kConvBM / args.dw_tw : 0;  // block rows per 128-row sub-tile
     uint8_t* ystage = smem + L.y_off + warp * ybufs * kYStageBytes;
-    const int group_cols = args.out_f32 ? 32 : 64;  // one 128 B swizzle row per lane
+    // store groups: one 128 B swizzle row per lane (64 bf16 / 32 fp32), or
+    // with y_narrow (sixteen epilogue warps) 32 bf16 in two 2 KiB 64 B-swizzled
+    // buffers, so the next slice fills while the last one's TMA store reads
+    const bool narrow = args.y_narrow != 0;
+    const int group_cols = narrow || args.out_f32 ? 32 : 64;
+    const int nbufs = narrow ? 2 : ybufs;
+    const uint32_t buf_bytes = narrow ? kYStageBytes / 2 : kYStageBytes;
     uint32_t j = 0, groups = 0;
     TileWalk tw(n_tiles, cl);
     for (int tile = walk_first; tile < walk_count; tile += walk_stride, ++j, tw.next()) {
@@ -1013,10 +1030,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         } else if (args.y_tma) {
           const int g_end = (part + 1) * part_cols;
           for (int g0 = part * part_cols; g0 < g_end && n0 + g0 < args.Cout; g0 += group_cols) {
-            uint8_t* group = ystage + (ybufs == 2 ? (groups & 1) * kYStageBytes : 0);
-            if (groups >= static_cast<uint32_t>(ybufs)) {  // the store that used `group` has read it
+            uint8_t* group = ystage + (nbufs == 2 ? (groups & 1) * buf_bytes : 0);
+            if (groups >= static_cast<uint32_t>(nbufs)) {  // the store that used `group` has read it
               if (lane == 0) {
-                if (ybufs == 2)
+                if (nbufs == 2)
                   ptx::bulk_wait_read<1>();
                 else
                   ptx::bulk_wait_read<0>();
@@ -1035,7 +1052,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               uint32_t raw[32];
               ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
               ptx::tmem_ld_wait();
-              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res);
+              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res, narrow);
             }
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
@@ -1671,6 +1688,20 @@ bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool encode_tmap_out_narrow(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
+                            uint64_t row_stride_elems) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn || (row_stride_elems * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0)
+    return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {row_stride_elems * 2};
+  const cuuint32_t box[2] = {32u, 32u};  // one 64 B row per output row
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int w, int c,
                            int box_w, int box_h) {
   EncodeTiledFn fn = get_encode_fn();
@@ -1950,6 +1981,21 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   if (tpa_on && (mode == ConvLoadMode::kTmaA || pair) && args.BN >= 128 && args.n_acc == 2 &&
       args.BN % (2 * group_cols) == 0)
     args.teams = 4;
+  // sixteen epilogue warps (one staging buffer each at 64-column groups):
+  // store 32-column slices through a 64 B-swizzled map instead, two buffers
+  // per warp (DS_Y_NARROW=0: off)
+  args.y_narrow = 0;
+  {
+    const char* e = std::getenv("DS_Y_NARROW");
+    const bool on = !(e && e[0] == '0');
+    const bool blk_mode = mode == ConvLoadMode::kDwFused || mode == ConvLoadMode::kWindow ||
+                          mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide || pd;
+    if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8 &&
+        encode_tmap_out_narrow(&args.tmap_y, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
+                               static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
+                               static_cast<uint64_t>(args.ldy)))
+      args.y_narrow = 1;
+  }
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;

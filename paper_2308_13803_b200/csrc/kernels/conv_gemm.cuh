@@ -27,6 +27,7 @@ struct ConvGemmArgs {
   CUtensorMap tmap_a;  // input viewed as [rows][C] (1x1 stride-1 convs only)
   CUtensorMap tmap_y;  // output slice [rows][Cout] at y + c_off, 128 B x 32-row boxes (y_tma)
   int y_tma;           // epilogue stores through smem + TMA (else direct stores)
+  int y_narrow;        // tmap_y has 32 x 32 boxes, 64 B swizzle (launch_conv_gemm sets it)
   const __nv_bfloat16* x;
   int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
   int R, S, stride_h, stride_w, pad_h, pad_w;
@@ -119,6 +120,11 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint
 // cannot address it (row stride or base not 16 B aligned).
 bool encode_tmap_out(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
                      uint64_t row_stride_elems, bool f32);
+
+// The same for bf16 with 32-column x 32-row boxes and 64 B swizzle (the
+// double-buffered 2 KiB staging of sixteen-warp epilogues).
+bool encode_tmap_out_narrow(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols,
+                            uint64_t row_stride_elems);
 
 // NHWC bf16 activation as a 4-D map {C, W, H, N} with a {box_c, box_w,
 // box_h, 1} box, no swizzle (used by the depthwise halo loads). Negative or

@@ -462,13 +462,14 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
       : "memory");
 }
 
-// Arrive (release, cluster scope) on the mbarrier at this offset in CTA `rank`.
+// Arrive on the mbarrier at this offset in CTA `rank` (default semantics: the
+// caller has already waited for its TMEM loads, which is all the leader needs).
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n\t"
       ".reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t"
       "}" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");

@@ -1,4 +1,5 @@
-mkdir -p gpurun_out/fc
-for b in 64 32 16; do
-DS_FC_BN=$b timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/fc/b$b.json 2>gpurun_out/fc/b$b.err
-done
+mkdir -p gpurun_out/arrive2
+timeout 900 python -m pytest tests -m gpu -q --timeout=200 --timeout-method=thread > gpurun_out/arrive2/pytest.log 2>&1; echo "exit $?" >> gpurun_out/arrive2/pytest.log
+timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/arrive2/mb.json 2>gpurun_out/arrive2/mb.err
+timeout 600 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:193 --max-converge 1 > gpurun_out/arrive2/r.json 2>gpurun_out/arrive2/r.err
+timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/arrive2/i.json 2>gpurun_out/arrive2/i.err

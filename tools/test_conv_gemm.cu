@@ -223,6 +223,8 @@ int main(int argc, char** argv) {
       {"tmaA C32 small", 3, 5, 7, 32, 1, 1, 1, 1, 0, 0, 48, 48, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 pw2 bs128", 128, 56, 56, 64, 1, 1, 1, 1, 0, 0, 128, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 pw7 bs128", 128, 14, 14, 512, 1, 1, 1, 1, 0, 0, 512, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 pw5 bs128", 128, 28, 28, 256, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 pw4 bs128", 128, 28, 28, 128, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
   };
   // Optional filter: substring of the case name; "--no-check" skips the CPU reference.
   const char* only = argc > 1 ? argv[1] : nullptr;
