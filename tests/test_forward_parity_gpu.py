@@ -263,3 +263,18 @@ def test_narrow_window_convs_match_gather(monkeypatch):
     with GpuBackend("inception_v3", Config(abs_max_bs=4, max_mtl=1)) as be:
         gather = be.forward(imgs)
     assert np.array_equal(win, gather)
+
+
+@pytest.mark.parametrize("bs", [1, 5])
+def test_depthwise_4channel_groups_match_8channel(monkeypatch, bs):
+    """The 14 x 14 depthwise layers with 4-channel thread groups (half the
+    registers, twice the occupancy) against 8-channel groups: the same fma
+    order per output, so bit-identical logits."""
+    imgs = generate_images("mobilenet_v1", 37, bs)
+    monkeypatch.setenv("DS_DW_G4", "1")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        g4 = be.forward(imgs)
+    monkeypatch.setenv("DS_DW_G4", "0")
+    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
+        g8 = be.forward(imgs)
+    assert np.array_equal(g4, g8)

@@ -1,5 +1,5 @@
-mkdir -p gpurun_out/arrive2
-timeout 900 python -m pytest tests -m gpu -q --timeout=200 --timeout-method=thread > gpurun_out/arrive2/pytest.log 2>&1; echo "exit $?" >> gpurun_out/arrive2/pytest.log
-timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/arrive2/mb.json 2>gpurun_out/arrive2/mb.err
-timeout 600 python bench.py --model resnet50_v1 --kernel-table --no-cpu-baseline --knob batching:193 --max-converge 1 > gpurun_out/arrive2/r.json 2>gpurun_out/arrive2/r.err
-timeout 600 python bench.py --model inception_v3 --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/arrive2/i.json 2>gpurun_out/arrive2/i.err
+mkdir -p gpurun_out/g4
+timeout 900 python -m pytest tests -m gpu -q --timeout=200 --timeout-method=thread -k "depthwise or logits" > gpurun_out/g4/pytest.log 2>&1; echo "exit $?" >> gpurun_out/g4/pytest.log
+for v in 1 0; do
+DS_DW_G4=$v timeout 300 python bench.py --kernel-table --no-cpu-baseline --knob batching:128 --max-converge 1 > gpurun_out/g4/mb$v.json 2>gpurun_out/g4/mb$v.err
+done
