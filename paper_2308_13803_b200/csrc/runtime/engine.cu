@@ -173,9 +173,14 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     check_cuda(cudaStreamSynchronize(stream_), "upload s2d stem weights");
   }
   check_cuda(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  check_cuda(cudaStreamCreateWithFlags(&out_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (int s = 0; s < 2; ++s) {
     check_cuda(cudaEventCreateWithFlags(&slot_free_[s], cudaEventDisableTiming), "event");
     check_cuda(cudaEventCreateWithFlags(&h2d_done_[s], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreateWithFlags(&out_ready_[s], cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreateWithFlags(&out_read_[s], cudaEventDisableTiming), "event");
+    check_cuda(cudaMalloc(&d_out_[s], static_cast<size_t>(max_bs) * m.classes * sizeof(float)),
+               "cudaMalloc logits slot");
   }
   for (size_t o : buf_off) bufs_.push_back(base + o);
   d_probs_ = reinterpret_cast<float*>(base + probs_off);
@@ -448,12 +453,17 @@ Instance::~Instance() {
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   if (copy_stream_) cudaStreamSynchronize(copy_stream_);
+  if (out_stream_) cudaStreamSynchronize(out_stream_);
   if (d_arena_) cudaFree(d_arena_);
   for (int s = 0; s < 2; ++s) {
     if (slot_free_[s]) cudaEventDestroy(slot_free_[s]);
     if (h2d_done_[s]) cudaEventDestroy(h2d_done_[s]);
+    if (out_ready_[s]) cudaEventDestroy(out_ready_[s]);
+    if (out_read_[s]) cudaEventDestroy(out_read_[s]);
+    if (d_out_[s]) cudaFree(d_out_[s]);
   }
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  if (out_stream_) cudaStreamDestroy(out_stream_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -704,10 +714,21 @@ void Backend::enqueue_request(int i, int bs) {
     check_cuda(cudaStreamWaitEvent(s, I.h2d_done(slot), 0), "wait h2d");
     I.enqueue_forward(bs, slot);
     check_cuda(cudaEventRecord(I.slot_free(slot), s), "event record");
+    // logits -> this slot's buffer (on the compute stream, once the D2H that
+    // last read it is done), then D2H on the instance's output stream, so
+    // the next request's forward does not queue behind the PCIe read
     const size_t lb = static_cast<size_t>(bs) * model_.classes * sizeof(float);
-    check_cuda(cudaMemcpyAsync(pinned_logits_[i], I.logits(), lb, cudaMemcpyDeviceToHost, s),
+    check_cuda(cudaStreamWaitEvent(s, I.out_read(slot), 0), "wait out slot");
+    check_cuda(cudaMemcpyAsync(I.out(slot), I.logits(), lb, cudaMemcpyDeviceToDevice, s),
+               "logits to slot");
+    check_cuda(cudaEventRecord(I.out_ready(slot), s), "event record");
+    cudaStream_t os = I.out_stream();
+    check_cuda(cudaStreamWaitEvent(os, I.out_ready(slot), 0), "wait logits");
+    check_cuda(cudaMemcpyAsync(pinned_logits_[i], I.out(slot), lb, cudaMemcpyDeviceToHost, os),
                "D2H logits");
+    check_cuda(cudaEventRecord(I.out_read(slot), os), "event record");
     d2h_bytes_ += static_cast<int64_t>(lb);
+    s = os;  // (the request ends when its logits are in host memory)
   }
   kernel_launches_ += I.kernels_per_forward();
   check_cuda(cudaEventRecord(f.end, s), "event record");

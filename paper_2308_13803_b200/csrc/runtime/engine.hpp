@@ -61,6 +61,10 @@ class Instance {
   cudaEvent_t slot_free(int slot) const { return slot_free_[slot]; }
   cudaEvent_t h2d_done(int slot) const { return h2d_done_[slot]; }
   float* logits() const { return d_logits_; }
+  cudaStream_t out_stream() const { return out_stream_; }
+  float* out(int slot) const { return d_out_[slot]; }
+  cudaEvent_t out_ready(int slot) const { return out_ready_[slot]; }
+  cudaEvent_t out_read(int slot) const { return out_read_[slot]; }
   float* probs() const { return d_probs_; }
   int max_bs() const { return max_bs_; }
   int kernels_per_forward() const { return kernels_per_forward_; }
@@ -84,6 +88,10 @@ class Instance {
   cudaStream_t copy_stream_ = nullptr;
   cudaEvent_t slot_free_[2] = {nullptr, nullptr};  // forward done reading a slot
   cudaEvent_t h2d_done_[2] = {nullptr, nullptr};   // a slot's images have landed
+  cudaStream_t out_stream_ = nullptr;               // logits D2H (end-to-end mode)
+  float* d_out_[2] = {nullptr, nullptr};            // per-slot logits copies
+  cudaEvent_t out_ready_[2] = {nullptr, nullptr};   // a slot's logits copy written
+  cudaEvent_t out_read_[2] = {nullptr, nullptr};    // ... and read back to the host
   float* d_logits_ = nullptr;
   float* d_probs_ = nullptr;
   std::vector<void*> bufs_;
