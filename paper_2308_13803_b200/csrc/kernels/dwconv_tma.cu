@@ -71,6 +71,14 @@ __device__ __forceinline__ uint32_t pack2f(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// relu then round == round then relu (rounding is monotonic and keeps 0), so
+// the ReLU runs on the packed bf16 pair: one max.bf16x2 instead of two FMNMX.
+__device__ __forceinline__ uint32_t relu_pack2(float lo, float hi) {
+  uint32_t d;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(pack2f(lo, hi)), "r"(0u));
+  return d;
+}
+
 // n / d for 0 <= n < 2^31 by multiply-high and shift (d >= 1, host-built).
 struct FastDiv {
   uint32_t d, mul, shift;
@@ -174,8 +182,9 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
   float bias[8];
   int cur_cbk = -1;
   uint32_t j = 0;
+  int stage = 0;
+  uint32_t phase = 0;  // (ring position advanced without divisions)
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++j) {
-    const int stage = j % a.stages;
     int cbk, tx, ty, tn;
     coords(t, cbk, tx, ty, tn);
     const int oy = ty * a.th + oyl;
@@ -190,7 +199,7 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
       bias[0] = b0.x; bias[1] = b0.y; bias[2] = b0.z; bias[3] = b0.w;
       bias[4] = b1.x; bias[5] = b1.y; bias[6] = b1.z; bias[7] = b1.w;
     }
-    ptx::mbar_wait(&full[stage], (j / a.stages) & 1);
+    ptx::mbar_wait(&full[stage], phase);
     if (active && oy < a.ho && img < a.n) {
       float acc[Q][8];
 #pragma unroll
@@ -214,16 +223,20 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         float* v = acc[q];
-        yp[q * cg_all] = make_uint4(pack2f(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)),
-                                    pack2f(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)),
-                                    pack2f(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)),
-                                    pack2f(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
+        yp[q * cg_all] = make_uint4(relu_pack2(v[0], v[1]),
+                                    relu_pack2(v[2], v[3]),
+                                    relu_pack2(v[4], v[5]),
+                                    relu_pack2(v[6], v[7]));
       }
     }
     __syncthreads();  // every thread is done with this stage's box
     if (threadIdx.x == 0) {
       const int nt = t + a.stages * static_cast<int>(gridDim.x);
       if (nt < a.tiles) issue(nt, stage);
+    }
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1u;
     }
   }
 }
@@ -294,8 +307,9 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma4_kernel(
   float bias[4];
   int cur_cbk = -1;
   uint32_t j = 0;
+  int stage = 0;
+  uint32_t phase = 0;  // (ring position advanced without divisions)
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++j) {
-    const int stage = j % a.stages;
     int cbk, tx, ty, tn;
     coords(t, cbk, tx, ty, tn);
     const int oy = ty * a.th + oyl;
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma4_kernel(
       const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias) + gg);
       bias[0] = b.x; bias[1] = b.y; bias[2] = b.z; bias[3] = b.w;
     }
-    ptx::mbar_wait(&full[stage], (j / a.stages) & 1);
+    ptx::mbar_wait(&full[stage], phase);
     if (active && oy < a.ho && img < a.n) {
       float acc[Q][4];
 #pragma unroll
@@ -337,13 +351,17 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma4_kernel(
                   ((static_cast<long long>(img) * a.ho + oy) * a.wo + tx * a.tw + sx * Q) * cg_all + gg;
 #pragma unroll
       for (int q = 0; q < Q; ++q)
-        yp[q * cg_all] = make_uint2(pack2f(fmaxf(acc[q][0], 0.f), fmaxf(acc[q][1], 0.f)),
-                                    pack2f(fmaxf(acc[q][2], 0.f), fmaxf(acc[q][3], 0.f)));
+        yp[q * cg_all] = make_uint2(relu_pack2(acc[q][0], acc[q][1]),
+                                    relu_pack2(acc[q][2], acc[q][3]));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       const int nt = t + a.stages * static_cast<int>(gridDim.x);
       if (nt < a.tiles) issue(nt, stage);
+    }
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1u;
     }
   }
 }
