@@ -504,6 +504,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// pack to bf16 pairs, then max with `floor` (0: ReLU; bf16 -inf pair: none).
+// ReLU after rounding equals rounding after ReLU (rounding is monotonic and
+// maps 0 to 0).
+__device__ __forceinline__ uint32_t relu_pack_bf16(float lo, float hi, uint32_t floor) {
+  uint32_t d;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(pack_bf16(lo, hi)), "r"(floor));
+  return d;
+}
+
 // bias_s: the layer's bias staged in shared memory (indexed by channel).
 __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const float* bias_s, int m,
                                                int n, const uint32_t (&raw)[16]) {
@@ -603,18 +612,23 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
       for (int j = 0; j < 32 && n + j < a.Cout; ++j) v[j] += __bfloat162float(rrow[j]);
     }
   }
-  if (a.relu) {
+  // (bf16 outputs: the ReLU runs on the packed pairs, after rounding — the
+  // same values, one max.bf16x2 per pair instead of two FMNMX)
+  if (a.relu && a.out_f32) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
   }
+  const uint32_t relu_floor = a.relu ? 0u : 0xFF80FF80u;  // max with 0, or with -inf (identity)
   if (narrow) {  // 64 B rows, 64 B swizzle: 16 B chunk c of row r at c ^ ((r >> 1) & 3)
     uint8_t* row64 = group + lane * 64;
     const int sw64 = (lane >> 1) & 3;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       *reinterpret_cast<uint4*>(row64 + ((q ^ sw64) << 4)) =
-          make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+          make_uint4(relu_pack_bf16(v[8 * q], v[8 * q + 1], relu_floor),
+                     relu_pack_bf16(v[8 * q + 2], v[8 * q + 3], relu_floor),
+                     relu_pack_bf16(v[8 * q + 4], v[8 * q + 5], relu_floor),
+                     relu_pack_bf16(v[8 * q + 6], v[8 * q + 7], relu_floor));
     return;
   }
   uint8_t* row = group + lane * 128;
@@ -629,8 +643,10 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       *reinterpret_cast<uint4*>(row + (((c16 + q) ^ sw) << 4)) =
-          make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+          make_uint4(relu_pack_bf16(v[8 * q], v[8 * q + 1], relu_floor),
+                     relu_pack_bf16(v[8 * q + 2], v[8 * q + 3], relu_floor),
+                     relu_pack_bf16(v[8 * q + 4], v[8 * q + 5], relu_floor),
+                     relu_pack_bf16(v[8 * q + 6], v[8 * q + 7], relu_floor));
   }
 }
 
@@ -967,7 +983,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // store groups: one 128 B swizzle row per lane (64 bf16 / 32 fp32), or
     // with y_narrow (sixteen epilogue warps) 32 bf16 in two 2 KiB 64 B-swizzled
     // buffers, so the next slice fills while the last one's TMA store reads
-    const bool narrow = args.y_narrow != 0;
+    const bool narrow = !kBlk && args.y_narrow != 0;  // (compiled out of the block modes)
     const int group_cols = narrow || args.out_f32 ? 32 : 64;
     const int nbufs = narrow ? 2 : ybufs;
     const uint32_t buf_bytes = narrow ? kYStageBytes / 2 : kYStageBytes;
@@ -1043,7 +1059,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int c = 0; c < group_cols && g0 + c < g_end; c += 32) {
               // residual slice first: its global load overlaps the TMEM load
               uint4 res[4];
-              if (args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
+              if (!kS2 && args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
                 const uint4* rp = reinterpret_cast<const uint4*>(
                     args.residual + static_cast<size_t>(m) * args.ld_res + n0 + g0 + c);
 #pragma unroll
