@@ -826,7 +826,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr long long ts0 = 0;
   const int epi_warps = 4 * args.teams;
   constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
-  constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow);
+  // kWindowT: kWindow with the transposed (C % 64 != 0) halo boxes, its own
+  // instantiation so the default in-place mode carries none of that code
+  constexpr bool kWinT = MODE == static_cast<int>(ConvLoadMode::kWindowT);
+  constexpr bool kWin = MODE == static_cast<int>(ConvLoadMode::kWindow) || kWinT;
+  const bool win_direct = kWin && !kWinT;
   // kS2DWide: kS2D over 16 or 32 channels (C / 16 boxes per block); its own
   // instantiation keeps the single-box stem kernel's registers lean
   constexpr bool kS2W = MODE == static_cast<int>(ConvLoadMode::kS2DWide);
@@ -904,8 +908,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       ptx::mbar_init(b_full, 1);
       for (int b = 0; b < 2; ++b) {
         ptx::mbar_init(&raw_full[b], 1);
-        ptx::mbar_init(&raw_free[b], args.win_direct ? 1 : kGatherWarps);
-        ptx::mbar_init(&cm_full[b], args.win_direct ? 1 : kGatherWarps);
+        ptx::mbar_init(&raw_free[b], win_direct ? 1 : kGatherWarps);
+        ptx::mbar_init(&cm_full[b], win_direct ? 1 : kGatherWarps);
         ptx::mbar_init(&cm_empty[b], 1);
       }
       for (int b = 0; b < n_acc; ++b) {
@@ -1137,7 +1141,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int raw_chunks = cb / 8;  // 16 B chunks per raw pixel row
       uint32_t u = 0;                  // box uses so far (slot u & 1, phase u >> 1)
       // (direct mode: the MMA reads the TMA's 128 B-swizzled box itself)
-      for (int tile = blockIdx.x; tile < (args.win_direct ? 0 : tiles); tile += gridDim.x) {
+      for (int tile = blockIdx.x; tile < (win_direct ? 0 : tiles); tile += gridDim.x) {
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
           const uint32_t b = u & 1, ph = (u >> 1) & 1;
           ptx::mbar_wait(&raw_full[b], ph);
@@ -1264,9 +1268,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int bx = blk - by * args.dw_tiles_x;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
           // (direct mode: 4 box slots, the MMA frees them; else 2 + 2 transposed)
-          const uint32_t nb_slots = args.win_direct ? 4u : 2u;
+          const uint32_t nb_slots = win_direct ? 4u : 2u;
           const uint32_t b = u % nb_slots, ph = (u / nb_slots) & 1;
-          if (u >= nb_slots) ptx::mbar_wait(args.win_direct ? &slot_free[b] : &raw_free[b], ph ^ 1);
+          if (u >= nb_slots) ptx::mbar_wait(win_direct ? &slot_free[b] : &raw_free[b], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&raw_full[b], args.win_box_bytes);  // (== slot_full[b])
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -1486,7 +1490,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const uint32_t d = tmem_base + acc * acc_stride;
         bool first = true;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
-          const bool direct = args.win_direct != 0;
+          const bool direct = win_direct;
           const uint32_t b = direct ? u & 3 : u & 1;
           t0 = clock64();
           if (direct) {
@@ -1922,6 +1926,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -2137,7 +2144,11 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     case ConvLoadMode::kStemU8:
       return launch_pdl(conv_gemm_kernel<4>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kWindow:
+      if (!args.win_direct)
+        return launch_pdl(conv_gemm_kernel<11>, grid, dim3(kConvThreads), smem, stream, args);
       return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
+    case ConvLoadMode::kWindowT:
+      return cudaErrorInvalidValue;  // (selected through kWindow + win_direct = 0)
     case ConvLoadMode::kS2D:
       return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kS2DWide:

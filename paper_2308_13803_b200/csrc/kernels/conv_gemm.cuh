@@ -103,6 +103,7 @@ enum class ConvLoadMode : int {
   kPairPwDw = 9,  // kPwDw on CTA pairs (two images per pair MMA, B halves as kPairTmaA)
   kS2DWide = 10,  // kS2D window MMAs for 16 / 32-channel stride-1 3x3 convs (one halo box
                   // per 16-channel block, padding as negative box coordinates)
+  kWindowT = 11,  // (internal) kWindow with transposed boxes: launch as kWindow, win_direct 0
 };
 
 // Whether a 1x1 conv (ho x wo output, cout channels, N tile bn) and its
