@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // store groups: one 128 B swizzle row per lane (64 bf16 / 32 fp32), or
     // with y_narrow (sixteen epilogue warps) 32 bf16 in two 2 KiB 64 B-swizzled
     // buffers, so the next slice fills while the last one's TMA store reads
-    const bool narrow = !kBlk && args.y_narrow != 0;  // (compiled out of the block modes)
+    const bool narrow = kTmaA && args.y_narrow != 0;  // (only the TMA-A modes have 16 epilogue warps)
     const int group_cols = narrow || args.out_f32 ? 32 : 64;
     const int nbufs = narrow ? 2 : ybufs;
     const uint32_t buf_bytes = narrow ? kYStageBytes / 2 : kYStageBytes;
