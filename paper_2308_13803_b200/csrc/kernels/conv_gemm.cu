@@ -514,6 +514,7 @@ __device__ __forceinline__ uint32_t relu_pack_bf16(float lo, float hi, uint32_t 
 }
 
 // bias_s: the layer's bias staged in shared memory (indexed by channel).
+template <bool RES>
 __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const float* bias_s, int m,
                                                int n, const uint32_t (&raw)[16]) {
   float v[16];
@@ -529,7 +530,7 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
       v[4 * q + 2] += b.z;
       v[4 * q + 3] += b.w;
     }
-    if (a.residual) {
+    if (RES && a.residual) {
       const uint4* rp =
           reinterpret_cast<const uint4*>(a.residual + static_cast<size_t>(m) * a.ld_res + n);
 #pragma unroll
@@ -566,7 +567,7 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
   } else {
     for (int j = 0; j < 16 && n + j < a.Cout; ++j) {
       float x = v[j] + bias_s[n + j];
-      if (a.residual) x += __bfloat162float(a.residual[static_cast<size_t>(m) * a.ld_res + n + j]);
+      if (RES && a.residual) x += __bfloat162float(a.residual[static_cast<size_t>(m) * a.ld_res + n + j]);
       if (a.relu) x = fmaxf(x, 0.0f);
       const size_t o = static_cast<size_t>(m) * a.ldy + a.c_off + n + j;
       if (a.out_f32)
@@ -581,6 +582,7 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
 // registers, + bias (+ residual), ReLU, packed into the 128 B-swizzled
 // staging rows (lane = row, conflict-free 16 B stores). `col` is the slice's
 // offset inside its staging group.
+template <bool RES>
 __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const float* bias_s, int m,
                                                    int n, const uint32_t (&raw)[32], uint8_t* group,
                                                    int col, int lane, const uint4 (&res)[4],
@@ -595,7 +597,7 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
     v[4 * q + 2] = __uint_as_float(raw[4 * q + 2]) + b.z;
     v[4 * q + 3] = __uint_as_float(raw[4 * q + 3]) + b.w;
   }
-  if (a.residual && m < a.M) {
+  if (RES && a.residual && m < a.M) {
     const __nv_bfloat16* rrow = a.residual + static_cast<size_t>(m) * a.ld_res + n;
     if (n + 32 <= a.Cout) {  // (loaded by the caller before the TMEM load)
 #pragma unroll
@@ -817,6 +819,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr bool kPD = MODE == static_cast<int>(ConvLoadMode::kPwDw) ||
                       MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
   constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kPD;
+  // residual adds are compiled into the 1x1 modes only (the runtime routes
+  // every residual conv there); the other modes carry none of that state
+  constexpr bool kRes = kTmaA && !kPD;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
   // (offsetting smem_raw, rather than masking the generic address, keeps the
@@ -997,7 +1002,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (static_cast<int>(j & (tile_teams - 1)) != team) continue;  // teams: power of two
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
-      if (!kBlk && args.residual) {
+      if (kRes && args.residual) {
         // pull this lane's residual rows (its column part) into L2 a tile
         // ahead — this team's next tile (and, the first time, this one) — so
         // the epilogue's loads do not each wait on HBM
@@ -1063,7 +1068,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int c = 0; c < group_cols && g0 + c < g_end; c += 32) {
               // residual slice first: its global load overlaps the TMEM load
               uint4 res[4];
-              if (!kS2 && args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
+              if (kRes && args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
                 const uint4* rp = reinterpret_cast<const uint4*>(
                     args.residual + static_cast<size_t>(m) * args.ld_res + n0 + g0 + c);
 #pragma unroll
@@ -1072,7 +1077,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               uint32_t raw[32];
               ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
               ptx::tmem_ld_wait();
-              epilogue_slice_tma(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res, narrow);
+              epilogue_slice_tma<kRes>(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res, narrow);
             }
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
@@ -1094,7 +1099,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint32_t raw[16];
             ptx::tmem_ld_32x32b_x16(t_row + c0, raw);
             ptx::tmem_ld_wait();
-            if (m < args.M) epilogue_chunk(args, bias_s, m, n0 + c0, raw);
+            if (m < args.M) epilogue_chunk<kRes>(args, bias_s, m, n0 + c0, raw);
           }
         }
       }

@@ -403,6 +403,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.ldy = dw_out.c;
       a.c_off = 0;
     }
+    if (op.residual >= 0 && pl.mode != ConvLoadMode::kTmaA)
+      throw std::logic_error("residual adds are supported on 1x1 stride-1 convs only");
     // wide TMA-A layers: CTA pairs may multicast each weight block (opt-in)
     const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
     a.cluster = pl.mode == ConvLoadMode::kTmaA && a.BN == 256 && !b_resident && cluster_on() ? 2 : 1;
