@@ -291,7 +291,10 @@ __device__ __forceinline__ uint32_t max_bf16x2(uint32_t a, uint32_t b) {
   return d;
 }
 
-template <int STRIDE, bool IS_MAX>
+// ROWS output rows per thread (grid.y = image x row group): input rows are
+// loaded once and feed every output row whose window covers them; each
+// output still sums its taps in row-outer, column-inner order.
+template <int STRIDE, bool IS_MAX, int ROWS>
 __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
                                     int cg, int ho, int wo, int pad, int ldo_g, int coff_g) {
   pdl_trigger();
@@ -302,44 +305,66 @@ __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restri
   if ((ox + 1) * cg <= i) ++ox;
   if (ox >= wo) return;
   const int g = i - ox * cg;
-  const int row = blockIdx.y;
-  const int n = row / ho;
-  const int oy = row - n * ho;
-  const int iy0 = oy * STRIDE - pad, ix0 = ox * STRIDE - pad;
-  uint4 mx = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // bf16 -inf pairs
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int hq = (ho + ROWS - 1) / ROWS;
+  const int n = blockIdx.y / hq;
+  const int oy0 = (blockIdx.y - n * hq) * ROWS;
+  const int iy0 = oy0 * STRIDE - pad, ix0 = ox * STRIDE - pad;
+  constexpr int IN_ROWS = (ROWS - 1) * STRIDE + 3;
+  uint4 mx[ROWS];
+  float acc[ROWS][8];
 #pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int iy = iy0 + r;
+  for (int o = 0; o < ROWS; ++o) {
+    mx[o] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // bf16 -inf pairs
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
+  }
+#pragma unroll
+  for (int ir = 0; ir < IN_ROWS; ++ir) {
+    const int iy = iy0 + ir;
     if (iy < 0 || iy >= h) continue;
     const uint4* xrow = x + (static_cast<long long>(n) * h + iy) * w * cg + g;
+    uint4 v[3];
+    bool ok[3];
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       const int ix = ix0 + s;
-      if (ix < 0 || ix >= w) continue;
-      const uint4 v = __ldg(xrow + ix * cg);
-      if constexpr (IS_MAX) {
-        mx.x = max_bf16x2(mx.x, v.x);
-        mx.y = max_bf16x2(mx.y, v.y);
-        mx.z = max_bf16x2(mx.z, v.z);
-        mx.w = max_bf16x2(mx.w, v.w);
-      } else {
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+      ok[s] = ix >= 0 && ix < w;
+      v[s] = ok[s] ? __ldg(xrow + ix * cg) : make_uint4(0, 0, 0, 0);
+    }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          acc[2 * k] = add_bf16_lo(vw[k], acc[2 * k]);
-          acc[2 * k + 1] = add_bf16_hi(vw[k], acc[2 * k + 1]);
+    for (int o = 0; o < ROWS; ++o) {
+      const int r = ir - o * STRIDE;  // this input row's tap row for output o
+      if (r < 0 || r >= 3) continue;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (!ok[s]) continue;
+        if constexpr (IS_MAX) {
+          mx[o].x = max_bf16x2(mx[o].x, v[s].x);
+          mx[o].y = max_bf16x2(mx[o].y, v[s].y);
+          mx[o].z = max_bf16x2(mx[o].z, v[s].z);
+          mx[o].w = max_bf16x2(mx[o].w, v[s].w);
+        } else {
+          const uint32_t vw[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc[o][2 * k] = add_bf16_lo(vw[k], acc[o][2 * k]);
+            acc[o][2 * k + 1] = add_bf16_hi(vw[k], acc[o][2 * k + 1]);
+          }
         }
       }
     }
   }
-  const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox;
-  if constexpr (IS_MAX) {
-    y[opix * ldo_g + coff_g + g] = mx;
-  } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = acc[e] / 9.0f;
-    y[opix * ldo_g + coff_g + g] = pack8(acc);
+  for (int o = 0; o < ROWS; ++o) {
+    if (oy0 + o >= ho) break;
+    const long long opix = (static_cast<long long>(n) * ho + oy0 + o) * wo + ox;
+    if constexpr (IS_MAX) {
+      y[opix * ldo_g + coff_g + g] = mx[o];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[o][e] = acc[o][e] / 9.0f;
+      y[opix * ldo_g + coff_g + g] = pack8(acc[o]);
+    }
   }
 }
 
@@ -492,17 +517,25 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
     const char* e = std::getenv("DS_POOL_LEGACY");
     return e && e[0] == '1';
   }();
-  const int rows = n * ho;
-  if (!legacy && rows <= 65535 && (stride == 1 || stride == 2) && wo * cg < (1 << 24)) {
+  const char* rows_env = std::getenv("DS_POOL_ROWS");  // output rows per thread: 1 or 2 (A/B)
+  const int prows = rows_env && rows_env[0] == '1' ? 1 : 2;
+  const int yrows = n * ((ho + prows - 1) / prows);
+  if (!legacy && yrows <= 65535 && (stride == 1 || stride == 2) && wo * cg < (1 << 24)) {
     const int per_row = wo * cg;
     const int bt = std::min(kBlock, (per_row + 31) / 32 * 32);
-    const dim3 grid((per_row + bt - 1) / bt, rows);
+    const dim3 grid((per_row + bt - 1) / bt, yrows);
     auto go = [&](auto kernel) {
       return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
                         reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8);
     };
-    if (stride == 1) return is_max ? go(pool3x3_rows_kernel<1, true>) : go(pool3x3_rows_kernel<1, false>);
-    return is_max ? go(pool3x3_rows_kernel<2, true>) : go(pool3x3_rows_kernel<2, false>);
+    if (prows == 1) {
+      if (stride == 1)
+        return is_max ? go(pool3x3_rows_kernel<1, true, 1>) : go(pool3x3_rows_kernel<1, false, 1>);
+      return is_max ? go(pool3x3_rows_kernel<2, true, 1>) : go(pool3x3_rows_kernel<2, false, 1>);
+    }
+    if (stride == 1)
+      return is_max ? go(pool3x3_rows_kernel<1, true, 2>) : go(pool3x3_rows_kernel<1, false, 2>);
+    return is_max ? go(pool3x3_rows_kernel<2, true, 2>) : go(pool3x3_rows_kernel<2, false, 2>);
   }
   const long long work = static_cast<long long>(n) * ho * wo * cg;
   return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
