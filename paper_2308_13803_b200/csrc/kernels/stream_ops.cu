@@ -518,7 +518,7 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
     return e && e[0] == '1';
   }();
   const char* rows_env = std::getenv("DS_POOL_ROWS");  // output rows per thread: 1 or 2 (A/B)
-  const int prows = rows_env && rows_env[0] == '1' ? 1 : 2;
+  const int prows = rows_env ? std::atoi(rows_env) : 2;
   const int yrows = n * ((ho + prows - 1) / prows);
   if (!legacy && yrows <= 65535 && (stride == 1 || stride == 2) && wo * cg < (1 << 24)) {
     const int per_row = wo * cg;
@@ -532,6 +532,11 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
       if (stride == 1)
         return is_max ? go(pool3x3_rows_kernel<1, true, 1>) : go(pool3x3_rows_kernel<1, false, 1>);
       return is_max ? go(pool3x3_rows_kernel<2, true, 1>) : go(pool3x3_rows_kernel<2, false, 1>);
+    }
+    if (prows == 4) {
+      if (stride == 1)
+        return is_max ? go(pool3x3_rows_kernel<1, true, 4>) : go(pool3x3_rows_kernel<1, false, 4>);
+      return is_max ? go(pool3x3_rows_kernel<2, true, 4>) : go(pool3x3_rows_kernel<2, false, 4>);
     }
     if (stride == 1)
       return is_max ? go(pool3x3_rows_kernel<1, true, 2>) : go(pool3x3_rows_kernel<1, false, 2>);
