@@ -82,8 +82,8 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
   L.y_off += 4 * static_cast<uint32_t>((win_bytes + 1023) / 1024 * 1024);
   L.bar_off = L.y_off + epi_warps * y_bufs(epi_warps) * kYStageBytes;
   // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
-  // box_full[stages], win barriers[8], tmem slot
-  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2 + 8) * 8 + 15) / 16 * 16;
+  // box_full[stages], win barriers[8], tmem slot, residual-staging barriers[2 x 16 warps]
+  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2 + 8 + 32) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
   L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
@@ -873,6 +873,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* slot_full = raw_full;               // [4] direct mode: box landed
   uint64_t* slot_free = raw_full + 4;           // [4] direct mode: all taps consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cm_empty + 2);
+  uint64_t* res_bar = cm_empty + 3;  // [2 per epilogue warp] residual slice landed (res_tma)
 
   // warp index via a shuffle: provably warp-uniform, so role branches are
   // uniform and the MMA-issue loops keep their operands in uniform registers
@@ -923,6 +924,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         ptx::mbar_init(&tmem_empty[b], (kPD ? 8 : 4 * (args.teams > n_acc ? args.teams / n_acc : 1)) *
                                            (kPair ? 2 : 1));
       }
+      if (kRes && args.res_tma)
+        for (int b = 0; b < 2 * epi_warps; ++b) ptx::mbar_init(&res_bar[b], 1);
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&args.tmap_b);
       if (kTmaA || kBlk) ptx::tma_prefetch_desc(&args.tmap_a);  // (A / halo / tap boxes)
@@ -1002,6 +1005,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (static_cast<int>(j & (tile_teams - 1)) != team) continue;  // teams: power of two
       const int n0 = tw.nb * args.BN;
       const uint32_t acc = j & (n_acc - 1);
+      // residual-staging mode: this tile's first residual slice is TMA-loaded
+      // into the staging buffer it will be added in, before the accumulator
+      // wait (each later slice is loaded one slice ahead)
+      const bool rtma = kRes && narrow && args.res_tma != 0;
+      if (rtma && lane == 0) {
+        ptx::bulk_wait_read<0>();  // (the buffer's last store has read it)
+        const uint32_t b = groups & 1;
+        ptx::mbar_arrive_expect_tx(&res_bar[2 * warp + b], 2048);
+        ptx::tma_load_2d(ptx::smem_u32(ystage + b * buf_bytes), &args.tmap_r, &res_bar[2 * warp + b],
+                         n0 + part * part_cols, tw.mb * tile_rows + quarter * 32);
+      }
       if (kRes && args.residual) {
         // pull this lane's residual rows (its column part) into L2 a tile
         // ahead — this team's next tile (and, the first time, this one) — so
@@ -1056,7 +1070,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const int g_end = (part + 1) * part_cols;
           for (int g0 = part * part_cols; g0 < g_end && n0 + g0 < args.Cout; g0 += group_cols) {
             uint8_t* group = ystage + (nbufs == 2 ? (groups & 1) * buf_bytes : 0);
-            if (groups >= static_cast<uint32_t>(nbufs)) {  // the store that used `group` has read it
+            if (rtma) {
+              // next slice's residual into the other buffer once its store has read it
+              if (lane == 0 && g0 + group_cols < g_end && n0 + g0 + group_cols < args.Cout) {
+                ptx::bulk_wait_read<0>();
+                const uint32_t b = (groups + 1) & 1;
+                ptx::mbar_arrive_expect_tx(&res_bar[2 * warp + b], 2048);
+                ptx::tma_load_2d(ptx::smem_u32(ystage + b * buf_bytes), &args.tmap_r,
+                                 &res_bar[2 * warp + b], n0 + g0 + group_cols, m0 + quarter * 32);
+              }
+              __syncwarp();
+            } else if (groups >= static_cast<uint32_t>(nbufs)) {  // the store that used `group` has read it
               if (lane == 0) {
                 if (nbufs == 2)
                   ptx::bulk_wait_read<1>();
@@ -1068,7 +1092,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int c = 0; c < group_cols && g0 + c < g_end; c += 32) {
               // residual slice first: its global load overlaps the TMEM load
               uint4 res[4];
-              if (kRes && args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
+              if (rtma) {
+                ptx::mbar_wait(&res_bar[2 * warp + (groups & 1)], (groups >> 1) & 1);
+                const uint32_t row64 = ptx::smem_u32(group) + lane * 64;
+                const int sw64 = (lane >> 1) & 3;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(res[q].x), "=r"(res[q].y), "=r"(res[q].z), "=r"(res[q].w)
+                               : "r"(row64 + ((q ^ sw64) << 4)));
+              } else if (kRes && args.residual && m < args.M && n0 + g0 + c + 32 <= args.Cout) {
                 const uint4* rp = reinterpret_cast<const uint4*>(
                     args.residual + static_cast<size_t>(m) * args.ld_res + n0 + g0 + c);
 #pragma unroll
@@ -2023,6 +2056,18 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
                                static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
                                static_cast<uint64_t>(args.ldy)))
       args.y_narrow = 1;
+  }
+  // ... and residual layers stage each residual slice into that buffer by TMA
+  // (DS_RES_TMA=0: off)
+  args.res_tma = 0;
+  {
+    const char* e = std::getenv("DS_RES_TMA");
+    const bool on = !(e && e[0] == '0');
+    if (on && args.y_narrow && args.residual && args.mt == 1 &&
+        encode_tmap_out_narrow(&args.tmap_r, const_cast<__nv_bfloat16*>(args.residual),
+                               static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
+                               static_cast<uint64_t>(args.ld_res)))
+      args.res_tma = 1;
   }
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)

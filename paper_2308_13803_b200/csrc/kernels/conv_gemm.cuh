@@ -28,6 +28,8 @@ struct ConvGemmArgs {
   CUtensorMap tmap_y;  // output slice [rows][Cout] at y + c_off, 128 B x 32-row boxes (y_tma)
   int y_tma;           // epilogue stores through smem + TMA (else direct stores)
   int y_narrow;        // tmap_y has 32 x 32 boxes, 64 B swizzle (launch_conv_gemm sets it)
+  CUtensorMap tmap_r;  // residual with the same 32 x 32 boxes (res_tma)
+  int res_tma;         // epilogue stages residual slices by TMA (launch_conv_gemm sets it)
   const __nv_bfloat16* x;
   int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
   int R, S, stride_h, stride_w, pad_h, pad_w;

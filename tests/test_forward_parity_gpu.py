@@ -278,3 +278,18 @@ def test_depthwise_4channel_groups_match_8channel(monkeypatch, bs):
     with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
         g8 = be.forward(imgs)
     assert np.array_equal(g4, g8)
+
+
+def test_residual_tma_staging_matches_register_loads(monkeypatch):
+    """ResNet residual 1x1s with each 32-column residual slice TMA-loaded into
+    the epilogue's staging buffer (one slice ahead) against per-lane global
+    loads: the same bf16 residual added to the same fp32 sum, so
+    bit-identical logits."""
+    imgs = generate_images("resnet50_v1", 41, 3)
+    monkeypatch.setenv("DS_RES_TMA", "1")
+    with GpuBackend("resnet50_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
+        staged = be.forward(imgs)
+    monkeypatch.setenv("DS_RES_TMA", "0")
+    with GpuBackend("resnet50_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
+        loads = be.forward(imgs)
+    assert np.array_equal(staged, loads)
