@@ -2006,7 +2006,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     return e ? std::max(1, std::min(4, std::atoi(e))) : dflt;
   };
   const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
-                   teams_tma = env_int("DS_CONV_TEAMS_TMA", 2);
+                   teams_tma = env_int("DS_CONV_TEAMS_TMA", 4);
   const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
                      : (mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide)
                          ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
