@@ -53,12 +53,12 @@ __host__ __device__ constexpr int y_bufs(int epi_warps) { return epi_warps > 8 ?
 
 // Warp roles (kConvThreads = 18 warps).
 constexpr int kEpiWarps = 8;      // warps 0-7: epilogue (two teams of four)
-constexpr int kMaxEpiWarps = 16;  // TMA-A mode: the idle gather warps join (four teams)
+// (TMA-A modes: the idle gather warps 8-15 join as epilogue teams 2-3)
 constexpr int kMaxAcc = 8;        // TMEM accumulators (tmem_full/tmem_empty barrier pairs)
 constexpr int kGatherWarp0 = 8;   // warps 8-15: A gather
 constexpr int kGatherWarps = 8;
 constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
-constexpr int kMmaWarp = 17;      // tcgen05.mma issuer
+// warp 17: tcgen05.mma issuer (the role branch's final else)
 
 struct SmemLayout {
   uint32_t a_off, b_off, box_off, win_off, y_off, bar_off, bias_off, total;
@@ -241,15 +241,6 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
       }
     }
     ptx::cp_async_mbar_arrive_noinc(&full[s]);
-  }
-}
-
-__device__ __forceinline__ void unpack8_bf16(const uint4& u, float (&f)[8]) {
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    f[2 * e] = __uint_as_float(w[e] << 16);
-    f[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
   }
 }
 
