@@ -85,9 +85,11 @@ bool s2d_tap_boxes() {
 
 // Stride-1 R x S convs as kWindow (shifted-window MMAs, no im2col). Default:
 // only where the halo box is read in place (C % 64 == 0) and the map is at
-// least 28 x 28 (the 16 x 8 pixel tiles waste few MMA rows there): ResNet's
-// 56^2 3x3s run in half the gather's time; on 14^2 / 7^2 maps and with the
-// transposed (C % 64 != 0) boxes the im2col gather is still faster.
+// least 56 x 56: ResNet's 56^2 3x3s run in 44 % of the gather's time, but at
+// 28^2 the gather wins (76 vs 88 us: with 128 channels the weights stream per
+// tap, 288 KB per 128-pixel tile, and the 16 x 8 tiles waste a third of the
+// rows); with the transposed (C % 64 != 0) boxes the gather is always faster.
+// DS_CONV_WINDOW_MIN overrides the map side.
 // DS_CONV_WINDOW=1: every eligible conv; DS_CONV_WINDOW=0: none (A/B).
 int window_mode() {
   const int m = [] {
@@ -106,7 +108,9 @@ bool narrow_window_on() {
 
 bool window_on(int c, int ho, int wo) {
   const int m = window_mode();
-  return m == 1 || (m == 2 && c % 64 == 0 && ho >= 28 && wo >= 28);
+  const char* e = std::getenv("DS_CONV_WINDOW_MIN");  // smallest map side (A/B)
+  const int min_side = e ? std::atoi(e) : 56;
+  return m == 1 || (m == 2 && c % 64 == 0 && ho >= min_side && wo >= min_side);
 }
 
 }  // namespace
