@@ -809,7 +809,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // channels, and whose epilogue runs the following depthwise 3x3 on it
   constexpr bool kPD = MODE == static_cast<int>(ConvLoadMode::kPwDw) ||
                       MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
-  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kPD;
+  // kIm2col: R x S / strided convs whose A blocks are TMA im2col loads (one per
+  // (tap, 64-channel block)); otherwise the TMA-A machinery
+  constexpr bool kI2C = MODE == static_cast<int>(ConvLoadMode::kIm2col);
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kPD || kI2C;
   // residual adds are compiled into the 1x1 modes only (the runtime routes
   // every residual conv there); the other modes carry none of that state
   constexpr bool kRes = kTmaA && !kPD;
@@ -1383,7 +1386,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                              kb * kConvBK, n0);
           }
-          if constexpr (kTmaA)
+          if constexpr (kI2C) {
+            // K block kb = (tap t, channel block cb); sub-tile q starts at output
+            // pixel m0 + 128 q, whose input window origin is (wo*sw - pw, ho*sh - ph)
+            const int cbs = args.C >> 6;
+            const int t = kb / cbs, cb = kb - t * cbs;
+            const int tr = t / args.S, tc = t - tr * args.S;
+            const int hw_o = args.Ho * args.Wo;
+            for (int q = 0; q < mt; ++q) {
+              const int mq = m0 + q * kConvBM;
+              const int n = mq / hw_o, rem = mq - n * hw_o;
+              const int ho = rem / args.Wo, wo = rem - ho * args.Wo;
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(
+                      ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes)),
+                  "l"(&args.tmap_a), "r"(cb * 64), "r"(wo * args.stride_w - args.pad_w),
+                  "r"(ho * args.stride_h - args.pad_h), "r"(n), "r"(ptx::smem_u32(&full[s])),
+                  "h"(static_cast<uint16_t>(tc)), "h"(static_cast<uint16_t>(tr))
+                  : "memory");
+            }
+          } else if constexpr (kTmaA)
             for (int q = 0; q < mt; ++q)  // (rows past M arrive as zeros)
               ptx::tma_load_2d(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes),
                                &args.tmap_a, &full[s], kb * kConvBK, m0 + q * kConvBM);
@@ -1706,7 +1729,46 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn get_encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
 }  // namespace
+
+bool encode_tmap_im2col(CUtensorMap* map, const void* base, int n, int h, int w, int c, int r, int s,
+                        int stride_h, int stride_w, int pad_h, int pad_w) {
+  EncodeIm2colFn fn = get_encode_im2col_fn();
+  if (!fn || c % 64 != 0 || pad_h > 127 || pad_w > 127 || stride_h > 8 || stride_w > 8) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
+                              static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2,
+                                 static_cast<cuuint64_t>(c) * 2 * w,
+                                 static_cast<cuuint64_t>(c) * 2 * w * h};
+  // the window origins walk [-pad, extent + pad - filter] (W first, then H)
+  const int lower[2] = {-pad_w, -pad_h};
+  const int upper[2] = {pad_w - (s - 1), pad_h - (r - 1)};
+  const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(stride_w), static_cast<cuuint32_t>(stride_h), 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower,
+            upper, 64u, static_cast<cuuint32_t>(kConvBM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                          uint64_t row_stride_elems, uint32_t box_rows) {
@@ -1958,6 +2020,9 @@ cudaError_t conv_gemm_init() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(conv_gemm_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                cap);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_gemm_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               cap);
     return e;
   }();
   return status;
@@ -2002,7 +2067,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
                      : (mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide)
                          ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
                      : mode == ConvLoadMode::kStemU8 ? mt_stem
-                     : mode == ConvLoadMode::kTmaA ? mt_tma
+                     : (mode == ConvLoadMode::kTmaA || mode == ConvLoadMode::kIm2col) ? mt_tma
                                                    : 1;
   args.mt = 1;
   while (args.mt * 2 <= mt_cap && args.mt * 2 * static_cast<int>(pow2_at_least(args.BN)) <= 256)
@@ -2015,7 +2080,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const uint32_t acc_cols = pow2_at_least(args.mt * args.BN);
   args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / acc_cols)));
   args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(acc_cols));
-  args.teams = std::min((mode == ConvLoadMode::kTmaA || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
+  const bool tmaa = mode == ConvLoadMode::kTmaA || mode == ConvLoadMode::kIm2col;
+  args.teams = std::min((tmaa || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
   if (args.teams == 3) args.teams = 2;  // a power of two
   if (pd) args.teams = 4;  // sixteen epilogue warps = two teams of eight (pwdw_epilogue)
@@ -2030,7 +2096,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const char* e = std::getenv("DS_CONV_TPA");
     return !(e && e[0] == '0');
   }();
-  if (tpa_on && (mode == ConvLoadMode::kTmaA || pair) && args.BN >= 128 && args.n_acc == 2 &&
+  if (tpa_on && (tmaa || pair) && args.BN >= 128 && args.n_acc == 2 &&
       args.BN % (2 * group_cols) == 0)
     args.teams = 4;
   // sixteen epilogue warps (one staging buffer each at 64-column groups):
@@ -2200,6 +2266,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return launch_pdl(conv_gemm_kernel<8>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kPairPwDw:
       break;  // (launched above)
+    case ConvLoadMode::kIm2col:
+      return launch_pdl(conv_gemm_kernel<12>, grid, dim3(kConvThreads), smem, stream, args);
   }
   return cudaGetLastError();
 }

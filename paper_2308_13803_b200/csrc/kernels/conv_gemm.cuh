@@ -106,7 +106,14 @@ enum class ConvLoadMode : int {
   kS2DWide = 10,  // kS2D window MMAs for 16 / 32-channel stride-1 3x3 convs (one halo box
                   // per 16-channel block, padding as negative box coordinates)
   kWindowT = 11,  // (internal) kWindow with transposed boxes: launch as kWindow, win_direct 0
+  kIm2col = 12,   // R x S / strided convs with C % 64 == 0: A blocks by TMA im2col loads
+                  // (tmap_a from encode_tmap_im2col), then the TMA-A pipeline
 };
+
+// Im2col map over an NHWC bf16 activation for an R x S conv (stride, padding):
+// 64-channel x 128-output-pixel blocks, 128 B swizzle.
+bool encode_tmap_im2col(CUtensorMap* map, const void* base, int n, int h, int w, int c, int r, int s,
+                        int stride_h, int stride_w, int pad_h, int pad_w);
 
 // Whether a 1x1 conv (ho x wo output, cout channels, N tile bn) and its
 // depthwise successor can run as one kPwDw launch.

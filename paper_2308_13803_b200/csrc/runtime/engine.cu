@@ -106,6 +106,15 @@ bool narrow_window_on() {
   return !(e && e[0] == '0');
 }
 
+// TMA im2col for convs with C % 64 == 0 on maps of at least 28 x 28 (ResNet's
+// 28^2 3x3s: 77 -> 70 us); on 17^2 and smaller maps the cp.async gather of
+// eight warps is faster than the TMA unit's per-pixel im2col walk (Inception
+// 17^2: 28.7 vs 36.9 us). DS_CONV_IM2COL=0: all on the gather.
+bool im2col_on() {
+  const char* e = std::getenv("DS_CONV_IM2COL");
+  return !(e && e[0] == '0');
+}
+
 bool window_on(int c, int ho, int wo) {
   const int m = window_mode();
   const char* e = std::getenv("DS_CONV_WINDOW_MIN");  // smallest map side (A/B)
@@ -390,6 +399,13 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       // A is a plain [pixels][C] matrix; for C < 64 the TMA box runs past
       // the row and the out-of-bounds columns arrive as zeros.
       pl.mode = ConvLoadMode::kTmaA;
+    } else if (im2col_on() && in.c % 64 == 0 && op.kind == OpKind::kConv && !out.f32 &&
+               out.h >= 28 && out.w >= 28 &&
+               encode_tmap_im2col(&a.tmap_a, bufs_[op.in], max_bs, in.h, in.w, in.c, op.r, op.s,
+                                  op.sh, op.sw, op.ph, op.pw)) {
+      // R x S / strided conv over 64-channel blocks: each K block's A tile is one
+      // TMA im2col load (the hardware walks the 128 output pixels' windows)
+      pl.mode = ConvLoadMode::kIm2col;
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }

@@ -293,3 +293,20 @@ def test_residual_tma_staging_matches_register_loads(monkeypatch):
     with GpuBackend("resnet50_v1", Config(abs_max_bs=4, max_mtl=1)) as be:
         loads = be.forward(imgs)
     assert np.array_equal(staged, loads)
+
+
+@pytest.mark.parametrize("model,bs", [("resnet50_v1", 3), ("inception_v3", 2)])
+def test_tma_im2col_matches_gather(monkeypatch, model, bs):
+    """Convs with C % 64 == 0 whose A blocks are TMA im2col loads (the tensor
+    map walks 128 output pixels' windows for one tap and 64 channels, padding
+    and stride in the map) against the cp.async gather: the same K order, so
+    bit-identical logits."""
+    imgs = generate_images(model, 43, bs)
+    monkeypatch.setenv("DS_CONV_IM2COL", "1")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        tma = be.forward(imgs)
+    monkeypatch.setenv("DS_CONV_IM2COL", "0")
+    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
+        gather = be.forward(imgs)
+    assert np.isfinite(tma).all()
+    assert np.array_equal(tma, gather)
