@@ -448,7 +448,11 @@ DwKernelArgs make_args(const DwPlan& p, int n, int h, int w, int c, int stride) 
   a.div_sp = make_fastdiv(static_cast<uint32_t>(a.tiles_x * a.tiles_y * a.tiles_n));
   a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.nb * p.cb * 2);
   // 2-4 boxes in flight, <= ~72 KB per CTA so three CTAs share an SM.
-  a.stages = std::max(2, std::min(4, static_cast<int>((72 * 1024) / a.box_bytes)));
+  const char* kb_env = std::getenv("DS_DW_STAGE_KB");  // ring budget per CTA (A/B)
+  const int budget = (kb_env ? std::atoi(kb_env) : 72) * 1024;
+  const char* st_env = std::getenv("DS_DW_MAX_STAGES");
+  const int max_st = st_env ? std::atoi(st_env) : 4;
+  a.stages = std::max(2, std::min(max_st, static_cast<int>(budget / a.box_bytes)));
   return a;
 }
 
