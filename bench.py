@@ -2,7 +2,7 @@
 """DNNScaler on B200 — headline benchmark.
 
 Metric (BASELINE.json): inferences/sec at p95 latency SLO (Batching vs
-Multi-Tenancy). N=1 workload = configs[1]: MobileNet-v1 224x224 synthetic
+Multi-Tenancy). Headline (N=1) = configs[1]: MobileNet-v1 224x224 synthetic
 images, Profiler + Scaler on one B200 (m=32, n=8, abs_max_bs=128,
 max_mtl=10, window=100, alpha=0.85), SLO = 13.44 x L(BS=1) measured on the
 device at start (paper's job-18 ratio).
@@ -20,12 +20,19 @@ timed with cudaEvents (drain + event at both ends, max over ranks).
                launches in one forward at the steady knob), timed live with
                event nodes between kernels
   cpu_baseline FP32 C oracle forward (port) on this host, bounded sample
+  configs      the other BASELINE configs measured in the same run (--configs):
+               1 synthetic CNN DNNScaler; 3 ResNet-50 batching sweep 1-256 +
+               DNNScaler abs_max_bs=256; 4 Inception-v3 MT sweep 1-16 +
+               DNNScaler max_mtl=16; 5 the mixed 18-job trace LPT-sharded over
+               the ranks (strong scaling) — each with p95, SLO, knob, the
+               network roofline fraction, e2e and a CPU baseline
 
 --impl reference: the reference's CPU path on this host — the compiled,
 unmodified reference control plane (oracle/_ref) driving the FP32 C oracle
 forward pass (the reference has no forward pass of its own).
-Multi-GPU (torchrun): one independent replica per GPU (weak scaling, no
-collective on the data path); value = sum of items / max elapsed.
+Multi-GPU (torchrun): one independent replica per GPU for the headline (weak
+scaling, no collective on the data path; value = sum of items / max elapsed)
+and config 5's trace sharded over the GPUs.
 """
 from __future__ import annotations
 
@@ -41,12 +48,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-
-SLO_FACTOR = {"mobilenet_v1": 13.44, "resnet50_v1": 4.66, "inception_v3": 22.54,
-              "synthetic_cnn": 4.15}
-MODEL_LIMITS = {"mobilenet_v1": (128, 10), "resnet50_v1": (256, 10), "inception_v3": (128, 16),
-                "synthetic_cnn": (32, 4)}
-PROBE = {"synthetic_cnn": (32, 4)}  # (m, n); default (32, 8)
 
 
 def dist_setup(gpus):
@@ -157,24 +158,12 @@ class EnergyMeter:
             return None
 
 
-def nearest_rank_p95(x):
-    x = np.sort(np.asarray(x))
-    rank = int(np.ceil(0.95 * len(x) - 1e-9))
-    return float(x[max(1, min(rank, len(x))) - 1])
-
-
-def load_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            p = json.load(f)
-        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
-    return 6650.0, 1590.0, 1400.0, "fallback"
-
-
-def roofline(be, model, knob, kernel_costs):
-    """Dominant kernel (implicit-GEMM conv) at the steady knob, timed live."""
-    bs = knob[1] if knob[0] == 0 else 1
+def roofline(be, model, bs, kernel_costs, conv_ms_live=None):
+    """Dominant kernel (tcgen05 implicit-GEMM conv) at the steady batch: its
+    launches of one forward timed live (event nodes between kernels, which add
+    ~5 us each — DESIGN.md §6), algorithmic bytes / flops per forward from
+    ds_model_kernels, against the measured peaks."""
+    from paper_2308_13803_b200 import serving as S
     ms = be.profile_kernels(bs, reps=20)
     conv = [i for i, k in enumerate(kernel_costs) if k["kind"] == "conv_gemm"]
     conv_ms = float(sum(ms[i] for i in conv))
@@ -182,7 +171,7 @@ def roofline(be, model, knob, kernel_costs):
                      for i in conv)
     conv_flops = sum(bs * kernel_costs[i]["flops_per_image"] for i in conv)
     fwd_ms = float(ms.sum())
-    hbm, tflops, tflops_sus, src = load_peaks()
+    hbm, tflops, tflops_sus, src = S.load_peaks()
     ai = conv_flops / conv_bytes
     ridge = tflops * 1e12 / (hbm * 1e9)
     per_launch = [dict(kernel=i, kind=kernel_costs[i]["kind"], ms=float(ms[i]),
@@ -210,8 +199,9 @@ def roofline(be, model, knob, kernel_costs):
               "peak_source": src, "batch": bs, "launches": len(conv),
               "algorithmic_bytes": conv_bytes, "algorithmic_flops": conv_flops,
               "arith_intensity": round(ai, 1), "ridge": round(ridge, 1),
-              "kernel_ms": round(conv_ms, 4), "forward_ms": round(fwd_ms, 4),
+              "kernel_ms": round(conv_ms, 4), "forward_ms_profiled": round(fwd_ms, 4),
               "share_of_forward": round(conv_ms / fwd_ms, 4),
+              "tensor_frac": round(conv_flops / (conv_ms * 1e-3) / 1e12 / tflops, 4),
               "forward_hbm_frac": round(
                   (sum(bs * k["bytes_per_image"] + k["fixed_bytes"] for k in kernel_costs)
                    / (fwd_ms * 1e-3) / 1e9) / hbm, 4)})
@@ -238,112 +228,201 @@ def cpu_baseline(model, seconds=12.0):
                       f"(oracle/fwd_oracle.c), {threads} threads, {dt:.1f} s"}
 
 
-def build_catalog(be, model, m, n):
-    """The served model's catalog row, measured on the device (B200 curves),
-    plus the paper's P40 rows as matrix-completion donors."""
+def _nvtx(tag, push):
+    from paper_2308_13803_b200 import _lib as L
+    if push:
+        L.load().ds_nvtx_push(tag.encode())
+    else:
+        L.load().ds_nvtx_pop()
+
+
+def serve_line(args, model, be, *, controller, knob=None, slo_factor=None, limits=None,
+               probe=None, local=0, dist=None, steps=None, warmup=None, e2e=True):
+    """One job on `be`, timed; returns (result dict, clocks, energy)."""
+    from paper_2308_13803_b200 import serving as S
+    box = {}
+
+    def between(timed_fn):
+        barrier(dist)
+        sampler = ClockSampler(local)
+        meter = EnergyMeter(local)
+        sampler.start()
+        e0 = meter.read_mj()
+        r = timed_fn()
+        e1 = meter.read_mj()
+        box["clocks"] = sampler.stop()
+        box["energy"] = None
+        if e0 is not None and e1 is not None and e1 > e0:
+            joules = (e1 - e0) / 1000.0
+            box["energy"] = {"joules": round(joules, 3), "avg_power_w": round(joules / (r[1] * 1e-3), 1),
+                             "inferences_per_joule": round(r[0] / joules, 1),
+                             "source": "NVML total energy counter over the timed periods (board)"}
+        return r
+
+    res = S.serve(be, model, controller=controller, slo_factor=slo_factor, limits=limits,
+                  probe=probe, steps=steps or args.steps, warmup=warmup or args.warmup,
+                  max_converge=args.max_converge, knob=knob, e2e=e2e, nvtx=_nvtx, between=between)
+    return res, box.get("clocks"), box.get("energy")
+
+
+def workload_name(model, res, info, slo_factor):
+    ctl = {"dnnscaler": "DNNScaler Profiler+Scaler", "clipper": "Clipper AIMD",
+           "static": "static knob (no search)"}[res["controller"]]
+    if res["controller"] == "static":
+        k = res["static_knob"]
+        ctl += f" {'batching' if k[0] == 0 else 'multi-tenancy'}={k[1]}"
+    return f"{model} {info.in_h}x{info.in_w}, {ctl}, SLO = {slo_factor} x L(BS=1)"
+
+
+def compact(res, model, info, slo_factor, extra=None):
+    """A config's result in the bench line's vocabulary."""
+    out = {
+        "workload": workload_name(model, res, info, slo_factor),
+        "value": round(res["value"], 2), "unit": "inferences/s",
+        "knob": res["knob"], "slo_ms": round(res["slo_ms"], 4), "l1_ms": round(res["l1_ms"], 4),
+        "p95_ms_timed": round(res["p95_ms_timed"], 4), "p95_within_slo": res["p95_within_slo"],
+        "roofline": {"img_s": round(res["roofline_img_s"], 1),
+                     "achieved_frac": round(res["roofline_achieved_frac"], 4),
+                     "basis": "SURVEY 8(d): sum over kernels of max(flops/peak, bytes/HBM) "
+                              "at the operating batch (MT: bs 1)"},
+        "profiler": ({k: (round(v, 2) if isinstance(v, float) else v)
+                      for k, v in res["profiler"].items()} if res["profiler"] else None),
+        "knob_trajectory": res["knob_trajectory"],
+        "gpu_launches": res["launches"],
+    }
+    if "e_items" in res:
+        out["e2e"] = {"value": round(res["e_items"] / (res["e_ms"] * 1e-3), 2), "unit": "inferences/s",
+                      "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]}
+    if extra:
+        out.update(extra)
+    return out
+
+
+def config1(args, local):
+    """Synthetic CNN, DNNScaler m=32 n=4, abs_max_bs=32, max_mtl=4."""
+    from paper_2308_13803_b200 import Config, GpuBackend
+    from paper_2308_13803_b200 import serving as S
+    model = "synthetic_cnn"
+    with GpuBackend(model, Config(*S.MODEL_LIMITS[model]), device=local) as be:
+        res, _, _ = serve_line(args, model, be, controller="dnnscaler", local=local)
+        info = be.info
+    return compact(res, model, info, S.SLO_FACTOR[model])
+
+
+def config3(args, local):
+    """ResNet-50 v1: batching sweep 1..256 (static knob) + DNNScaler abs_max_bs=256."""
+    from paper_2308_13803_b200 import Config, GpuBackend
+    from paper_2308_13803_b200 import serving as S
+    model = "resnet50_v1"
+    with GpuBackend(model, Config(256, 10), device=local) as be:
+        res, _, _ = serve_line(args, model, be, controller="dnnscaler", limits=(256, 10), local=local)
+        sweep = S.batch_sweep(be, [1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256], calls=20)
+        info = be.info
+    best = S.best_under_slo(sweep, "bs", res["slo_ms"])
+    return compact(res, model, info, S.SLO_FACTOR[model], {
+        "batching_sweep": sweep,
+        "sweep_best_under_slo": best,
+        "scaler_vs_sweep_best": round(res["value"] / best["measured_throughput"], 4) if best else None})
+
+
+def config4(args, local):
+    """Inception-v3: multi-tenancy sweep 1..16 (static knob) + DNNScaler max_mtl=16."""
+    from paper_2308_13803_b200 import Config, GpuBackend
+    from paper_2308_13803_b200 import serving as S
+    model = "inception_v3"
+    with GpuBackend(model, Config(128, 16), device=local) as be:
+        res, _, _ = serve_line(args, model, be, controller="dnnscaler", limits=(128, 16), local=local)
+        sweep = S.mt_sweep(be, list(range(1, 17)), calls_per_instance=10)
+        best = S.best_under_slo(sweep, "mtl", res["slo_ms"])
+        # the MT knob under the Scaler's own AIMD loop (static MT start, Scaler free)
+        forced = None
+        if best:
+            fres, _, _ = serve_line(args, model, be, controller="static",
+                                    knob=("multi-tenancy", best["mtl"]), limits=(128, 16),
+                                    local=local, e2e=False)
+            forced = {"knob": fres["knob"], "value": round(fres["value"], 2),
+                      "p95_ms_timed": round(fres["p95_ms_timed"], 4),
+                      "p95_within_slo": fres["p95_within_slo"],
+                      "roofline_achieved_frac": round(fres["roofline_achieved_frac"], 4)}
+        info = be.info
+    return compact(res, model, info, S.SLO_FACTOR[model], {
+        "mt_sweep": sweep, "sweep_best_under_slo": best, "mt_at_best_k_static": forced})
+
+
+def config5(args, rank, world, local, dist):
+    """Mixed trace (the reference's 30-job scenario restricted to the built
+    families, per-job SLO tightness kept), LPT-sharded over the ranks; each
+    rank runs its jobs sequentially on fresh backends (replicas, no
+    collective); value = sum of items / makespan (slowest rank's device time)."""
     from paper_2308_13803_b200 import control as C
-    be.run_batches(1, 10)
-    l1 = float(np.median(be.run_batches(1, 50)))
-    lat_m = float(np.median(be.run_batches(m, 20)))
-    be.set_mtl(n)
-    be.run_mt_requests(4 * n)
-    mt = be.run_mt_requests(20 * n)
-    be.set_mtl(1)
-    # The reference catalog schema needs an increasing, non-negative-intercept
-    # batch cost (perf_model.cpp:37-44); keep the measured row inside it even
-    # when a profiler distorts the timings.
-    lat_m = min(max(lat_m, l1 * 1.001), m * l1 * 0.999)
-    t1 = 1000.0 / l1
-    t_mt = max(mt.size * 1000.0 / (mt.sum() / n), t1 * 1.0001)
-    row = C.DnnProfile(model, [(1, t1), (m, m * 1000.0 / lat_m)], [(1, t1), (n, t_mt)])
-    donors = C.load_catalog(os.path.join(ROOT, "paper_2308_13803_b200", "data", "p40_donors.json"))
-    return l1, [row] + donors
+    from paper_2308_13803_b200 import replicas as R
+    from paper_2308_13803_b200 import serving as S
+    b200 = C.load_catalog(S.B200_CATALOG)
+    sc, jobs = R.mixed_trace(b200, C.load_catalog(S.P40_DONORS), args.trace_scale)
+    mine = R.shard_jobs(jobs, world)[rank]
+    t0 = time.perf_counter()
+    out = R.run_shard(rank, mine, sc, b200, seam="device", device=local)
+    wall = time.perf_counter() - t0
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (out, wall))
+    else:
+        gathered = [(out, wall)]
+    flat = sorted([o for part, _ in gathered for o in part], key=lambda o: o.job_id)
+    agg = R.aggregate(flat, world)
+    return {
+        "workload": f"mixed trace: {len(jobs)} jobs of scenario_30jobs.json (mobv1 -> mobilenet_v1, "
+                    f"resv2 -> resnet50_v1, inc -> inception_v3), per-job SLO = c_job x L_B200(BS=1), "
+                    f"durations x {args.trace_scale:g}, LPT over {world} GPU(s)",
+        "value": round(agg["inferences_per_s"], 2), "unit": "inferences/s",
+        "scaling": "strong (fixed trace)",
+        "items": agg["items"], "makespan_s": round(agg["makespan_s"], 4),
+        "wall_s_per_rank": [round(w, 2) for _, w in gathered],
+        "jobs": agg["jobs"], "failed": agg["failed"],
+        "slo_compliance_mean": round(float(np.mean([o.slo_compliance for o in flat])), 4),
+        "per_job": [{"job": o.job_id, "model": o.dnn_id, "rank": o.rank,
+                     "knob": list(o.steady_knob), "steady_tput": round(o.steady_throughput, 1),
+                     "items": o.total_items, "device_s": round(o.duration_s, 3),
+                     "slo_compliance": round(o.slo_compliance, 4), "error": o.error} for o in flat],
+        "timing": "per-job virtual clock = sum of cudaEvent request latencies + measured "
+                  "instance-change delays (device time); makespan = max over ranks",
+    }
 
 
 def run_ours(args, rank, world, local, dist):
     from paper_2308_13803_b200 import Config, GpuBackend
-    from paper_2308_13803_b200 import control as C
+    from paper_2308_13803_b200 import serving as S
     from paper_2308_13803_b200.backend import kernel_costs
 
     model = args.model
-    max_bs, max_mtl = MODEL_LIMITS[model]
-    m, n = PROBE.get(model, (32, 8))
-    window = 100
+    max_bs, max_mtl = S.MODEL_LIMITS[model]
     be = GpuBackend(model, Config(max_bs, max_mtl), seed=42 + rank, device=local)
-    l1, catalog = build_catalog(be, model, m, n)
-    slo = SLO_FACTOR[model] * l1
-    sc = C.Scenario(controller=args.controller, seed=42, alpha=0.85, m=m, n=n,
-                    abs_max_bs=max_bs, max_mtl=max_mtl, window=window)
-    if args.knob:  # static knob (profiling runs): skips the Profiler/Scaler search
+    knob = None
+    if args.knob:  # static knob (profiling runs): the reference's kStaticKnob controller
         kind, value = args.knob.split(":")
-        sc.controller = "static"
-        sc.static_knob = (0 if kind == "batching" else 1, int(value))
-    job = C.JobSpec(1 + rank, model, slo, 1e9)
-    sess = C.JobSession(sc, job, catalog, seam="device", backend=be)
-    # converge: until the knob holds for 3 periods
-    knobs = []
-    for _ in range(args.max_converge):
-        rec, _ = sess.step()
-        knobs.append(rec["knob"])
-        if len(knobs) >= 4 and knobs[-1] == knobs[-2] == knobs[-3] == knobs[-4]:
-            break
-    for _ in range(args.warmup):
-        sess.step()
-
-    from paper_2308_13803_b200 import _lib as L
-
-    def timed(steps, tag):
-        items = 0.0
-        st0 = be.stats()
-        barrier(dist)
-        be.timer_start()
-        L.load().ds_nvtx_push(tag.encode())
-        recs = []
-        for _ in range(steps):
-            rec, _ = sess.step()
-            recs.append(rec)
-            k = rec["knob"]
-            items += window * (k[1] if k[0] == 0 else 1)
-        ms = be.timer_stop()
-        L.load().ds_nvtx_pop()
-        st1 = be.stats()
-        return items, ms, recs, st0, st1
-
-    sampler = ClockSampler(local)
-    meter = EnergyMeter(local)
-    sampler.start()
-    e_start = meter.read_mj()
-    items, ms, recs, st0, st1 = timed(args.steps, "timed")
-    e_end = meter.read_mj()
-    clocks = sampler.stop()
-    energy = None
-    if e_start is not None and e_end is not None and e_end > e_start:
-        joules = (e_end - e_start) / 1000.0
-        energy = {"joules": round(joules, 3), "avg_power_w": round(joules / (ms * 1e-3), 1),
-                  "inferences_per_joule": round(items / joules, 1),
-                  "source": "NVML total energy counter over the timed periods (board power)"}
-    # e2e through host buffers, same session (the Scaler keeps control)
-    be.set_host_io(True)
-    e_warm = max(1, args.warmup // 2)
-    for _ in range(e_warm):
-        sess.step()
-    e_items, e_ms, e_recs, e0, e1 = timed(args.steps, "timed_e2e")
-    be.set_host_io(False)
-    res = sess.finish()
-    tail = (e_warm + args.steps) * window  # latencies served after the timed region
-    end = res.latencies.size - tail
-    timed_lat = res.latencies[end - args.steps * window:end]
-    knob = recs[-1]["knob"]
+        knob = (kind, int(value))
+    res, clocks, energy = serve_line(args, model, be, controller=args.controller, knob=knob,
+                                     local=local, dist=dist)
+    k = res["knob"]
+    bs_op = k["value"] if k["kind"] == "batching" else 1
     costs = kernel_costs(model)
-    rl, per_launch = roofline(be, model, knob, costs) if rank == 0 else (None, None)
-    (max_ms, max_ems), (sum_items, sum_eitems) = reduce_max_sum(dist, local, [ms, e_ms],
-                                                                [items, e_items])
+    rl, per_launch = roofline(be, model, bs_op, costs) if rank == 0 else (None, None)
+    (max_ms, max_ems), (sum_items, sum_eitems) = reduce_max_sum(
+        dist, local, [res["ms"], res["e_ms"]], [res["items"], res["e_items"]])
     value = sum_items / (max_ms * 1e-3)
     e2e = sum_eitems / (max_ems * 1e-3)
+    info = be.info
+    be.close()
+    extra = {}
+    if args.configs:
+        wanted = [c.strip() for c in args.configs.split(",") if c.strip()]
+        for c in wanted:
+            if c == "5":
+                extra["5"] = config5(args, rank, world, local, dist)
+            elif rank == 0 and world == 1:
+                extra[c] = {"1": config1, "3": config3, "4": config4}[c](args, local)
     if rank != 0:
         return None
-    rep = res.report
-    info = be.info
     fwd_flops = 2 * info.macs_per_image
     out = {
         "metric": "inferences/sec at p95 latency SLO (Batching vs Multi-Tenancy), 1/2/4/8 B200",
@@ -357,49 +436,51 @@ def run_ours(args, rank, world, local, dist):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (seeded u8 images, seeded He-init weights with folded BN; DESIGN.md)",
+        "data": "synthetic (seeded textured u8 images, seeded He-init weights with folded BN, "
+                "calibrated classifier head; DESIGN.md §5)",
         "config": {
-            "workload": f"{model} {info.in_h}x{info.in_w}, "
-                        f"{'DNNScaler Profiler+Scaler' if args.controller == 'dnnscaler' else 'Clipper AIMD'}, "
-                        f"SLO = {SLO_FACTOR[model]} x L(BS=1)",
+            "workload": workload_name(model, res, info, S.SLO_FACTOR[model]),
             "model": model,
-            "global_batch": knob[1] if knob[0] == 0 else knob[1] * world,
-            "knob": {"kind": "batching" if knob[0] == 0 else "multi-tenancy", "value": knob[1]},
-            "slo_ms": round(slo, 4),
-            "l1_ms": round(l1, 4),
-            "p95_ms_timed": round(nearest_rank_p95(timed_lat), 4),
-            "p95_within_slo": bool(nearest_rank_p95(timed_lat) <= slo),
-            "profiler": {"ti_batching": round(rep.get("ti_batching", 0.0), 2),
-                         "ti_mt": round(rep.get("ti_mt", 0.0), 2),
-                         "approach": res.summary["approach_kind"] and "multi-tenancy" or "batching",
-                         "tput_base": round(rep.get("tput_base", 0.0), 1),
-                         "tput_batching": round(rep.get("tput_batching", 0.0), 1),
-                         "tput_mt": round(rep.get("tput_mt", 0.0), 1)}
-            if args.controller == "dnnscaler" else None,
-            "controller": args.controller,
-            "knob_trajectory": [list(k) for k in knobs],
-            "scenario": {"m": m, "n": n, "abs_max_bs": max_bs, "max_mtl": max_mtl,
-                         "window": window, "alpha": 0.85},
+            "global_batch": bs_op * world,
+            "knob": k,
+            "slo_ms": round(res["slo_ms"], 4),
+            "l1_ms": round(res["l1_ms"], 4),
+            "p95_ms_timed": round(res["p95_ms_timed"], 4),
+            "p95_within_slo": res["p95_within_slo"],
+            "profiler": ({kk: (round(v, 2) if isinstance(v, float) else v)
+                          for kk, v in res["profiler"].items()} if res["profiler"] else None),
+            "controller": res["controller"],
+            "static_knob": res["static_knob"],
+            "knob_trajectory": res["knob_trajectory"],
+            "scenario": res["scenario"],
             "parallelism": f"replicas x{world} (no collective on the data path)",
-            "l2": "working set per step > 126 MB L2 (bs x 21 MB activations per MobileNet image)"
-                  if knob[0] == 0 and knob[1] >= 8 else "bs=1 requests; weights L2-resident",
+            "l2": (f"working set per step > 126 MB L2 ({bs_op} x "
+                   f"{info.act_bytes_per_image / 1e6:.1f} MB activations per image)"
+                   if bs_op * info.act_bytes_per_image > 126e6
+                   else "small batches: weights and activations partly L2-resident"),
             "fwd_gflop_per_image": round(fwd_flops / 1e9, 4),
             "achieved_tflops_whole_forward": round(value * fwd_flops / 1e12, 2),
+            "network_roofline": {"img_s": round(res["roofline_img_s"], 1),
+                                 "achieved_frac": round(value / world / res["roofline_img_s"], 4)},
         },
         "e2e": {"value": round(e2e, 2), "unit": "inferences/s",
-                "h2d_bytes_per_step": int((e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps),
-                "d2h_bytes_per_step": int((e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps),
-                "knob": list(e_recs[-1]["knob"])},
-        "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+                "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
+                "knob": res["e_knob"]},
+        "gpu_launches": res["launches"],
         "roofline": rl,
         "clocks": clocks,
         "energy": energy,
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(model, args.cpu_seconds)
+    if extra:
+        out["configs"] = extra
+        if world == 1 and not args.no_cpu_baseline:
+            for c, m in (("1", "synthetic_cnn"), ("3", "resnet50_v1"), ("4", "inception_v3")):
+                if c in extra:
+                    extra[c]["cpu_baseline"] = cpu_baseline(m, args.cpu_seconds / 3)
     if args.kernel_table:
         out["kernel_table"] = per_launch
-    be.close()
     return out
 
 
@@ -409,8 +490,9 @@ def run_reference(args, rank, world, local, dist):
         return None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref_cpu_serving
-    return ref_cpu_serving.run(args.model, args.steps, args.warmup, SLO_FACTOR[args.model],
-                               MODEL_LIMITS[args.model], PROBE.get(args.model, (32, 8)))
+    from paper_2308_13803_b200 import serving as S
+    return ref_cpu_serving.run(args.model, args.steps, args.warmup, S.SLO_FACTOR[args.model],
+                               S.MODEL_LIMITS[args.model], S.PROBE.get(args.model, (32, 8)))
 
 
 def main():
@@ -419,12 +501,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default="mobilenet_v1", choices=sorted(SLO_FACTOR))
+    ap.add_argument("--model", default="mobilenet_v1",
+                    choices=["mobilenet_v1", "resnet50_v1", "inception_v3", "synthetic_cnn"])
     ap.add_argument("--max-converge", type=int, default=40)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-table", action="store_true")
     ap.add_argument("--knob", default="", help="static knob, e.g. batching:128 (profiling only)")
+    ap.add_argument("--configs", default="1,3,4,5",
+                    help="BASELINE configs measured besides the headline (config 2), reported "
+                         "under 'configs'; at N>1 only config 5 (the sharded trace) runs")
+    ap.add_argument("--trace-scale", type=float, default=1.0 / 200.0,
+                    help="config 5: duration scale of the reference trace (virtual = device time)")
     ap.add_argument("--controller", default="dnnscaler", choices=["dnnscaler", "clipper"],
                     help="clipper: the paper's baseline controller on the same backend "
                          "(Table 5 comparison; the headline is dnnscaler)")

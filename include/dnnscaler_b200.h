@@ -99,6 +99,15 @@ ds_status ds_set_host_io(ds_backend* b, int enabled);
 /* Waits for all in-flight requests (the device is idle on return). */
 ds_status ds_drain(ds_backend* b);
 
+/* Parity aid: the output of the last request served by `instance`
+ * (0 = batching instance, 1..max_mtl-1 = MT instances, max_mtl+k-1 =
+ * B x MT combination instance k), after draining. logits: [bs][classes]
+ * fp32 (cap elements; in host-I/O mode the copy the request itself read back
+ * to pinned memory); first_image: pool index of its first image (images
+ * first..first+bs-1 of ds_generate_images(seed)). Not in the reference. */
+ds_status ds_last_output(ds_backend* b, int instance, float* logits, size_t cap,
+                         int64_t* first_image, int* bs);
+
 /* NVTX range markers (header-only NVTX v3; no-ops without a tool attached),
  * used to scope ncu captures to a bench's timed region. */
 void ds_nvtx_push(const char* name);
@@ -115,6 +124,9 @@ typedef struct {
   double macs_per_image;   /* algorithmic MACs (real input channels) */
   double weight_count;     /* parameters incl. biases */
   double act_bytes_per_image; /* bf16 bytes written by all layers (+input) */
+  int feature_buffer;   /* pooled-feature buffer read by the FC (ds_debug_read_buffer id) */
+  int feature_channels; /* its width (the FC's fan-in) */
+  int head_k;           /* calibrated head: principal directions used (0: plain random head) */
 } ds_model_info;
 
 ds_status ds_model_info_get(const char* model_id, ds_model_info* out);

@@ -25,14 +25,16 @@
  *   w = bf16_rne((float)(z * sd * gain)); then one bias per channel
  *   (float)(0.1 z) (FC: bias 0, no draws); sd = sqrt(2/fan_in) (FC sqrt(1/fan_in));
  *   depthwise: per channel 9 taps, sd = sqrt(2/9).
- *   image i: RandomStream(mix_seed(seed, 1000000+i)); pixel byte = next>>56 in
- *   (h, w, c) order; x = bf16_rne((p - 127.5f) / 63.75f).
+ *   image i: RandomStream(mix_seed(seed, 1000000+i)); a textured image (img_one:
+ *   base colour + three triangle gratings + per-pixel noise, integer math);
+ *   x = bf16_rne((p - 127.5f) / 63.75f).
  *
  * bf16_storage = 1 rounds every stored activation to bf16 exactly where the
  * device stores bf16 (all layer outputs and the pooled features); 0 keeps
  * everything fp32 after the bf16 input/weights.
  */
 #include <math.h>
+#include <stdio.h>
 #include <pthread.h>
 #include <unistd.h>
 #include <stdint.h>
@@ -431,6 +433,58 @@ static void build_inception(net* n) {
 
 static int has_params(const op* o) { return o->kind == K_CONV || o->kind == K_DW || o->kind == K_FC; }
 
+/* Calibrated classifier head (product synth.hpp HeadCalib):
+ * <head_dir>/<id>.head = "DSHEAD1\0", int32 C, int32 k, f64 mu[C],
+ * f64 scale[k], f64 v[k][C]. W[co][c] = bf16(sum_j (R[co][j] scale[j]) v[j][c])
+ * with R drawn co-major from the FC layer's stream, b = -sum_c W mu. The
+ * file is model data shared with the product (like trained weights); absent
+ * file = plain random head. */
+static char g_head_dir[1024] = "";
+
+void oracle_set_head_dir(const char* dir) {
+  strncpy(g_head_dir, dir ? dir : "", sizeof(g_head_dir) - 1);
+}
+
+static int gen_head(net* n, op* o, rstream* rs) {
+  if (!g_head_dir[0]) return 0;
+  char path[1200];
+  snprintf(path, sizeof(path), "%s/%s.head", g_head_dir, n->id);
+  FILE* f = fopen(path, "rb");
+  if (!f) return 0;
+  char magic[8];
+  int32_t dims[2];
+  if (fread(magic, 1, 8, f) != 8 || memcmp(magic, "DSHEAD1", 8) != 0 || fread(dims, 4, 2, f) != 2 ||
+      dims[0] != o->cin || dims[1] <= 0 || dims[1] > dims[0]) {
+    fclose(f);
+    abort(); /* corrupt or mismatched calibration: never silently fall back */
+  }
+  const int C = dims[0], k = dims[1];
+  double* mu = (double*)malloc(sizeof(double) * C);
+  double* scale = (double*)malloc(sizeof(double) * k);
+  double* v = (double*)malloc(sizeof(double) * (size_t)k * C);
+  if (fread(mu, 8, C, f) != (size_t)C || fread(scale, 8, k, f) != (size_t)k ||
+      fread(v, 8, (size_t)k * C, f) != (size_t)k * C)
+    abort();
+  fclose(f);
+  double* r = (double*)malloc(sizeof(double) * (size_t)o->cout * k);
+  for (size_t q = 0; q < (size_t)o->cout * k; ++q) r[q] = rs_gaussian(rs);
+  o->wt = (float*)malloc(sizeof(float) * (size_t)C * o->cout);
+  o->bias = (float*)malloc(sizeof(float) * o->cout);
+  for (int co = 0; co < o->cout; ++co) {
+    double bacc = 0.0;
+    for (int c = 0; c < C; ++c) {
+      double acc = 0.0;
+      for (int j = 0; j < k; ++j) acc += (r[(size_t)co * k + j] * scale[j]) * v[(size_t)j * C + c];
+      const float wv = bf16_round((float)acc);
+      o->wt[(size_t)c * o->cout + co] = wv;
+      bacc += (double)wv * mu[c];
+    }
+    o->bias[co] = (float)(-bacc);
+  }
+  free(mu); free(scale); free(v); free(r);
+  return 1;
+}
+
 static void gen_weights(net* n) {
   int layer = 0;
   for (int i = 0; i < n->nops; ++i) {
@@ -451,6 +505,7 @@ static void gen_weights(net* n) {
     }
     int kk = o->kh * o->kw * o->cin;
     int fc = o->kind == K_FC;
+    if (fc && gen_head(n, o, &rs)) continue;
     double sd = (fc ? sqrt(1.0 / kk) : sqrt(2.0 / kk)) * (double)o->gain;
     o->wt = (float*)malloc(sizeof(float) * (size_t)kk * o->cout);
     o->bias = (float*)malloc(sizeof(float) * o->cout);
@@ -674,7 +729,34 @@ static void img_one(void* c, int i) {
   rstream rs;
   rs_init(&rs, mix_seed(x->seed, 1000000ULL + (uint64_t)(x->first + i)));
   uint8_t* o = x->out + per * (size_t)i;
-  for (size_t q = 0; q < per; ++q) o[q] = (uint8_t)(mt64_next(&rs.g) >> 56);
+  /* Textured image: a base colour,
+   * three triangle-wave gratings with per-channel amplitude, and per-pixel
+   * noise, all in integer arithmetic. Draw order: base[3]; per grating fx, fy,
+   * phase, amp[3]; then one noise draw per (h, w, c). */
+  int base[3], fx[3], fy[3], ph[3], amp[3][3];
+  for (int c = 0; c < 3; ++c) base[c] = 64 + (int)(mt64_next(&rs.g) >> 57);
+  for (int g = 0; g < 3; ++g) {
+    fx[g] = (int)(mt64_next(&rs.g) >> 59) - 16;
+    fy[g] = (int)(mt64_next(&rs.g) >> 59) - 16;
+    ph[g] = (int)(mt64_next(&rs.g) >> 56);
+    for (int c = 0; c < 3; ++c) amp[g][c] = (int)(mt64_next(&rs.g) >> 58);
+  }
+  for (int y = 0; y < x->h; ++y) {
+    const int py = y * 256 / x->h;
+    for (int xx = 0; xx < x->w; ++xx) {
+      const int px = xx * 256 / x->w;
+      int tri[3];
+      for (int g = 0; g < 3; ++g) {
+        const unsigned p = (unsigned)(fx[g] * px + fy[g] * py + ph[g]) & 255u;
+        tri[g] = abs((int)p - 128) - 64;
+      }
+      for (int c = 0; c < 3; ++c) {
+        int v = base[c] + (int)(mt64_next(&rs.g) >> 58) - 32;
+        for (int g = 0; g < 3; ++g) v += (tri[g] * amp[g][c] + 4096) / 64 - 64; /* floor(t*a/64) */
+        *o++ = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+      }
+    }
+  }
 }
 
 void oracle_generate_images(int h, int w, uint64_t seed, int64_t first, int count, uint8_t* out) {

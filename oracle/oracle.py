@@ -14,6 +14,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 FWD_LIB = os.path.join(HERE, "_build", "liboracle_fwd.so")
 REF_LIB = os.path.join(HERE, "_ref", "libref_replay.so")
+HEAD_DIR = os.environ.get("DS_HEAD_DIR") or os.path.join(os.path.dirname(HERE),
+                                                         "paper_2308_13803_b200", "data", "heads")
 
 _fwd = None
 
@@ -35,6 +37,10 @@ def fwd() -> ctypes.CDLL:
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         lib.oracle_get_threads.restype = ctypes.c_int
         lib.oracle_debug_features.argtypes = [ctypes.c_void_p]
+        lib.oracle_set_head_dir.argtypes = [ctypes.c_char_p]
+        # The calibrated classifier heads are model data shared with the
+        # product (same directory the product library reads).
+        lib.oracle_set_head_dir(HEAD_DIR.encode())
         _fwd = lib
     return _fwd
 

@@ -37,6 +37,9 @@ class DsModelInfo(ctypes.Structure):
         ("macs_per_image", ctypes.c_double),
         ("weight_count", ctypes.c_double),
         ("act_bytes_per_image", ctypes.c_double),
+        ("feature_buffer", ctypes.c_int),
+        ("feature_channels", ctypes.c_int),
+        ("head_k", ctypes.c_int),
     ]
 
 
@@ -84,6 +87,8 @@ SIGNATURES = {
     "ds_nvtx_pop": (None, []),
     "ds_timer_start": (ctypes.c_int, [_vp]),
     "ds_timer_stop": (ctypes.c_int, [_vp, _c_double_p]),
+    "ds_last_output": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_size_t,
+                                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
     "ds_model_info_get": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(DsModelInfo)]),
     "ds_backend_stats_get": (ctypes.c_int, [_vp, ctypes.POINTER(DsBackendStats)]),
     "ds_model_kernels": (

@@ -34,6 +34,9 @@ class ModelInfo:
     macs_per_image: float
     weight_count: float
     act_bytes_per_image: float
+    feature_buffer: int
+    feature_channels: int
+    head_k: int
 
 
 def model_info(model_id: str) -> ModelInfo:
@@ -41,7 +44,8 @@ def model_info(model_id: str) -> ModelInfo:
     mi = _lib.DsModelInfo()
     _lib.check(lib.ds_model_info_get(model_id.encode(), ctypes.byref(mi)))
     return ModelInfo(mi.in_h, mi.in_w, mi.classes, mi.n_ops, mi.n_params, mi.macs_per_image,
-                     mi.weight_count, mi.act_bytes_per_image)
+                     mi.weight_count, mi.act_bytes_per_image, mi.feature_buffer,
+                     mi.feature_channels, mi.head_k)
 
 
 KERNEL_KINDS = ("stage", "conv_gemm", "dwconv", "pool", "gap", "softmax")
@@ -165,6 +169,16 @@ class GpuBackend:
 
     def set_host_io(self, enabled: bool) -> None:
         _lib.check(self._lib.ds_set_host_io(self._h, 1 if enabled else 0))
+
+    def last_output(self, instance: int = 0):
+        """(logits [bs, classes], first_image) of the last request the
+        instance served (0 batching, 1..max_mtl-1 MT, max_mtl+k-1 combo k)."""
+        cap = self._config.abs_max_bs * self.info.classes
+        buf = np.empty(cap, dtype=np.float32)
+        first, bs = ctypes.c_int64(), ctypes.c_int()
+        _lib.check(self._lib.ds_last_output(self._h, instance, buf.ctypes.data, cap,
+                                            ctypes.byref(first), ctypes.byref(bs)))
+        return buf[:bs.value * self.info.classes].reshape(bs.value, self.info.classes).copy(), first.value
 
     def drain(self) -> None:
         _lib.check(self._lib.ds_drain(self._h))

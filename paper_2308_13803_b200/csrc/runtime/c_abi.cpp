@@ -154,6 +154,17 @@ ds_status ds_set_host_io(ds_backend* b, int enabled) {
   return guard([&] { b->impl->set_host_io(enabled != 0); });
 }
 
+ds_status ds_last_output(ds_backend* b, int instance, float* logits, size_t cap,
+                         int64_t* first_image, int* bs) {
+  if (!b || !bs) return null_handle();
+  return guard([&] {
+    const int n = b->impl->last_output(instance, nullptr, nullptr);
+    const size_t need = static_cast<size_t>(n) * b->impl->model().classes;
+    if (logits && cap < need) throw std::invalid_argument("output buffer too small");
+    *bs = b->impl->last_output(instance, logits, first_image);
+  });
+}
+
 ds_status ds_drain(ds_backend* b) {
   if (!b) return null_handle();
   return guard([&] { b->impl->drain(); });
@@ -195,6 +206,9 @@ ds_status ds_model_info_get(const char* model_id, ds_model_info* out) {
     double act = 0.0;
     for (const auto& b : m.buffers) act += static_cast<double>(b.h) * b.w * b.c * (b.f32 ? 4 : 2);
     out->act_bytes_per_image = act;
+    out->feature_buffer = m.ops.back().in;
+    out->feature_channels = m.params.back().cin;
+    out->head_k = ds::params_for(m).head.k;
   });
 }
 

@@ -649,6 +649,8 @@ Backend::Backend(const std::string& model_id, BackendConfig cfg, uint64_t seed, 
   io_cursor_.assign(2 * cfg_.max_mtl, 0);
   io_seq_.assign(2 * cfg_.max_mtl, 0);
   pinned_logits_.assign(2 * cfg_.max_mtl, nullptr);
+  last_first_.assign(2 * cfg_.max_mtl, -1);
+  last_bs_.assign(2 * cfg_.max_mtl, 0);
   instance(0);
 }
 
@@ -713,7 +715,9 @@ void Backend::enqueue_request(int i, int bs) {
   Inflight f{take_event(), take_event(), bs};
   cudaStream_t s = I.stream();
   const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
+  last_bs_[i] = bs;
   if (!host_io_) {
+    last_first_[i] = (i == 0 || i >= cfg_.max_mtl) ? 0 : i % pool_images_;
     check_cuda(cudaEventRecord(f.start, s), "event record");
     I.enqueue_forward(bs);
   } else {
@@ -725,7 +729,13 @@ void Backend::enqueue_request(int i, int bs) {
     int64_t& cur = io_cursor_[i];
     if (cur + bs > pool_images_) cur = 0;
     const uint8_t* src = pinned_images_ + img_bytes * static_cast<size_t>(cur);
-    cur = (i == 0) ? cur + bs : (cur + cfg_.max_mtl) % pool_images_;
+    last_first_[i] = cur;
+    const bool full = i == 0 || i >= cfg_.max_mtl;
+    cur = full ? cur + bs : (cur + cfg_.max_mtl) % pool_images_;
+    if (!pinned_logits_[i])
+      check_cuda(cudaMallocHost(&pinned_logits_[i], static_cast<size_t>(I.max_bs()) *
+                                                        model_.classes * sizeof(float)),
+                 "cudaMallocHost");
     cudaStream_t cs = I.copy_stream();
     check_cuda(cudaStreamWaitEvent(cs, I.slot_free(slot), 0), "wait slot");
     check_cuda(cudaEventRecord(f.start, cs), "event record");
@@ -795,7 +805,6 @@ void Backend::run_combo_requests(int bs, int mtl, int count, double* lat_out) {
   // batches round robin over the instances; clock += latency / mtl as for MT.
   if (bs < 1 || bs > cfg_.abs_max_bs) throw std::invalid_argument("invalid batch size");
   if (mtl < 1 || mtl > cfg_.max_mtl) throw std::invalid_argument("invalid instance count");
-  if (host_io_) throw std::invalid_argument("combination requests run device-resident");
   drain();
   auto idx = [&](int k) { return k == 0 ? 0 : cfg_.max_mtl + k - 1; };
   for (int k = 0; k < mtl; ++k) instance(idx(k));  // (created outside the timed calls)
@@ -917,14 +926,27 @@ void Backend::set_host_io(bool enabled) {
   if (enabled && !pinned_images_) {
     check_cuda(cudaMallocHost(&pinned_images_, host_images_.size()), "cudaMallocHost");
     std::memcpy(pinned_images_, host_images_.data(), host_images_.size());
-    for (int i = 0; i < cfg_.max_mtl; ++i) {
-      const int mbs = (i == 0) ? cfg_.abs_max_bs : 1;
-      check_cuda(cudaMallocHost(&pinned_logits_[i],
-                                static_cast<size_t>(mbs) * model_.classes * sizeof(float)),
-                 "cudaMallocHost");
-    }
   }
   host_io_ = enabled;
+}
+
+int Backend::last_output(int i, float* host_logits, int64_t* first_image) {
+  if (i < 0 || i >= static_cast<int>(inst_.size()) || !inst_[i] || last_bs_[i] == 0)
+    throw std::invalid_argument("instance has served no request");
+  drain();
+  const int bs = last_bs_[i];
+  const size_t lb = static_cast<size_t>(bs) * model_.classes * sizeof(float);
+  if (host_logits) {
+    // host-I/O requests: the logits the request itself read back to pinned
+    // memory; device-resident requests: the instance's logits buffer
+    if (host_io_ && pinned_logits_[i])
+      std::memcpy(host_logits, pinned_logits_[i], lb);
+    else
+      check_cuda(cudaMemcpy(host_logits, inst_[i]->logits(), lb, cudaMemcpyDeviceToHost),
+                 "read logits");
+  }
+  if (first_image) *first_image = last_first_[i];
+  return bs;
 }
 
 }  // namespace ds

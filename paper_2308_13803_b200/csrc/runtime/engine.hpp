@@ -141,6 +141,11 @@ class Backend {
   // End-to-end mode: every request copies its images from a pinned host pool
   // and reads its logits back inside the timed event pair.
   void set_host_io(bool enabled);
+  // Output of the last request served by instance i (0: batching; 1..max_mtl-1:
+  // MT; max_mtl + k - 1: combination instance k), after draining: its logits
+  // (host-I/O mode: the copy that request read back) and the pool index of its
+  // first image (images first .. first + bs - 1). Returns bs.
+  int last_output(int i, float* host_logits, int64_t* first_image);
   bool host_io() const { return host_io_; }
   // Drains every in-flight request (device idle on return).
   void drain();
@@ -187,7 +192,9 @@ class Backend {
   uint8_t* pinned_images_ = nullptr;  // pinned copy for host-I/O mode
   std::vector<float*> pinned_logits_;
   std::vector<int64_t> io_cursor_;
-  std::vector<uint64_t> io_seq_;  // per-instance request count (input slot parity)
+  std::vector<uint64_t> io_seq_;
+  std::vector<int64_t> last_first_;  // per instance: first image of the last request
+  std::vector<int> last_bs_;         // ... and its batch size (0: none yet)  // per-instance request count (input slot parity)
   int pool_images_ = 0;
   bool host_io_ = false;
   int batch_bs_ = 0;  // bs of batches in flight on instance 0 (0: none)

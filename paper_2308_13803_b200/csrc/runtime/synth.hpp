@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdint>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "model.hpp"
@@ -53,7 +54,24 @@ class RandomStream {
 //   dw:   bf16 [9][C] (tap-major)
 //   fc:   bf16 [classes][kpad]
 // Offsets are in elements and keep every layer 128 B aligned.
+// Calibrated classifier head (paper_2308_13803_b200/data/heads/<model>.head,
+// written by tools/calibrate_heads.py from the device's own pooled features
+// over a calibration image set): feature mean mu[C], the top-k principal
+// directions v[k][C] and per-direction scales. The FC becomes
+// W = bf16(R diag(scale) V) with R ~ N(0,1) [classes][k] from the FC layer's
+// stream and b = -W mu, so the logits respond to the input-dependent part of
+// the features instead of being dominated by their common mean (random-init
+// CNNs map every input to nearly the same pooled feature vector).
+// File: "DSHEAD1\0", int32 C, int32 k, f64 mu[C], f64 scale[k], f64 v[k][C].
+struct HeadCalib {
+  int c = 0, k = 0;  // k == 0: no file, plain random head
+  std::vector<double> mu, scale, v;
+};
+std::string head_dir();  // $DS_HEAD_DIR, else <library dir>/data/heads
+HeadCalib load_head(const std::string& model_id);
+
 struct HostParams {
+  HeadCalib head;
   std::vector<uint16_t> w;
   std::vector<float> b;
   std::vector<size_t> w_off, b_off;
@@ -69,7 +87,8 @@ HostParams generate_params(const ModelSpec& m, uint64_t seed = kWeightSeed);
 
 uint16_t f32_to_bf16_rne(float f);
 
-// u8 NHWC images [count][h][w][3], image index first..first+count-1.
+// u8 NHWC images [count][h][w][3], image index first..first+count-1:
+// textured (base colour + three triangle gratings + per-pixel noise).
 void generate_images(int h, int w, uint64_t seed, int64_t first, int count, uint8_t* out);
 
 }  // namespace ds

@@ -12,6 +12,8 @@ loaded rank) on the jobs' durations.
 """
 from __future__ import annotations
 
+import json
+import os
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence
 
@@ -88,7 +90,12 @@ def run_distributed(jobs: Sequence[C.JobSpec], scenario: C.Scenario,
 
     rank, world = dist.get_rank(), dist.get_world_size()
     mine = shard_jobs(jobs, world)[rank]
-    local = run_shard(rank, mine, scenario, catalog, seam=seam, device=rank % 8)
+    import os
+
+    import torch
+
+    device = int(os.environ.get("LOCAL_RANK", rank % max(1, torch.cuda.device_count())))
+    local = run_shard(rank, mine, scenario, catalog, seam=seam, device=device)
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(local, gathered, dst=0)
     if rank != 0:
@@ -98,3 +105,45 @@ def run_distributed(jobs: Sequence[C.JobSpec], scenario: C.Scenario,
     res = aggregate(flat, world)
     res["outcomes"] = flat
     return res
+
+
+# ------------------------------------------------------------------ config 5
+
+TRACE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "scenario_30jobs.json")
+# the reference trace's DNN families -> the architectures built here
+FAMILY = (("mobv1-", "mobilenet_v1"), ("resv2-", "resnet50_v1"), ("inc-", "inception_v3"))
+
+
+def _l1_ms(row: C.DnnProfile) -> float:
+    """L(BS=1) of a catalog row: 1000 / throughput at bs = 1."""
+    for x, t in row.batching_points:
+        if int(x) == 1:
+            return 1000.0 / float(t)
+    raise ValueError(f"catalog row {row.id} has no bs=1 point")
+
+
+def mixed_trace(b200_catalog: Sequence[C.DnnProfile], p40_catalog: Sequence[C.DnnProfile],
+                duration_scale: float = 1.0 / 200.0, trace_path: str = TRACE):
+    """the reference's 30-job trace
+    (data/scenario_30jobs.json) restricted to the implemented families. Each
+    job keeps its SLO tightness c = slo_ms / L_P40(BS=1) of its own P40 DNN
+    (PAPER.md:384 rule), re-based on the B200 L(BS=1) of the architecture that
+    serves it; durations scaled by duration_scale (virtual = device time).
+    Returns (scenario, jobs)."""
+    with open(trace_path) as f:
+        doc = json.load(f)
+    p40 = {r.id: r for r in p40_catalog}
+    b200 = {r.id: r for r in b200_catalog}
+    jobs = []
+    for j in doc["jobs"]:
+        model = next((m for pre, m in FAMILY if j["dnn_id"].startswith(pre)), None)
+        if model is None or j["dnn_id"] not in p40 or model not in b200:
+            continue
+        c = float(j["slo_ms"]) / _l1_ms(p40[j["dnn_id"]])
+        jobs.append(C.JobSpec(int(j["job_id"]), model, c * _l1_ms(b200[model]),
+                              float(j["duration_s"]) * duration_scale))
+    sc = C.Scenario(controller=doc.get("controller", "dnnscaler"), seed=int(doc.get("seed", 42)),
+                    alpha=float(doc.get("alpha", 0.85)), m=int(doc.get("m", 32)),
+                    n=int(doc.get("n", 8)), abs_max_bs=int(doc.get("abs_max_bs", 128)),
+                    max_mtl=int(doc.get("max_mtl", 10)), window=int(doc.get("window", 100)))
+    return sc, jobs

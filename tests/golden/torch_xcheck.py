@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.join(HERE, "..", "..", "oracle"))
 import oracle  # noqa: E402
 
 K_CONV, K_DW, K_MAXPOOL, K_AVGPOOL, K_GAP, K_FC = range(6)
-IMAGES = {"synthetic_cnn": 4, "mobilenet_v1": 2, "resnet50_v1": 1, "inception_v3": 1}
+IMAGES = {"synthetic_cnn": 8, "mobilenet_v1": 4, "resnet50_v1": 2, "inception_v3": 2}
 
 
 def lib():

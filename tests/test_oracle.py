@@ -132,3 +132,22 @@ def test_stem_normalisation_exact():
     div = bf16_rn((t / np.float32(63.75)).astype(np.float32))
     mul = bf16_rn((t * (np.float32(1) / np.float32(63.75))).astype(np.float32))
     assert np.array_equal(div, mul)
+
+
+@pytest.mark.parametrize("model", MODELS)
+def test_top1_fixture_reproduces(model):
+    """The 4,096-image top-1 fixture (tests/golden/make_top1.py) is the
+    current oracle's verdict: its first images re-run here."""
+    g = np.load(os.path.join(GOLDEN, f"top1_{model}.npz"))
+    n = 8
+    ref = oracle.forward(model, oracle.images(model, 0, n), bf16_storage=False)
+    assert np.array_equal(ref.argmax(1), g["top1_32"][:n])
+    s = np.sort(ref, 1)
+    np.testing.assert_allclose(s[:, -1] - s[:, -2], g["margin_32"][:n], rtol=1e-5, atol=1e-6)
+
+
+def test_heads_shared_with_product():
+    """Product and oracle build the FC from the same calibrated head files."""
+    for model in MODELS:
+        assert model_info(model).head_k > 0, model
+        assert os.path.exists(os.path.join(oracle.HEAD_DIR, model + ".head"))
