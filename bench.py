@@ -334,6 +334,10 @@ def config4(args, local):
         res, _, _ = serve_line(args, model, be, controller="dnnscaler", limits=(128, 16), local=local)
         sweep = S.mt_sweep(be, list(range(1, 17)), calls_per_instance=10)
         best = S.best_under_slo(sweep, "mtl", res["slo_ms"])
+        # the same sweep on green-context SM partitions (K8's alternative backing)
+        be.set_mt_mode("green")
+        green = S.mt_sweep(be, [1, 2, 4, 6, 8, 10, 12, 16], calls_per_instance=10)
+        be.set_mt_mode("streams")
         # the MT knob under the Scaler's own AIMD loop (static MT start, Scaler free)
         forced = None
         if best:
@@ -346,7 +350,8 @@ def config4(args, local):
                       "roofline_achieved_frac": round(fres["roofline_achieved_frac"], 4)}
         info = be.info
     return compact(res, model, info, S.SLO_FACTOR[model], {
-        "mt_sweep": sweep, "sweep_best_under_slo": best, "mt_at_best_k_static": forced})
+        "mt_sweep": sweep, "mt_sweep_green_contexts": green, "sweep_best_under_slo": best,
+        "mt_at_best_k_static": forced})
 
 
 def config5(args, rank, world, local, dist):

@@ -99,6 +99,14 @@ ds_status ds_set_host_io(ds_backend* b, int enabled);
 /* Waits for all in-flight requests (the device is idle on return). */
 ds_status ds_drain(ds_backend* b);
 
+/* Multi-tenancy backing (not in the reference): 0 = every
+ * co-located instance on its own stream over the whole device (default);
+ * 1 = green-context SM partitions: at MT level k the SMs are split into k
+ * equal groups and instance i runs on group i with grids sized to it.
+ * DS_ERUNTIME when the driver has no green contexts. */
+ds_status ds_set_mt_mode(ds_backend* b, int mode);
+int ds_get_mt_mode(const ds_backend* b);
+
 /* Parity aid: the output of the last request served by `instance`
  * (0 = batching instance, 1..max_mtl-1 = MT instances, max_mtl+k-1 =
  * B x MT combination instance k), after draining. logits: [bs][classes]

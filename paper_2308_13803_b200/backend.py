@@ -180,6 +180,13 @@ class GpuBackend:
                                             ctypes.byref(first), ctypes.byref(bs)))
         return buf[:bs.value * self.info.classes].reshape(bs.value, self.info.classes).copy(), first.value
 
+    def set_mt_mode(self, mode: str) -> None:
+        """'streams' (default) or 'green' (green-context SM partitions)."""
+        _lib.check(self._lib.ds_set_mt_mode(self._h, {"streams": 0, "green": 1}[mode]))
+
+    def mt_mode(self) -> str:
+        return ("streams", "green")[self._lib.ds_get_mt_mode(self._h)]
+
     def drain(self) -> None:
         _lib.check(self._lib.ds_drain(self._h))
 

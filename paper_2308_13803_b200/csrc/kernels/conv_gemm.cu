@@ -2035,7 +2035,7 @@ int conv_gemm_sm_count() {
       cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  return sms;
+  return budgeted_sms(sms);
 }
 
 cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cudaStream_t stream) {

@@ -373,7 +373,7 @@ int sm_count() {
       cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  return n;
+  return budgeted_sms(n);
 }
 
 // (bring-up knob: DS_DW14_ROWS overrides the 14x14 tile height)
@@ -448,11 +448,21 @@ DwKernelArgs make_args(const DwPlan& p, int n, int h, int w, int c, int stride) 
   a.div_sp = make_fastdiv(static_cast<uint32_t>(a.tiles_x * a.tiles_y * a.tiles_n));
   a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.nb * p.cb * 2);
   // 2-4 boxes in flight, <= ~72 KB per CTA so three CTAs share an SM.
-  const char* kb_env = std::getenv("DS_DW_STAGE_KB");  // ring budget per CTA (A/B)
-  const int budget = (kb_env ? std::atoi(kb_env) : 72) * 1024;
-  const char* st_env = std::getenv("DS_DW_MAX_STAGES");
-  const int max_st = st_env ? std::atoi(st_env) : 4;
-  a.stages = std::max(2, std::min(max_st, static_cast<int>(budget / a.box_bytes)));
+  // (A/B knobs; garbage or out-of-range values fall back to the defaults, and
+  // the ring always fits the 200 KB dynamic shared memory set in launch_plan)
+  auto env_int = [](const char* name, int def, int lo, int hi) {
+    const char* e = std::getenv(name);
+    if (!e || !*e) return def;
+    char* end = nullptr;
+    const long v = std::strtol(e, &end, 10);
+    return (end && *end == 0 && v >= lo && v <= hi) ? static_cast<int>(v) : def;
+  };
+  const int budget = env_int("DS_DW_STAGE_KB", 72, 8, 192) * 1024;
+  const int max_st = env_int("DS_DW_MAX_STAGES", 4, 2, 8);
+  constexpr int kSmemCap = 200 * 1024;
+  int st = std::max(2, std::min(max_st, static_cast<int>(budget / a.box_bytes)));
+  while (st > 2 && st * static_cast<int>(a.box_bytes) + 8 * st + 16 > kSmemCap) --st;
+  a.stages = st;
   return a;
 }
 

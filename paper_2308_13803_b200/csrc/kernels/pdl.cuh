@@ -14,6 +14,20 @@
 
 namespace ds {
 
+// SM budget of the launches being enqueued on this host thread (0: the whole
+// device). Persistent kernels size their grids by it; the runtime sets it
+// while it enqueues (or captures) a forward for a green-context SM partition
+// (MT instances, engine.cu), so a partition's grid is not 148 SMs deep.
+inline int& launch_sm_budget() {
+  static thread_local int budget = 0;
+  return budget;
+}
+
+inline int budgeted_sms(int device_sms) {
+  const int b = launch_sm_budget();
+  return (b > 0 && b < device_sms) ? b : device_sms;
+}
+
 inline bool pdl_enabled() {
   const bool on = [] {
     const char* e = std::getenv("DS_PDL");

@@ -165,6 +165,13 @@ ds_status ds_last_output(ds_backend* b, int instance, float* logits, size_t cap,
   });
 }
 
+ds_status ds_set_mt_mode(ds_backend* b, int mode) {
+  if (!b) return null_handle();
+  return guard([&] { b->impl->set_mt_mode(mode); });
+}
+
+int ds_get_mt_mode(const ds_backend* b) { return b ? b->impl->mt_mode() : -1; }
+
 ds_status ds_drain(ds_backend* b) {
   if (!b) return null_handle();
   return guard([&] { b->impl->drain(); });

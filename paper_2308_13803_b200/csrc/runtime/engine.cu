@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "../kernels/pdl.cuh"
 #include "../kernels/stream_ops.cuh"
 
 namespace ds {
@@ -131,6 +132,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   check_cuda(cudaSetDevice(device), "cudaSetDevice");
   check_cuda(conv_gemm_init(), "conv_gemm_init");
   check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cur_stream_ = stream_;
   const HostParams& hp = params_for(m);
 
   size_t off = 0;
@@ -495,18 +497,18 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
   size_t mark = 0;
   auto record_mark = [&] {
     if (marks)
-      check_cuda(cudaEventRecordWithFlags((*marks)[mark++], stream_, cudaEventRecordExternal),
+      check_cuda(cudaEventRecordWithFlags((*marks)[mark++], cur_stream_, cudaEventRecordExternal),
                  "mark");
   };
   record_mark();
   if (s2d_.op >= 0) {
     check_cuda(launch_stage_s2d(d_images_[slot], d_s2d_, bs, m.in_h, m.in_w, s2d_.hs, s2d_.ws,
-                                s2d_.pad, stream_),
+                                s2d_.pad, cur_stream_),
                "stage_s2d");
     record_mark();
   } else if (stem_ < 0) {
     check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs,
-                                  m.in_h, m.in_w, stream_),
+                                  m.in_h, m.in_w, cur_stream_),
                "stage_input");
     record_mark();
   }
@@ -529,32 +531,32 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
           if (std::sscanf(dbg, "%d:%d", &op_i, &flags) == 2 && op_i == static_cast<int>(i))
             a.debug_flags = flags;
         }
-        e = launch_conv_gemm(a, plans_[i].mode, stream_);
+        e = launch_conv_gemm(a, plans_[i].mode, cur_stream_);
         break;
       }
       case OpKind::kDwConv: {
         const auto* w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off[op.param]);
         if (i < dw_tma_.size() && dw_tma_[i])
           e = launch_dwconv3x3_tma(dw_maps_[i], w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w,
-                                   in.c, op.sh, stream_);
+                                   in.c, op.sh, cur_stream_);
         else
           e = launch_dwconv3x3(x, w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c, op.sh,
-                               stream_);
+                               cur_stream_);
         break;
       }
       case OpKind::kMaxPool:
       case OpKind::kAvgPool:
         e = launch_pool3x3(x, y, bs, in.h, in.w, in.c, op.sh, op.ph, op.kind == OpKind::kMaxPool,
-                           out.c, op.c_off, stream_);
+                           out.c, op.c_off, cur_stream_);
         break;
       case OpKind::kGlobalAvgPool:
-        e = launch_global_avgpool(x, y, bs, in.h * in.w, in.c, stream_);
+        e = launch_global_avgpool(x, y, bs, in.h * in.w, in.c, cur_stream_);
         break;
     }
     check_cuda(e, "layer launch");
     record_mark();
   }
-  check_cuda(launch_softmax(d_logits_, d_probs_, bs, m.classes, stream_), "softmax");
+  check_cuda(launch_softmax(d_logits_, d_probs_, bs, m.classes, cur_stream_), "softmax");
   record_mark();
 }
 
@@ -606,27 +608,39 @@ void Instance::read_buffer(int id, int bs, void* host) const {
   check_cuda(cudaMemcpy(host, bufs_.at(id), bytes, cudaMemcpyDeviceToHost), "read_buffer");
 }
 
-void Instance::enqueue_forward(int bs, int slot) {
+void Instance::enqueue_forward(int bs, int slot) { enqueue_forward_on(bs, slot, stream_, 0, 0); }
+
+void Instance::enqueue_forward_on(int bs, int slot, cudaStream_t s, int sms, int lane_key) {
   if (bs < 1 || bs > max_bs_) throw std::invalid_argument("invalid batch size");
-  const int key = bs * 2 + slot;
+  const int64_t key = (static_cast<int64_t>(lane_key) * 4096 + bs) * 2 + slot;
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
+    // Capture on the lane's stream with the persistent kernels' grids sized
+    // to its SM budget (green-context partitions; 0 = whole device).
+    struct Budget {
+      int saved;
+      explicit Budget(int v) : saved(launch_sm_budget()) { launch_sm_budget() = v; }
+      ~Budget() { launch_sm_budget() = saved; }
+    } budget(sms);
+    cur_stream_ = s;
     cudaGraph_t g = nullptr;
-    check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
+    check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture begin");
     try {
       enqueue_layers(bs, nullptr, slot);
     } catch (...) {
-      cudaStreamEndCapture(stream_, &g);
+      cudaStreamEndCapture(s, &g);
       if (g) cudaGraphDestroy(g);
+      cur_stream_ = stream_;
       throw;
     }
-    check_cuda(cudaStreamEndCapture(stream_, &g), "capture end");
+    cur_stream_ = stream_;
+    check_cuda(cudaStreamEndCapture(s, &g), "capture end");
     cudaGraphExec_t exec = nullptr;
     check_cuda(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
     cudaGraphDestroy(g);
     it = graphs_.emplace(key, exec).first;
   }
-  check_cuda(cudaGraphLaunch(it->second, stream_), "graph launch");
+  check_cuda(cudaGraphLaunch(it->second, s), "graph launch");
 }
 
 // ------------------------------------------------------------------ Backend
@@ -661,6 +675,7 @@ Backend::~Backend() {
   } catch (...) {
   }
   inst_.clear();
+  green_.reset();
   for (cudaEvent_t e : all_events_) cudaEventDestroy(e);
   for (cudaEvent_t e : timer_)
     if (e) cudaEventDestroy(e);
@@ -713,13 +728,25 @@ cudaEvent_t Backend::take_event() {
 void Backend::enqueue_request(int i, int bs) {
   Instance& I = instance(i);
   Inflight f{take_event(), take_event(), bs};
-  cudaStream_t s = I.stream();
+  // MT requests in green-context mode run on instance i's SM partition lane
+  const GreenLane* lane = nullptr;
+  if (mt_mode_ == 1 && mt_active_ && bs == 1 && i < cfg_.max_mtl) {
+    const auto& lanes = green_->level(mtl_);
+    lane = &lanes[i % lanes.size()];
+  }
+  cudaStream_t s = lane ? lane->stream : I.stream();
+  auto forward = [&](int slot) {
+    if (lane)
+      I.enqueue_forward_on(bs, slot, lane->stream, lane->sms, mtl_);
+    else
+      I.enqueue_forward(bs, slot);
+  };
   const size_t img_bytes = static_cast<size_t>(model_.in_h) * model_.in_w * 3;
   last_bs_[i] = bs;
   if (!host_io_) {
     last_first_[i] = (i == 0 || i >= cfg_.max_mtl) ? 0 : i % pool_images_;
     check_cuda(cudaEventRecord(f.start, s), "event record");
-    I.enqueue_forward(bs);
+    forward(0);
   } else {
     // End to end: the request's images cross PCIe on the instance's copy
     // stream into one of two input slots (so the next request's copy runs
@@ -744,7 +771,7 @@ void Backend::enqueue_request(int i, int bs) {
     check_cuda(cudaEventRecord(I.h2d_done(slot), cs), "event record");
     h2d_bytes_ += static_cast<int64_t>(img_bytes) * bs;
     check_cuda(cudaStreamWaitEvent(s, I.h2d_done(slot), 0), "wait h2d");
-    I.enqueue_forward(bs, slot);
+    forward(slot);
     check_cuda(cudaEventRecord(I.slot_free(slot), s), "event record");
     // logits -> this slot's buffer (on the compute stream, once the D2H that
     // last read it is done), then D2H on the instance's output stream, so
@@ -865,6 +892,16 @@ double Backend::apply_instance_change(int delta) {
     check_cuda(cudaStreamSynchronize(I.stream()), "instance warm-up");
   }
   mtl_ = target;
+  if (mt_mode_ == 1) {
+    // green mode: the new level's partitions (created once per level) and
+    // every active instance's lane graph, so requests never capture
+    const auto& lanes = green_->level(mtl_);
+    for (int i = 0; i < mtl_; ++i) {
+      const GreenLane& l = lanes[i % lanes.size()];
+      instance(i).enqueue_forward_on(1, 0, l.stream, l.sms, mtl_);
+    }
+    for (const auto& l : lanes) check_cuda(cudaStreamSynchronize(l.stream), "lane warm-up");
+  }
   const double delay =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   clock_ms_ += delay;
@@ -928,6 +965,24 @@ void Backend::set_host_io(bool enabled) {
     std::memcpy(pinned_images_, host_images_.data(), host_images_.size());
   }
   host_io_ = enabled;
+}
+
+void Backend::set_mt_mode(int mode) {
+  if (mode != 0 && mode != 1) throw std::invalid_argument("invalid multi-tenancy mode");
+  drain();
+  if (mode == 1 && !green_) {
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    green_ = std::make_unique<GreenPartitions>(device_);
+  }
+  mt_mode_ = mode;
+  if (mode == 1) {  // current level's lanes and graphs
+    const auto& lanes = green_->level(mtl_);
+    for (int i = 0; i < mtl_; ++i) {
+      const GreenLane& l = lanes[i % lanes.size()];
+      instance(i).enqueue_forward_on(1, 0, l.stream, l.sms, mtl_);
+    }
+    for (const auto& l : lanes) check_cuda(cudaStreamSynchronize(l.stream), "lane warm-up");
+  }
 }
 
 int Backend::last_output(int i, float* host_logits, int64_t* first_image) {

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../kernels/conv_gemm.cuh"
+#include "green.hpp"
 #include "model.hpp"
 #include "synth.hpp"
 
@@ -45,6 +46,10 @@ class Instance {
   // (graph per (bs, slot)). Two slots let the next request's H2D copy (on
   // copy_stream()) overlap the current forward.
   void enqueue_forward(int bs, int slot = 0);
+  // The same forward on another stream (a green-context lane) with the
+  // persistent kernels' grids sized to `sms` (0: whole device); lane_key
+  // separates its graphs from the default-stream ones.
+  void enqueue_forward_on(int bs, int slot, cudaStream_t s, int sms, int lane_key);
   // Same sequence without a graph (used for capture and first launch). When
   // `marks` is given (kernels_per_forward()+1 events), an externally visible
   // event is recorded before the first and after every kernel.
@@ -80,6 +85,7 @@ class Instance {
   int max_bs_;
   int device_;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t cur_stream_ = nullptr;  // stream enqueue_layers launches on
   void* d_arena_ = nullptr;
   size_t device_bytes_ = 0;
   uint16_t* d_w_ = nullptr;
@@ -104,7 +110,7 @@ class Instance {
   __nv_bfloat16* d_stem_w_ = nullptr;  // stem weights re-laid for the s2d taps [cout][kpad]
   std::vector<CUtensorMap> dw_maps_;  // TMA halo maps of depthwise inputs (by op)
   std::vector<bool> dw_tma_;          // depthwise op uses the TMA kernel
-  std::map<int, cudaGraphExec_t> graphs_;
+  std::map<int64_t, cudaGraphExec_t> graphs_;
   int kernels_per_forward_ = 0;
 };
 
@@ -146,6 +152,10 @@ class Backend {
   // (host-I/O mode: the copy that request read back) and the pool index of its
   // first image (images first .. first + bs - 1). Returns bs.
   int last_output(int i, float* host_logits, int64_t* first_image);
+  // Multi-tenancy backing: 0 = concurrent streams over the whole device,
+  // 1 = green-context SM partitions (green.hpp), one per active instance.
+  void set_mt_mode(int mode);
+  int mt_mode() const { return mt_mode_; }
   bool host_io() const { return host_io_; }
   // Drains every in-flight request (device idle on return).
   void drain();
@@ -201,6 +211,8 @@ class Backend {
   bool mt_active_ = false;
   int rr_ = 0;
   int mtl_ = 1;
+  int mt_mode_ = 0;
+  std::unique_ptr<GreenPartitions> green_;
   double clock_ms_ = 0.0;
   int64_t kernel_launches_ = 0;
   int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;

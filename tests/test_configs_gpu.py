@@ -58,7 +58,8 @@ def test_config3_resnet50_batching_sweep_and_dnnscaler(tmp_path):
         # latency grows with the batch (bs 1-4 sit on the fixed per-forward cost,
         # so neighbours there may tie to the microsecond)
         assert all(lat[b2] >= 0.98 * lat[b1] for b1, b2 in zip(list(lat)[:-1], list(lat)[1:]))
-        assert lat[256] > 2 * lat[16] > 2 * lat[1]
+        assert lat[256] > 2 * lat[16]
+        assert lat[16] > 2 * lat[1]
         assert tput[256] > 8 * tput[1]  # batching pays on B200
         l1, catalog = _row(be, "resnet50_v1")
         slo = 4.66 * l1
@@ -72,6 +73,11 @@ def test_config3_resnet50_batching_sweep_and_dnnscaler(tmp_path):
     kind, value = dev.summary["steady_knob"]
     print("profiler ti_b %.1f ti_mt %.1f -> %s %d (static best %d)" % (
         dev.summary["ti_batching"], dev.summary["ti_mt"], "MT" if kind else "B", value, best))
+    # the Scaler settles on batching within the SLO band near the brute-force
+    # best static batch (its pseudo-binary search stops inside the alpha band,
+    # reference scaler.cpp:28-63, so it may sit below the best)
+    assert kind == C.BATCHING
+    assert 0.5 * best <= value <= 256
     _replay_matches_reference(sc, job, catalog, dev, tmp_path)
 
 
