@@ -354,6 +354,31 @@ def config4(args, local):
         "mt_at_best_k_static": forced})
 
 
+def table5(args, local, headline):
+    """PAPER.md Table 5 on the device: DNNScaler vs Clipper (clipper.cpp:17-35,
+    AIMD on the batch size) serving MobileNet-v1 under the same SLO rule,
+    throughput and throughput per watt from the board's NVML energy counter
+    (SURVEY §8(f) rows 1-2). The DNNScaler side is the headline run."""
+    from paper_2308_13803_b200 import Config, GpuBackend
+    from paper_2308_13803_b200 import serving as S
+    model = "mobilenet_v1"
+    with GpuBackend(model, Config(*S.MODEL_LIMITS[model]), device=local) as be:
+        res, _, energy = serve_line(args, model, be, controller="clipper", local=local, e2e=False)
+    dn_e = headline.get("energy") or {}
+    return {
+        "workload": f"{model}: Clipper AIMD vs DNNScaler, SLO = {S.SLO_FACTOR[model]} x L(BS=1)",
+        "clipper": {"value": round(res["value"], 2), "knob": res["knob"],
+                    "p95_ms_timed": round(res["p95_ms_timed"], 4),
+                    "p95_within_slo": res["p95_within_slo"], "slo_ms": round(res["slo_ms"], 4),
+                    "energy": energy, "knob_trajectory": res["knob_trajectory"]},
+        "dnnscaler": {"value": headline["value"], "knob": headline["config"]["knob"],
+                      "energy": dn_e},
+        "throughput_ratio": round(headline["value"] / res["value"], 4),
+        "per_watt_ratio": (round(dn_e["inferences_per_joule"] / energy["inferences_per_joule"], 4)
+                           if dn_e and energy else None),
+    }
+
+
 def config5(args, rank, world, local, dist):
     """Mixed trace (the reference's 30-job scenario restricted to the built
     families, per-job SLO tightness kept), LPT-sharded over the ranks; each
@@ -424,6 +449,8 @@ def run_ours(args, rank, world, local, dist):
         for c in wanted:
             if c == "5":
                 extra["5"] = config5(args, rank, world, local, dist)
+            elif c == "t5":
+                continue  # (after the headline line exists)
             elif rank == 0 and world == 1:
                 extra[c] = {"1": config1, "3": config3, "4": config4}[c](args, local)
     if rank != 0:
@@ -478,6 +505,8 @@ def run_ours(args, rank, world, local, dist):
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(model, args.cpu_seconds)
+    if "t5" in (args.configs or "") and world == 1:
+        extra["table5"] = table5(args, local, out)
     if extra:
         out["configs"] = extra
         if world == 1 and not args.no_cpu_baseline:
@@ -513,7 +542,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-table", action="store_true")
     ap.add_argument("--knob", default="", help="static knob, e.g. batching:128 (profiling only)")
-    ap.add_argument("--configs", default="1,3,4,5",
+    ap.add_argument("--configs", default="1,3,4,5,t5",
                     help="BASELINE configs measured besides the headline (config 2), reported "
                          "under 'configs'; at N>1 only config 5 (the sharded trace) runs")
     ap.add_argument("--trace-scale", type=float, default=1.0 / 200.0,

@@ -250,6 +250,8 @@ typedef struct {
   int host_io;         /* DEVICE with backend == NULL: end-to-end copies */
   const double* tape;  /* REPLAY */
   size_t tape_len;
+  const double* energy_tape; /* REPLAY (optional): (mJ, wall ms, W) triples of a device run */
+  size_t energy_tape_len;
 } ds_seam_spec;
 
 typedef struct {
@@ -281,6 +283,9 @@ typedef struct {
   double slo_compliance, avg_power_w, power_efficiency, final_slo_ms;
   int n_readaptations;
   int failed; /* run_scenario semantics: error captured, see ds_job_result_error */
+  int power_measured; /* 1: avg_power_w / power_efficiency / power_w from the board's
+                         NVML energy counter (efficiency = inferences per joule),
+                         0: the reference PowerModel */
 } ds_job_summary;
 
 typedef struct ds_job_result ds_job_result;
@@ -307,6 +312,8 @@ size_t ds_job_result_records(const ds_job_result* r, ds_metrics_record* out, siz
 ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* out);
 ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* out);
 size_t ds_job_result_tape(const ds_job_result* r, double* out, size_t cap);
+/* (mJ, wall ms, W) energy readings of a device run, for ds_seam_spec.energy_tape. */
+size_t ds_job_result_energy_tape(const ds_job_result* r, double* out, size_t cap);
 size_t ds_job_result_latencies(const ds_job_result* r, double* out, size_t cap);
 size_t ds_job_result_readaptations(const ds_job_result* r, double* at_s, int* periods, size_t cap);
 const char* ds_job_result_error(const ds_job_result* r);

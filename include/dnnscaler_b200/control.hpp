@@ -163,6 +163,16 @@ class Seam {
   // One control window at a fixed knob; equal to `count` single calls.
   virtual void run_batches(int bs, int count, double* out);
   virtual void run_mt_requests(int count, double* out);
+  // Measured board power: the device's cumulative
+  // energy counter (mJ), a wall clock (ms) and the current power draw (W).
+  // Seams without a power meter (analytic, plain replay) return false and the
+  // harness keeps the reference PowerModel (perf_model.cpp:88-101).
+  virtual bool energy_reading(double* mj, double* wall_ms, double* power_w) {
+    (void)mj;
+    (void)wall_ms;
+    (void)power_w;
+    return false;
+  }
 };
 
 // The reference's simulated GPU (gpu_sim.cpp:7-46): analytic latency with
@@ -199,9 +209,14 @@ class ReplaySeam : public Seam {
   double clock_ms() const override { return clock_ms_; }
   Config config() const override { return config_; }
   size_t consumed() const { return pos_; }
+  // Recorded (mJ, wall ms, W) triples of a device run; replays its measured power.
+  void set_energy_tape(std::vector<double> tape) { energy_ = std::move(tape); }
+  bool energy_reading(double* mj, double* wall_ms, double* power_w) override;
 
  private:
   double next();
+  std::vector<double> energy_;
+  size_t epos_ = 0;
   std::vector<double> tape_;
   size_t pos_ = 0;
   Config config_;
@@ -221,11 +236,14 @@ class RecordingSeam : public Seam {
   Config config() const override { return inner_.config(); }
   void run_batches(int bs, int count, double* out) override;
   void run_mt_requests(int count, double* out) override;
+  bool energy_reading(double* mj, double* wall_ms, double* power_w) override;
   const std::vector<double>& tape() const { return tape_; }
+  const std::vector<double>& energy_tape() const { return energy_; }
 
  private:
   Seam& inner_;
   std::vector<double> tape_;
+  std::vector<double> energy_;
 };
 
 // ------------------------------------------------------------- profiler
@@ -401,6 +419,10 @@ struct JobSummary {
   double slo_compliance = 0.0;
   double avg_power_w = 0.0;
   double power_efficiency = 0.0;
+  // true: avg_power_w / power_efficiency / records' power_w come from the
+  // device's measured energy counter (board average power over the job's wall
+  // time; efficiency = items per joule), else from the reference PowerModel
+  bool power_measured = false;
   double final_slo_ms = 0.0;
   std::vector<Readaptation> readaptations;
   std::string error;
@@ -412,6 +434,7 @@ struct JobTrace {
   JobSummary summary;
   ProfileReport report;
   std::vector<double> tape;  // every seam value, in call order
+  std::vector<double> energy_tape;  // (mJ, wall ms, W) per energy reading (device runs)
   std::vector<double> latencies;  // all served latencies, in order
 };
 

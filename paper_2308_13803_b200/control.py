@@ -50,7 +50,8 @@ class _Scenario(ctypes.Structure):
 class _SeamSpec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("backend", ctypes.c_void_p), ("device", ctypes.c_int),
                 ("host_io", ctypes.c_int), ("tape", ctypes.POINTER(ctypes.c_double)),
-                ("tape_len", ctypes.c_size_t)]
+                ("tape_len", ctypes.c_size_t), ("energy_tape", ctypes.POINTER(ctypes.c_double)),
+                ("energy_tape_len", ctypes.c_size_t)]
 
 
 class _Record(ctypes.Structure):
@@ -78,7 +79,8 @@ class _Summary(ctypes.Structure):
         (n, ctypes.c_double) for n in (
             "duration_s", "total_items", "avg_throughput", "steady_throughput", "p95_overall_ms",
             "slo_compliance", "avg_power_w", "power_efficiency", "final_slo_ms")] + [
-        ("n_readaptations", ctypes.c_int), ("failed", ctypes.c_int)]
+        ("n_readaptations", ctypes.c_int), ("failed", ctypes.c_int),
+        ("power_measured", ctypes.c_int)]
 
 
 class _BatchScaler(ctypes.Structure):
@@ -105,6 +107,7 @@ _SIGS = {
     "ds_job_result_summary": (ctypes.c_int, [_vp, _P(_Summary)]),
     "ds_job_result_profile": (ctypes.c_int, [_vp, _P(_Report)]),
     "ds_job_result_tape": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
+    "ds_job_result_energy_tape": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
     "ds_job_result_latencies": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
     "ds_job_result_readaptations": (ctypes.c_size_t, [_vp, _vp, _vp, ctypes.c_size_t]),
     "ds_job_result_error": (ctypes.c_char_p, [_vp]),
@@ -232,6 +235,7 @@ class JobResult:
     latencies: np.ndarray
     readaptations: list
     error: str
+    energy_tape: np.ndarray = None  # (mJ, wall ms) readings of a device run
 
 
 class _Marshal:
@@ -263,15 +267,21 @@ class _Marshal:
         self.n_catalog = len(catalog)
 
     def seam(self, kind: str, backend: Optional[GpuBackend] = None, device: int = 0,
-             host_io: bool = False, tape: Optional[np.ndarray] = None) -> _SeamSpec:
+             host_io: bool = False, tape: Optional[np.ndarray] = None,
+             energy_tape: Optional[np.ndarray] = None) -> _SeamSpec:
         k = {"analytic": 0, "device": 1, "replay": 2}[kind]
-        t = None
-        if tape is not None:
-            t = np.ascontiguousarray(tape, dtype=np.float64)
-            self.keep.append(t)
+
+        def arr(x):
+            if x is None:
+                return None, 0
+            a = np.ascontiguousarray(x, dtype=np.float64)
+            self.keep.append(a)
+            return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.size
+
+        t, tn = arr(tape)
+        e, en = arr(energy_tape)
         return _SeamSpec(k, backend._h if backend is not None else None, device, int(host_io),
-                         t.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if t is not None else None,
-                         0 if t is None else t.size)
+                         t, tn, e, en)
 
 
 def _collect(lib, res) -> JobResult:
@@ -301,18 +311,22 @@ def _collect(lib, res) -> JobResult:
     pe = np.empty(max(1, nr), dtype=np.int32)
     lib.ds_job_result_readaptations(res, at.ctypes.data, pe.ctypes.data, nr)
     err = lib.ds_job_result_error(res).decode()
+    ne = lib.ds_job_result_energy_tape(res, None, 0)
+    etape = np.empty(ne, dtype=np.float64)
+    lib.ds_job_result_energy_tape(res, etape.ctypes.data, ne)
     return JobResult(records, summary, report, tape, lat,
-                     [(float(at[i]), int(pe[i])) for i in range(nr)], err)
+                     [(float(at[i]), int(pe[i])) for i in range(nr)], err, etape)
 
 
 def run_job(scenario: Scenario, job: JobSpec, catalog: Sequence[DnnProfile], seam: str = "analytic",
             backend: Optional[GpuBackend] = None, device: int = 0, host_io: bool = False,
-            tape: Optional[np.ndarray] = None) -> JobResult:
+            tape: Optional[np.ndarray] = None,
+            energy_tape: Optional[np.ndarray] = None) -> JobResult:
     """run_job (reference harness.cpp:329-333) on the chosen seam:
     'analytic' (the reference's simulated GPU), 'device' (B200), 'replay' (tape)."""
     lib = _l()
     m = _Marshal(scenario, job, catalog)
-    spec = m.seam(seam, backend, device, host_io, tape)
+    spec = m.seam(seam, backend, device, host_io, tape, energy_tape)
     res = ctypes.c_void_p()
     _lib.check(lib.ds_job_run(ctypes.byref(m.sc), ctypes.byref(m.job), m.catalog, m.n_catalog,
                               ctypes.byref(spec), ctypes.byref(res)))

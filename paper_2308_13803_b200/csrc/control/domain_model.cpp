@@ -265,6 +265,23 @@ double ReplaySeam::apply_instance_change(int delta) {
   return delay;
 }
 
+bool ReplaySeam::energy_reading(double* mj, double* wall_ms, double* power_w) {
+  if (energy_.empty()) return false;
+  if (epos_ + 3 > energy_.size()) throw std::runtime_error("energy tape exhausted");
+  *mj = energy_[epos_++];
+  *wall_ms = energy_[epos_++];
+  *power_w = energy_[epos_++];
+  return true;
+}
+
+bool RecordingSeam::energy_reading(double* mj, double* wall_ms, double* power_w) {
+  if (!inner_.energy_reading(mj, wall_ms, power_w)) return false;
+  energy_.push_back(*mj);
+  energy_.push_back(*wall_ms);
+  energy_.push_back(*power_w);
+  return true;
+}
+
 double RecordingSeam::run_batch(int bs) {
   const double v = inner_.run_batch(bs);
   tape_.push_back(v);

@@ -105,9 +105,13 @@ ds::SeamFactory make_factory(const ds_seam_spec& spec) {
       return ds::analytic_seam_factory();
     case DS_SEAM_REPLAY: {
       std::vector<double> tape(spec.tape, spec.tape + spec.tape_len);
-      return [tape](const ds::Scenario& sc, const ds::JobSpec&, const ds::BatchingModel&,
-                    const ds::MtModel&) {
-        return std::make_unique<ds::ReplaySeam>(tape, ds::Seam::Config{sc.abs_max_bs, sc.max_mtl});
+      std::vector<double> energy;
+      if (spec.energy_tape) energy.assign(spec.energy_tape, spec.energy_tape + spec.energy_tape_len);
+      return [tape, energy](const ds::Scenario& sc, const ds::JobSpec&, const ds::BatchingModel&,
+                            const ds::MtModel&) {
+        auto r = std::make_unique<ds::ReplaySeam>(tape, ds::Seam::Config{sc.abs_max_bs, sc.max_mtl});
+        r->set_energy_tape(energy);
+        return r;
       };
     }
     case DS_SEAM_DEVICE: {
@@ -240,6 +244,7 @@ ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* o) {
   o->p95_overall_ms = s.p95_overall_ms;
   o->slo_compliance = s.slo_compliance;
   o->avg_power_w = s.avg_power_w;
+  o->power_measured = s.power_measured ? 1 : 0;
   o->power_efficiency = s.power_efficiency;
   o->final_slo_ms = s.final_slo_ms;
   o->n_readaptations = static_cast<int>(s.readaptations.size());
@@ -265,6 +270,13 @@ ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* o) {
 size_t ds_job_result_tape(const ds_job_result* r, double* out, size_t cap) {
   if (!r) return 0;
   const auto& t = r->trace.tape;
+  if (out) std::memcpy(out, t.data(), std::min(cap, t.size()) * sizeof(double));
+  return t.size();
+}
+
+size_t ds_job_result_energy_tape(const ds_job_result* r, double* out, size_t cap) {
+  if (!r) return 0;
+  const auto& t = r->trace.energy_tape;
   if (out) std::memcpy(out, t.data(), std::min(cap, t.size()) * sizeof(double));
   return t.size();
 }

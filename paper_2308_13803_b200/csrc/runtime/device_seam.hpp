@@ -4,7 +4,10 @@
 #include <memory>
 
 #include "../../../include/dnnscaler_b200/control.hpp"
+#include <cstdlib>
+
 #include "engine.hpp"
+#include "nvml_energy.hpp"
 
 namespace ds {
 
@@ -35,6 +38,11 @@ class DeviceSeam : public Seam {
     return d;
   }
   int mtl() const override { return b_.mtl(); }
+  bool energy_reading(double* mj, double* wall_ms, double* power_w) override {
+    if (const char* e = std::getenv("DS_MODEL_POWER"))  // A/B: keep the PowerModel
+      if (e[0] == '1') return false;
+    return board_energy_mj(b_.device(), mj, wall_ms, power_w);
+  }
   double clock_ms() const override { return clock_ms_; }
   Config config() const override { return Config{b_.config().abs_max_bs, b_.config().max_mtl}; }
   void run_batches(int bs, int count, double* out) override {

@@ -132,6 +132,7 @@ class Backend {
   double apply_instance_change(int delta);
   double set_mtl(int target);
   int mtl() const { return mtl_; }
+  int device() const { return device_; }
   double clock_ms() const { return clock_ms_; }
   const BackendConfig& config() const { return cfg_; }
 
