@@ -40,8 +40,10 @@ def main(path, forwards=1):
             v = r.get(k, 0.0)
             u = r.get(k + "_unit", "byte")
             a["bytes"] += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        a["tensor_pct_x_ns"] += r.get(
-            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0.0) * ns
+        # (tools/gpu_round.sh captures the _elapsed form; older captures _active)
+        tp = r.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                   r.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0.0))
+        a["tensor_pct_x_ns"] += tp * ns
     tot = sum(a["ns"] for a in agg.values())
     out = {}
     print(f"{'kernel':40s} {'launches':>8s} {'share':>7s} {'us/fwd':>9s} {'DRAM MB/fwd':>12s} {'GB/s':>7s} {'tensor%':>8s}")
