@@ -42,6 +42,17 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
                            int stride, int pad, bool is_max, int ldo, int c_off,
                            cudaStream_t stream);
 
+// The same pooling streamed through TMA halo boxes (pool_tma.cu), bit-identical
+// to launch_pool3x3 for average pools and for max pools whose edge taps are
+// zeros-equivalent (pad 0, or inputs >= 0). The input map comes from
+// pool_tma_input_map over the (max-batch) input buffer.
+bool pool_tma_plan_ok(int h, int w, int c, int stride, int pad);
+bool pool_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w, int c,
+                        int stride, int pad);
+cudaError_t launch_pool3x3_tma(const CUtensorMap& in_map, __nv_bfloat16* y, int n, int h, int w,
+                               int c, int stride, int pad, bool is_max, int ldo, int c_off,
+                               cudaStream_t stream);
+
 // Mean over all pixels: [n][hw][c] -> [n][c] bf16.
 cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,
                                   cudaStream_t stream);

@@ -224,6 +224,22 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                    dwconv_tma_input_map(&dw_maps_[i], bufs_[op.in], max_bs, din.h, din.w, din.c,
                                         op.sh);
     }
+    if (op.kind == OpKind::kMaxPool || op.kind == OpKind::kAvgPool) {
+      // TMA halo-box pooling (pool_tma.cu). A padded max pool reads its edge
+      // taps as zeros there, so it qualifies only when its input is a ReLU
+      // output (every input >= 0): the producer of op.in must apply ReLU.
+      const BufferSpec& pin = m.buffers.at(op.in);
+      bool relu_input = false;
+      for (size_t j = 0; j < i; ++j)
+        if (m.ops[j].out == op.in) relu_input = m.ops[j].relu;
+      const char* legacy = std::getenv("DS_POOL_TMA");
+      const bool allow = !(legacy && legacy[0] == '0');
+      pool_maps_.resize(m.ops.size());
+      pool_tma_.resize(m.ops.size(), false);
+      pool_tma_[i] = allow && (op.kind == OpKind::kAvgPool || op.ph == 0 || relu_input) &&
+                     pool_tma_input_map(&pool_maps_[i], bufs_[op.in], max_bs, pin.h, pin.w, pin.c,
+                                        op.sh, op.ph);
+    }
     if (op.kind != OpKind::kConv && op.kind != OpKind::kFc) continue;
     const ParamSpec& p = m.params.at(op.param);
     const BufferSpec& in = m.buffers.at(op.in);
@@ -546,6 +562,11 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
       }
       case OpKind::kMaxPool:
       case OpKind::kAvgPool:
+        if (i < pool_tma_.size() && pool_tma_[i]) {
+          e = launch_pool3x3_tma(pool_maps_[i], y, bs, in.h, in.w, in.c, op.sh, op.ph,
+                                 op.kind == OpKind::kMaxPool, out.c, op.c_off, cur_stream_);
+          break;
+        }
         e = launch_pool3x3(x, y, bs, in.h, in.w, in.c, op.sh, op.ph, op.kind == OpKind::kMaxPool,
                            out.c, op.c_off, cur_stream_);
         break;

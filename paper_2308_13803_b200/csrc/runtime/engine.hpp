@@ -110,6 +110,8 @@ class Instance {
   __nv_bfloat16* d_stem_w_ = nullptr;  // stem weights re-laid for the s2d taps [cout][kpad]
   std::vector<CUtensorMap> dw_maps_;  // TMA halo maps of depthwise inputs (by op)
   std::vector<bool> dw_tma_;          // depthwise op uses the TMA kernel
+  std::vector<CUtensorMap> pool_maps_;  // TMA halo maps of pool inputs (by op)
+  std::vector<bool> pool_tma_;          // pool op uses the TMA kernel (DS_POOL_TMA=0: off)
   std::map<int64_t, cudaGraphExec_t> graphs_;
   int kernels_per_forward_ = 0;
 };
