@@ -61,6 +61,17 @@ __device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) {
   return d;
 }
 
+// x / 9 correctly rounded without the IEEE division sequence: the product
+// with RN(1/9) corrected by one fma residual step. Checked exhaustively
+// against x / 9.0f over every finite fp32 (equal except x = -0, which a sum
+// starting from +0 never produces).
+__device__ __forceinline__ float div9(float x) {
+  constexpr float kInv9 = 1.0f / 9.0f;
+  const float q0 = __fmul_rn(x, kInv9);
+  const float r = __fmaf_rn(-q0, 9.0f, x);
+  return __fmaf_rn(r, kInv9, q0);
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -91,7 +102,8 @@ struct PoolArgs {
   int tiles_x, tiles_y, n, cblocks, tiles;
   FastDivP div_tx, div_ty, div_sp;  // by tiles_x, tiles_y, tiles_x * tiles_y * n
   int stages;
-  uint32_t box_bytes;
+  uint32_t box_bytes;     // TMA transaction bytes per box
+  uint32_t stage_bytes;   // ring slot stride (box_bytes rounded up to 128 B: TMA destination alignment)
 };
 
 // Tile t -> (channel block [slowest], image, tile row, tile column).
@@ -100,7 +112,7 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
     const __grid_constant__ CUtensorMap in_map, const __grid_constant__ PoolArgs a) {
   constexpr int XN = (Q - 1) * S + 3;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.box_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.stage_bytes);
   const int groups = 1 << a.glog2;
   const int cb = groups * 8;
   auto coords = [&](int t, int& cbk, int& tx, int& ty, int& tn) {
@@ -117,7 +129,7 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
     ptx::mbar_arrive_expect_tx(&full[stage], a.box_bytes);
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + stage * a.box_bytes)),
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + stage * a.stage_bytes)),
         "l"(&in_map), "r"(ptx::smem_u32(&full[stage])), "r"(cbk * cb),
         "r"(tx * a.tw * S - a.pad), "r"(ty * a.th * S - a.pad), "r"(tn)
         : "memory");
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
   const int sx = strip % spr, oyl = strip / spr;
   const uint4* my_box =
       reinterpret_cast<const uint4*>(smem) + (((oyl * S) * a.iw + sx * Q * S) << a.glog2) + g;
-  const int box_vecs = static_cast<int>(a.box_bytes >> 4);
+  const int box_vecs = static_cast<int>(a.stage_bytes >> 4);
   int stage = 0;
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
@@ -201,7 +213,7 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
         } else {
           float* v = acc[q];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = v[e] / 9.0f;
+          for (int e = 0; e < 8; ++e) v[e] = div9(v[e]);
           yp[q * a.ldo_g] = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]),
                                        pack2(v[6], v[7]));
         }
@@ -272,7 +284,7 @@ cudaError_t launch(const CUtensorMap& map, const PoolArgs& a, int threads, cudaS
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const size_t smem = static_cast<size_t>(a.stages) * a.box_bytes + 8 * a.stages + 16;
+  const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 8 * a.stages + 16;
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
           cudaSuccess ||
@@ -329,9 +341,10 @@ cudaError_t launch_pool3x3_tma(const CUtensorMap& in_map, __nv_bfloat16* y, int 
   a.div_ty = fastdiv(static_cast<uint32_t>(a.tiles_y));
   a.div_sp = fastdiv(static_cast<uint32_t>(a.tiles_x * a.tiles_y * n));
   a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.cb * 2);
+  a.stage_bytes = (a.box_bytes + 127u) / 128u * 128u;
   constexpr int kBudget = 72 * 1024, kSmemCap = 200 * 1024;
-  int st = std::max(2, std::min(4, kBudget / static_cast<int>(a.box_bytes)));
-  while (st > 2 && st * static_cast<int>(a.box_bytes) + 8 * st + 16 > kSmemCap) --st;
+  int st = std::max(2, std::min(4, kBudget / static_cast<int>(a.stage_bytes)));
+  while (st > 2 && st * static_cast<int>(a.stage_bytes) + 8 * st + 16 > kSmemCap) --st;
   a.stages = st;
   const int items = ((p.tw / p.q) * p.th) * (p.cb / 8);
   const int threads = std::min(kPoolMaxThreads, (items + 31) / 32 * 32);
