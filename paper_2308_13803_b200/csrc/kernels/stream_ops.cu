@@ -368,32 +368,29 @@ __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restri
   }
 }
 
-// Global average pool: four threads (adjacent lanes) per (image, 8-channel
-// group), each summing every 4th pixel with all its loads in flight; the four
-// partial sums combine in a fixed order (p0+p1)+(p2+p3), so results are
-// deterministic (and within fp32 rounding of the oracle's sequential sum).
-constexpr int kGapParts = 4;
-
+// Global average pool: one warp per (image, 256-channel block), lane l owns
+// channels [8l, 8l + 8) of the block, so every pixel is one coalesced 512 B
+// warp load. Each lane sums its pixels in order (p0 + p1 + ... in fp32, the
+// oracle's sequential order, so results equal it bit for bit) with eight
+// loads in flight, then divides by the pixel count.
 __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int hw,
-                                      int cg, long long work) {
+                                      int cg, int blocks_per_image, int warps) {
   pdl_trigger();
   pdl_wait();
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long i = t / kGapParts;
-  const int part = static_cast<int>(t % kGapParts);
-  const bool live = i < work;
-  const int g = live ? static_cast<int>(i % cg) : 0;
-  const long long n = live ? i / cg : 0;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= warps) return;
+  const int lane = threadIdx.x & 31;
+  const int n = w / blocks_per_image;
+  const int g = (w - n * blocks_per_image) * 32 + lane;
+  if (g >= cg) return;
+  const uint4* p = x + static_cast<long long>(n) * hw * cg + g;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const uint4* p = x + n * hw * cg + g;
-  constexpr int U = 13;  // 49 / 4 pixels per part in one batch of loads
-  for (int q0 = part; live && q0 < hw; q0 += U * kGapParts) {
+  constexpr int U = 8;
+  int q0 = 0;
+  for (; q0 + U <= hw; q0 += U) {
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int q = q0 + u * kGapParts;
-      v[u] = q < hw ? __ldg(p + static_cast<long long>(q) * cg) : make_uint4(0u, 0u, 0u, 0u);
-    }
+    for (int u = 0; u < U; ++u) v[u] = __ldg(p + static_cast<long long>(q0 + u) * cg);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float xv[8];
@@ -402,16 +399,16 @@ __global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __rest
       for (int e = 0; e < 8; ++e) acc[e] += xv[e];
     }
   }
+  for (; q0 < hw; ++q0) {
+    float xv[8];
+    unpack8(__ldg(p + static_cast<long long>(q0) * cg), xv);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);  // (p0+p1), (p2+p3)
-    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);  // (p0+p1)+(p2+p3)
+    for (int e = 0; e < 8; ++e) acc[e] += xv[e];
   }
-  if (!live || part != 0) return;
   const float inv = static_cast<float>(hw);
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = acc[e] / inv;
-  y[i] = pack8(acc);
+  y[static_cast<long long>(n) * cg + g] = pack8(acc);
 }
 
 __global__ void softmax_kernel(const float* __restrict__ logits, float* __restrict__ probs, int n,
@@ -552,9 +549,12 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
 cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,
                                   cudaStream_t stream) {
   const int cg = c / 8;
-  const long long work = static_cast<long long>(n) * cg;
-  return launch_pdl(global_avgpool_kernel, dim3(grid_for(work * kGapParts)), dim3(kBlock), 0, stream,
-                    reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, work);
+  const int bpi = (cg + 31) / 32;  // 256-channel blocks per image
+  const int warps = n * bpi;
+  const int per_block = kBlock / 32;
+  return launch_pdl(global_avgpool_kernel, dim3((warps + per_block - 1) / per_block), dim3(kBlock),
+                    0, stream, reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw,
+                    cg, bpi, warps);
   return cudaGetLastError();
 }
 
