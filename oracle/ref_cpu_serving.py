@@ -11,8 +11,11 @@ assembled from:
     run_batch(bs) is a timed CPU forward of bs synthetic images on all host
     threads; each run_mt_request() at mtl k is one of k concurrent
     single-image forwards (k instances co-located on the CPU).
-Same metric and SLO rule as the B200 arm (SLO = c x L(BS=1) measured on this
-platform), window shortened to 10 requests so the run stays within minutes.
+Same metric, workload and SLO rule as the B200 arm (SLO = c x L(BS=1)
+measured on this platform) and the same --steps K / --warmup W; each step
+is a bounded sample of the workload (a control window of 10 requests
+instead of 100: one bs-128 window costs ~6 s of CPU forward), so the run
+stays within minutes.
 """
 from __future__ import annotations
 
@@ -86,7 +89,8 @@ def run(model: str, steps: int, warmup: int, slo_factor: float, limits, probe) -
     slo = slo_factor * l1
     # duration: profiling plus enough control periods to converge + W + K
     period_guess_ms = WINDOW * lm
-    duration_s = (30 * l1 + 10 * lm + 10 * lmt + (12 + warmup + steps) * period_guess_ms) / 1000.0
+    # (enough periods for the search to converge, then W warm-up + K timed)
+    duration_s = (30 * l1 + 10 * lm + 10 * lmt + (16 + warmup + steps) * period_guess_ms) / 1000.0
     sc = {"controller": "dnnscaler", "seed": 42, "alpha": 0.85, "m": m, "n": n,
           "abs_max_bs": max_bs, "max_mtl": max_mtl, "window": WINDOW, "sigma": 0.05,
           "jobs": [{"job_id": 1, "dnn_id": model, "slo_ms": slo, "duration_s": duration_s}]}
@@ -100,7 +104,9 @@ def run(model: str, steps: int, warmup: int, slo_factor: float, limits, probe) -
     res = ref.run_job(spath, 0, "callback")
     wall = time.perf_counter() - t0
     recs = res["records"]  # [time_s, job, kind, value, p95, mean, tput, power, slo, violated]
-    k = min(steps, len(recs))
+    if len(recs) < steps:
+        raise RuntimeError(f"reference job served {len(recs)} periods < {steps} timed steps")
+    k = steps
     tail = recs[-k:]
     # per-period elapsed = items / throughput; value over the last K periods
     items = np.where(tail[:, 2] == 0, WINDOW * tail[:, 3], WINDOW)
@@ -121,9 +127,12 @@ def run(model: str, steps: int, warmup: int, slo_factor: float, limits, probe) -
         "vs_baseline": None,
         "dtype": "fp32",
         "data": "synthetic (same seeded images and weights as the B200 arm)",
-        "config": {"workload": f"{model}, reference DNNScaler Profiler+Scaler on the host CPU, "
-                               f"SLO = {slo_factor} x L(BS=1)",
-                   "model": model, "slo_ms": round(slo, 3), "l1_ms": round(l1, 3),
+        "config": {"workload": f"{model} {dev.imgs.shape[1]}x{dev.imgs.shape[2]}, DNNScaler "
+                               f"Profiler+Scaler, SLO = {slo_factor} x L(BS=1)",
+                   "model": model, "global_batch": knob[1] if knob[0] == "batching" else 1,
+                   "device": f"host CPU, {dev.threads} threads (reference control plane + "
+                             f"FP32 C oracle forward)",
+                   "slo_ms": round(slo, 3), "l1_ms": round(l1, 3),
                    "knob": {"kind": knob[0], "value": knob[1]},
                    "profiler": {"ti_batching": round(summ["ti_batching"], 2),
                                 "ti_mt": round(summ["ti_mt"], 2),
