@@ -99,6 +99,15 @@ ds_status ds_set_host_io(ds_backend* b, int enabled);
 /* Waits for all in-flight requests (the device is idle on return). */
 ds_status ds_drain(ds_backend* b);
 
+/* Live per-kernel timing inside the real graph-launched forwards (no event
+ * nodes; CTA 0 of every kernel adds its %globaltimer after
+ * griddepcontrol.wait into a slot): reset = 1 zeroes instance `instance`'s
+ * slots; reset = 0 drains and writes each kernel's in-situ duration (ms,
+ * ds_model_kernels() order, averaged over *forwards forwards since the reset)
+ * to ms_out. Not in the reference. */
+ds_status ds_kernel_spans(ds_backend* b, int instance, int reset, double* ms_out, int cap,
+                          int64_t* forwards);
+
 /* Multi-tenancy backing (not in the reference): 0 = every
  * co-located instance on its own stream over the whole device (default);
  * 1 = green-context SM partitions: at MT level k the SMs are split into k

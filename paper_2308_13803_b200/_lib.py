@@ -89,6 +89,8 @@ SIGNATURES = {
     "ds_timer_stop": (ctypes.c_int, [_vp, _c_double_p]),
     "ds_set_mt_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
     "ds_get_mt_mode": (ctypes.c_int, [_vp]),
+    "ds_kernel_spans": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int64)]),
     "ds_last_output": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_size_t,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
     "ds_model_info_get": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(DsModelInfo)]),

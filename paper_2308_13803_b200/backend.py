@@ -205,6 +205,21 @@ class GpuBackend:
         _lib.check(self._lib.ds_profile_kernels(self._h, bs, reps, out.ctypes.data, n))
         return out
 
+    def reset_kernel_spans(self, instance: int = 0) -> None:
+        """Zero the live per-kernel timing slots of an instance."""
+        n = ctypes.c_int64()
+        _lib.check(self._lib.ds_kernel_spans(self._h, instance, 1, None, 0, ctypes.byref(n)))
+
+    def kernel_spans(self, instance: int = 0):
+        """(ms per kernel of the forward, forwards) measured live since the
+        last reset, inside the real graph launches (ds_kernel_spans)."""
+        k = len(kernel_costs(self.model_id))
+        out = np.zeros(k, dtype=np.float64)
+        n = ctypes.c_int64()
+        _lib.check(self._lib.ds_kernel_spans(self._h, instance, 0, out.ctypes.data, k,
+                                             ctypes.byref(n)))
+        return out, n.value
+
     def stats(self) -> dict:
         s = _lib.DsBackendStats()
         _lib.check(self._lib.ds_backend_stats_get(self._h, ctypes.byref(s)))

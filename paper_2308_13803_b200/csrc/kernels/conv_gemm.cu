@@ -940,6 +940,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // activations (and the residual) come from earlier layers
+  span_mark(args.span);
   if (args.ts && threadIdx.x == 0) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -2041,6 +2042,7 @@ int conv_gemm_sm_count() {
 cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cudaStream_t stream) {
   // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
   ConvGemmArgs args = in_args;
+  args.span = launch_span();
   const bool pair = mode == ConvLoadMode::kPairTmaA || mode == ConvLoadMode::kPairPwDw;
   const bool pd = mode == ConvLoadMode::kPwDw || mode == ConvLoadMode::kPairPwDw;
   if (pd && !conv_gemm_pwdw_ok(args.Ho, args.Wo, args.Cout, args.BN, args.dw_stride))

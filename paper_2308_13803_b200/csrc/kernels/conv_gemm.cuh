@@ -59,6 +59,7 @@ struct ConvGemmArgs {
   // bring-up timeline (tools/test_conv_gemm TS=1): per CTA 64 clock64 stamps
   // relative to kernel entry, see conv_gemm.cu ts_mark(); nullptr in the runtime
   unsigned long long* ts;
+  unsigned long long* span;  // live per-kernel timing slot (pdl.cuh span_mark), or nullptr
   // kDwFused: A[m, c] = relu(dw3x3(x)[m, c] + dw_b[c]), computed in the
   // producer from the depthwise input x ([H][W][C], pad 1, stride dw_stride);
   // Ho/Wo are the depthwise output dims, R = S = 1. Tiles are dw_th x dw_tw

@@ -111,6 +111,7 @@ struct DwKernelArgs {
   FastDiv div_tx, div_ty, div_sp;  // by tiles_x, tiles_y, tiles_x*tiles_y*tiles_n
   int stages;
   uint32_t box_bytes;
+  unsigned long long* span;  // live timing slot (pdl.cuh span_mark)
 };
 
 // Tile t -> (channel block, x, y, image block). The channel block varies
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
   __syncthreads();
   pdl_trigger();
   pdl_wait();  // the input is the previous layer's output
+  span_mark(a.span);
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int t = blockIdx.x + s * gridDim.x;
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma4_kernel(
   __syncthreads();
   pdl_trigger();
   pdl_wait();
+  span_mark(a.span);
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int t = blockIdx.x + s * gridDim.x;
@@ -506,6 +509,7 @@ cudaError_t launch_dwconv3x3_tma(const CUtensorMap& in_map, const __nv_bfloat16*
   if (!dwconv_tma_plan_ok(h, wd, c, stride)) return cudaErrorInvalidValue;
   const DwPlan p = dw_plan((h - 1) / stride + 1, (wd - 1) / stride + 1, c, stride);
   DwKernelArgs a = make_args(p, n, h, wd, c, stride);
+  a.span = launch_span();
   a.w = w;
   a.bias = bias;
   a.y = reinterpret_cast<uint4*>(y);

@@ -28,6 +28,18 @@ inline int budgeted_sms(int device_sms) {
   return (b > 0 && b < device_sms) ? b : device_sms;
 }
 
+// Live per-kernel timing inside the real (graph-launched, PDL-chained)
+// forward: the runtime points each launch at a slot {sum, count}; CTA 0 of
+// the kernel adds the %globaltimer value at which it passed
+// griddepcontrol.wait (= when the previous kernel's grid completed) with
+// fire-and-forget reductions (no latency on the kernel's critical path).
+// Kernel k's in-situ duration over n forwards is (sum[k+1] - sum[k]) / n;
+// the forward's last kernel also marks its end into the slot after it.
+inline unsigned long long*& launch_span() {
+  static thread_local unsigned long long* slot = nullptr;
+  return slot;
+}
+
 inline bool pdl_enabled() {
   const bool on = [] {
     const char* e = std::getenv("DS_PDL");
@@ -74,6 +86,15 @@ cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, 
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void span_mark(unsigned long long* slot) {
+  if (slot != nullptr && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicAdd(slot, t);
+    atomicAdd(slot + 1, 1ull);
+  }
+}
 
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -104,6 +104,7 @@ struct PoolArgs {
   int stages;
   uint32_t box_bytes;     // TMA transaction bytes per box
   uint32_t stage_bytes;   // ring slot stride (box_bytes rounded up to 128 B: TMA destination alignment)
+  unsigned long long* span;  // live timing slot (pdl.cuh span_mark)
 };
 
 // Tile t -> (channel block [slowest], image, tile row, tile column).
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
   __syncthreads();
   pdl_trigger();
   pdl_wait();  // the input is the previous layer's output
+  span_mark(a.span);
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       const int t = blockIdx.x + s * gridDim.x;
@@ -318,6 +320,7 @@ cudaError_t launch_pool3x3_tma(const CUtensorMap& in_map, __nv_bfloat16* y, int 
   const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
   const PoolPlan p = pool_plan(ho, wo, c, stride);
   PoolArgs a{};
+  a.span = launch_span();
   a.y = reinterpret_cast<uint4*>(y);
   a.ldo_g = ldo / 8;
   a.coff_g = c_off / 8;

@@ -39,9 +39,10 @@ inline unsigned grid_for(long long work) {
 }
 
 __global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __restrict__ out,
-                                   long long pixels) {
+                                   long long pixels, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= pixels) return;
   const uint8_t* s = img + 3 * p;
@@ -56,9 +57,10 @@ __global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __res
 // above (zero outside the image and for c == 3). A stride-2 R x S conv over x
 // is then a stride-1 ceil(R/2) x ceil(S/2) conv over S with 16 channels.
 __global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restrict__ out, int h,
-                                 int w, int hs, int ws, int pad, long long pixels) {
+                                 int w, int hs, int ws, int pad, long long pixels, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   // (32-bit index arithmetic: the launcher keeps pixels below 2^31)
   const int i = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
   if (i >= pixels) return;
@@ -102,9 +104,10 @@ template <int STRIDE>
 __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
     const uint4* __restrict__ x, const __nv_bfloat16* __restrict__ w,
     const float* __restrict__ bias, uint4* __restrict__ y, int h, int wd, int c, int ho, int wo,
-    int cg_log2, int xq_per_row) {
+    int cg_log2, int xq_per_row, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   // grid.y = output row (image * ho + oy); x covers (column quad, channel group)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = 1 << cg_log2;
@@ -179,9 +182,10 @@ __global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
 // column is shared by at most two outputs and blocking does not pay).
 __global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
                                  const float4* __restrict__ bias, uint4* __restrict__ y, int h,
-                                 int wd, int cg, int ho, int wo, int stride, long long work) {
+                                 int wd, int cg, int ho, int wo, int stride, long long work, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= work) return;
   const int g = static_cast<int>(i % cg);
@@ -217,9 +221,10 @@ __global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __
 
 __global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
                                int cg, int ho, int wo, int stride, int pad, int is_max, int ldo_g,
-                               int coff_g, long long work) {
+                               int coff_g, long long work, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= work) return;
   const int g = static_cast<int>(i % cg);
@@ -296,9 +301,10 @@ __device__ __forceinline__ uint32_t max_bf16x2(uint32_t a, uint32_t b) {
 // output still sums its taps in row-outer, column-inner order.
 template <int STRIDE, bool IS_MAX, int ROWS>
 __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
-                                    int cg, int ho, int wo, int pad, int ldo_g, int coff_g) {
+                                    int cg, int ho, int wo, int pad, int ldo_g, int coff_g, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int ox = __float2int_rz(__int2float_rz(i) * (1.0f / static_cast<float>(cg)));
   if (ox * cg > i) --ox;
@@ -368,53 +374,71 @@ __global__ void pool3x3_rows_kernel(const uint4* __restrict__ x, uint4* __restri
   }
 }
 
-// Global average pool: one warp per (image, 256-channel block), lane l owns
-// channels [8l, 8l + 8) of the block, so every pixel is one coalesced 512 B
-// warp load. Each lane sums its pixels in order (p0 + p1 + ... in fp32, the
-// oracle's sequential order, so results equal it bit for bit) with eight
-// loads in flight, then divides by the pixel count.
-__global__ void global_avgpool_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int hw,
-                                      int cg, int blocks_per_image, int warps) {
+// Global average pool: one 256-thread block per (image, 256-channel block);
+// lane l of every warp owns channels [8l, 8l + 8) of the block (each pixel
+// is one coalesced 512 B warp load) and warp w sums pixels w, w + 8, ... in
+// order with all its loads in flight; the eight partial sums are added in
+// warp order through shared memory (deterministic), then divided by the
+// pixel count. One warp per block (the old layout) left ~4 warps per SM at
+// batch 128 and ran latency-bound at ~1 TB/s.
+constexpr int kGapWarps = 8;
+
+__global__ void __launch_bounds__(kGapWarps * 32) global_avgpool_kernel(
+    const uint4* __restrict__ x, uint4* __restrict__ y, int hw, int cg, int blocks_per_image,
+    unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= warps) return;
-  const int lane = threadIdx.x & 31;
-  const int n = w / blocks_per_image;
-  const int g = (w - n * blocks_per_image) * 32 + lane;
-  if (g >= cg) return;
+  span_mark(span);
+  __shared__ float part[kGapWarps][32][9];  // (+1 pad: conflict-free column reads)
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x / blocks_per_image;
+  const int g = (blockIdx.x - n * blocks_per_image) * 32 + lane;
+  const bool live = g < cg;
   const uint4* p = x + static_cast<long long>(n) * hw * cg + g;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  constexpr int U = 8;
-  int q0 = 0;
-  for (; q0 + U <= hw; q0 += U) {
-    uint4 v[U];
+  if (live) {
+    constexpr int U = 8;
+    int q = wid;
+    for (; q + (U - 1) * kGapWarps < hw; q += U * kGapWarps) {
+      uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldg(p + static_cast<long long>(q0 + u) * cg);
+      for (int u = 0; u < U; ++u) v[u] = __ldg(p + static_cast<long long>(q + u * kGapWarps) * cg);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U; ++u) {
+        float xv[8];
+        unpack8(v[u], xv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += xv[e];
+      }
+    }
+    for (; q < hw; q += kGapWarps) {
       float xv[8];
-      unpack8(v[u], xv);
+      unpack8(__ldg(p + static_cast<long long>(q) * cg), xv);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += xv[e];
     }
   }
-  for (; q0 < hw; ++q0) {
-    float xv[8];
-    unpack8(__ldg(p + static_cast<long long>(q0) * cg), xv);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] += xv[e];
-  }
+  for (int e = 0; e < 8; ++e) part[wid][lane][e] = acc[e];
+  __syncthreads();
+  if (wid != 0 || !live) return;
+  float sum[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sum[e] = part[0][lane][e];
+  for (int w = 1; w < kGapWarps; ++w)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sum[e] += part[w][lane][e];
   const float inv = static_cast<float>(hw);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = acc[e] / inv;
-  y[static_cast<long long>(n) * cg + g] = pack8(acc);
+  for (int e = 0; e < 8; ++e) sum[e] = sum[e] / inv;
+  y[static_cast<long long>(n) * cg + g] = pack8(sum);
 }
 
 __global__ void softmax_kernel(const float* __restrict__ logits, float* __restrict__ probs, int n,
-                               int classes) {
+                               int classes, unsigned long long* span) {
   pdl_trigger();
   pdl_wait();
+  span_mark(span);
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -446,6 +470,7 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
       const int j = lane + 32 * u;
       if (j < classes) p[j] = v[u] * inv;
     }
+    span_mark(span ? span + 2 : nullptr);  // the forward's end (last kernel)
     return;
   }
   float mx = -INFINITY;
@@ -458,6 +483,7 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float inv = 1.0f / sum;
   for (int j = lane; j < classes; j += 32) p[j] = expf(l[j] - mx) * inv;
+  span_mark(span ? span + 2 : nullptr);
 }
 
 }  // namespace
@@ -466,7 +492,7 @@ cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, in
                                cudaStream_t stream) {
   const long long pixels = static_cast<long long>(n) * h * w;
   return launch_pdl(stage_input_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
-                    reinterpret_cast<uint2*>(out), pixels);
+                    reinterpret_cast<uint2*>(out), pixels, launch_span());
   return cudaGetLastError();
 }
 
@@ -475,7 +501,7 @@ cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int 
   const long long pixels = static_cast<long long>(n) * hs * ws;
   if (pixels >= (1LL << 31)) return cudaErrorInvalidValue;
   return launch_pdl(stage_s2d_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
-                    reinterpret_cast<uint4*>(out), h, w, hs, ws, pad, pixels);
+                    reinterpret_cast<uint4*>(out), h, w, hs, ws, pad, pixels, launch_span());
 }
 
 cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
@@ -494,13 +520,13 @@ cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, con
     const int bt = block_for(xq * cg);
     return launch_pdl(dwconv3x3_kernel<1>, dim3((xq * cg + bt - 1) / bt, rows), dim3(bt), 0, stream,
                       reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h,
-                      wd, c, ho, wo, cg_log2, xq);
+                      wd, c, ho, wo, cg_log2, xq, launch_span());
   } else {
     const long long pw = static_cast<long long>(n) * ho * wo * cg;
     return launch_pdl(dwconv3x3_px_kernel, dim3(grid_for(pw)), dim3(kBlock), 0, stream,
                       reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
                       reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd,
-                      cg, ho, wo, stride, pw);
+                      cg, ho, wo, stride, pw, launch_span());
   }
   return cudaGetLastError();
 }
@@ -523,7 +549,7 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
     const dim3 grid((per_row + bt - 1) / bt, yrows);
     auto go = [&](auto kernel) {
       return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
-                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8);
+                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8, launch_span());
     };
     if (prows == 1) {
       if (stride == 1)
@@ -542,7 +568,7 @@ cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int 
   const long long work = static_cast<long long>(n) * ho * wo * cg;
   return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
                     reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho,
-                    wo, stride, pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work);
+                    wo, stride, pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work, launch_span());
   return cudaGetLastError();
 }
 
@@ -550,19 +576,16 @@ cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int 
                                   cudaStream_t stream) {
   const int cg = c / 8;
   const int bpi = (cg + 31) / 32;  // 256-channel blocks per image
-  const int warps = n * bpi;
-  const int per_block = kBlock / 32;
-  return launch_pdl(global_avgpool_kernel, dim3((warps + per_block - 1) / per_block), dim3(kBlock),
-                    0, stream, reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw,
-                    cg, bpi, warps);
-  return cudaGetLastError();
+  return launch_pdl(global_avgpool_kernel, dim3(n * bpi), dim3(kGapWarps * 32), 0, stream,
+                    reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), hw, cg, bpi,
+                    launch_span());
 }
 
 cudaError_t launch_softmax(const float* logits, float* probs, int n, int classes,
                            cudaStream_t stream) {
   const int rows_per_block = kBlock / 32;
   return launch_pdl(softmax_kernel, dim3((n + rows_per_block - 1) / rows_per_block), dim3(kBlock),
-                    0, stream, logits, probs, n, classes);
+                    0, stream, logits, probs, n, classes, launch_span());
   return cudaGetLastError();
 }
 

@@ -172,6 +172,24 @@ ds_status ds_set_mt_mode(ds_backend* b, int mode) {
 
 int ds_get_mt_mode(const ds_backend* b) { return b ? b->impl->mt_mode() : -1; }
 
+ds_status ds_kernel_spans(ds_backend* b, int instance, int reset, double* ms_out, int cap,
+                          int64_t* forwards) {
+  if (!b) return null_handle();
+  return guard([&] {
+    if (reset) {
+      b->impl->reset_spans(instance);
+      if (forwards) *forwards = 0;
+      return;
+    }
+    std::vector<double> ms;
+    const int64_t n = b->impl->read_spans(instance, &ms);
+    if (n < 0) throw std::runtime_error("live kernel timing slots disagree");
+    if (forwards) *forwards = n;
+    if (ms_out)
+      for (int i = 0; i < cap && i < static_cast<int>(ms.size()); ++i) ms_out[i] = ms[i];
+  });
+}
+
 ds_status ds_drain(ds_backend* b) {
   if (!b) return null_handle();
   return guard([&] { b->impl->drain(); });

@@ -485,11 +485,33 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
         a.y_tma = encode_tmap_out(&a.tmap_y, base, rows, p.cout, out.c, out.f32) ? 1 : 0;
     }
   }
+  spans_bytes_ = sizeof(unsigned long long) * 2 * (kernels_per_forward_ + 1);
+  check_cuda(cudaMalloc(&d_spans_, spans_bytes_), "cudaMalloc spans");
+  check_cuda(cudaMemsetAsync(d_spans_, 0, spans_bytes_, stream_), "zero spans");
   check_cuda(cudaStreamSynchronize(stream_), "instance setup");
+}
+
+void Instance::reset_spans() {
+  check_cuda(cudaMemset(d_spans_, 0, spans_bytes_), "reset spans");
+}
+
+int64_t Instance::read_spans(std::vector<double>* ms) const {
+  std::vector<unsigned long long> h(spans_bytes_ / sizeof(unsigned long long));
+  check_cuda(cudaMemcpy(h.data(), d_spans_, spans_bytes_, cudaMemcpyDeviceToHost), "read spans");
+  const int k = kernels_per_forward_;
+  const unsigned long long n = h[1];
+  ms->assign(k, 0.0);
+  for (int i = 0; i <= k; ++i)
+    if (h[2 * i + 1] != n) return -1;  // a kernel without a live-timing slot, or in flight
+  if (n == 0) return 0;
+  for (int i = 0; i < k; ++i)
+    (*ms)[i] = static_cast<double>(h[2 * (i + 1)] - h[2 * i]) / static_cast<double>(n) / 1e6;
+  return static_cast<int64_t>(n);
 }
 
 Instance::~Instance() {
   cudaSetDevice(device_);
+  if (d_spans_) cudaFree(d_spans_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   if (copy_stream_) cudaStreamSynchronize(copy_stream_);
@@ -511,12 +533,21 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
   const ModelSpec& m = m_;
   const HostParams& hp = params_for(m);
   size_t mark = 0;
+  int launch = 0;  // kernel index in the forward: its live-timing slot
+  launch_span() = d_spans_;
   auto record_mark = [&] {
+    ++launch;
+    launch_span() = d_spans_ + 2 * launch;
     if (marks)
       check_cuda(cudaEventRecordWithFlags((*marks)[mark++], cur_stream_, cudaEventRecordExternal),
                  "mark");
   };
-  record_mark();
+  struct SpanReset {
+    ~SpanReset() { launch_span() = nullptr; }
+  } span_reset;
+  if (marks)
+    check_cuda(cudaEventRecordWithFlags((*marks)[mark++], cur_stream_, cudaEventRecordExternal),
+               "mark");
   if (s2d_.op >= 0) {
     check_cuda(launch_stage_s2d(d_images_[slot], d_s2d_, bs, m.in_h, m.in_w, s2d_.hs, s2d_.ws,
                                 s2d_.pad, cur_stream_),

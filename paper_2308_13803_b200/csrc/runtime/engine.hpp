@@ -72,6 +72,11 @@ class Instance {
   cudaEvent_t out_read(int slot) const { return out_read_[slot]; }
   float* probs() const { return d_probs_; }
   int max_bs() const { return max_bs_; }
+  // Live per-kernel timing (pdl.cuh span_mark): zero the slots; then the
+  // in-situ duration of each kernel of the forward averaged over the forwards
+  // run since (returns that count, or -1 when the slots disagree).
+  void reset_spans();
+  int64_t read_spans(std::vector<double>* ms) const;
   int kernels_per_forward() const { return kernels_per_forward_; }
   size_t device_bytes() const { return device_bytes_; }
 
@@ -113,6 +118,8 @@ class Instance {
   std::vector<CUtensorMap> pool_maps_;  // TMA halo maps of pool inputs (by op)
   std::vector<bool> pool_tma_;          // pool op uses the TMA kernel (DS_POOL_TMA=0: off)
   std::map<int64_t, cudaGraphExec_t> graphs_;
+  unsigned long long* d_spans_ = nullptr;  // [kernels + 1] x {sum of start times, count}
+  size_t spans_bytes_ = 0;
   int kernels_per_forward_ = 0;
 };
 
@@ -171,6 +178,15 @@ class Backend {
   std::vector<double> profile_kernels(int bs, int reps) {
     drain();
     return instance(0).profile_kernels(bs, reps);
+  }
+  // Live per-kernel timing of instance i (see Instance::read_spans).
+  void reset_spans(int i) {
+    drain();
+    instance(i).reset_spans();
+  }
+  int64_t read_spans(int i, std::vector<double>* ms) {
+    drain();
+    return instance(i).read_spans(ms);
   }
 
   const ModelSpec& model() const { return model_; }

@@ -189,6 +189,7 @@ def serve(be: GpuBackend, model: str, *, controller: str = "dnnscaler", slo_fact
         if nvtx:
             nvtx(tag, True)
         be.timer_start()
+        be.reset_kernel_spans(0)
         recs = []
         for _ in range(k):
             rec, _ = sess.step()
@@ -198,13 +199,17 @@ def serve(be: GpuBackend, model: str, *, controller: str = "dnnscaler", slo_fact
         ms = be.timer_stop()
         if nvtx:
             nvtx(tag, False)
+        spans[tag] = be.kernel_spans(0)
         return items, ms, recs, st0, be.stats()
+
+    spans = {}
 
     if between is not None:
         items, ms, recs, st0, st1 = between(lambda: timed(steps, "timed"))
     else:
         items, ms, recs, st0, st1 = timed(steps, "timed")
-    out = {"items": items, "ms": ms, "launches": int(st1["kernel_launches"] - st0["kernel_launches"])}
+    out = {"items": items, "ms": ms, "launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+           "kernel_spans_ms": spans["timed"][0].tolist(), "span_forwards": spans["timed"][1]}
     e_warm = 0
     if e2e:
         be.set_host_io(True)

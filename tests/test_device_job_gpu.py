@@ -201,3 +201,22 @@ def test_combination_sweep_on_device():
     by = {(c["bs"], c["mtl"]): c for c in cells}
     # two concurrent instances deliver more than one (or at worst about the same)
     assert by[(8, 2)]["measured_throughput"] > 0.8 * by[(8, 1)]["measured_throughput"]
+
+
+@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 64), ("resnet50_v1", 32)])
+def test_live_kernel_spans(model, bs):
+    """Live per-kernel timing inside the real graph launches (ds_kernel_spans):
+    every kernel of the forward has a positive in-situ span, and the spans of
+    one forward add up to the forward's device time (back-to-back batches)."""
+    with GpuBackend(model, Config(abs_max_bs=bs, max_mtl=1)) as be:
+        be.run_batches(bs, 5)
+        be.timer_start()
+        be.reset_kernel_spans(0)
+        be.run_batches(bs, 40)
+        ms = be.timer_stop()
+        spans, n = be.kernel_spans(0)
+    assert n == 40 + 1  # (the run keeps kDepth requests in flight: one more forward ran)
+    assert np.all(spans > 0), spans
+    per_fwd = ms / n
+    print(f"{model} bs {bs}: sum of spans {spans.sum():.4f} ms vs timer {per_fwd:.4f} ms per forward")
+    assert 0.7 * per_fwd < spans.sum() < 1.1 * per_fwd
