@@ -90,14 +90,16 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
 }
 
 // Bring-up timeline stamps (args.ts, tools/test_conv_gemm TS=1): slot k of
-// this CTA's 64 = clock64() (slot 4: at entry). Slots: 0 entry globaltimer (ns),
-// 1 pdl_wait done, 2 MMA loop done, 3 exit; per tile j < 8: 8+j first A/B
-// stage landed (MMA), 16+j tile committed (MMA), 24+j epilogue got the
-// accumulator, 32+j epilogue stores issued, 40+j TMA first load issued.
-// (raw clocks; slot 4 holds the entry clock, which the tool subtracts, so no
-// register stays live for it)
+// this CTA's 64 = %globaltimer (ns). Slots: 0 and 1 pdl_wait done, 2 MMA loop
+// done, 3 exit, 4 entry, 5 prologue done (before pdl_wait); per tile j < 8:
+// 8+j first A/B stage landed (MMA), 16+j tile committed (MMA), 24+j epilogue
+// got the accumulator, 32+j epilogue stores issued, 40+j TMA first load issued.
 __device__ __forceinline__ void ts_mark(unsigned long long* ts, int k, long long = 0) {
-  if (ts) ts[blockIdx.x * 64 + k] = static_cast<unsigned long long>(clock64());
+  if (ts) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ts[blockIdx.x * 64 + k] = t;
+  }
 }
 
 // floor(a / d) for a < 2^24 through a float reciprocal computed once per
@@ -938,6 +940,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (cl > 1) ptx::cluster_sync();  // peers' barriers exist before any multicast lands
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) ts_mark(args.ts, 5);
   pdl_trigger();
   pdl_wait();  // activations (and the residual) come from earlier layers
   span_mark(args.span);

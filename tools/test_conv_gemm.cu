@@ -64,6 +64,10 @@ static int run(const Case& cs) {
   ConvGemmArgs a{};
   a.cluster = getenv("CLUSTER") ? atoi(getenv("CLUSTER")) : 1;  // 2: CTA pairs multicast B
   ConvLoadMode mode = cs.mode;
+  Case cs_bn = cs;  // BN=<n> overrides the case's N tile (A/B experiments)
+  if (getenv("BN")) cs_bn.BN = atoi(getenv("BN"));
+  const Case& cs2 = cs_bn;
+#define cs cs2
   const bool pd = getenv("PWDW") && mode == ConvLoadMode::kTmaA;  // + depthwise epilogue (timing only)
   if (pd) {
     mode = ConvLoadMode::kPwDw;
@@ -104,6 +108,7 @@ static int run(const Case& cs) {
   if (getenv("STAGES")) a.stages = atoi(getenv("STAGES"));
   if (getenv("DEBUG_FLAGS")) a.debug_flags = atoi(getenv("DEBUG_FLAGS"));
   if (getenv("TMEM_COLS")) a.tmem_cols = atoi(getenv("TMEM_COLS"));  // 512 forces 1 CTA/SM
+#undef cs
   a.bias = db; a.residual = cs.residual ? dr : nullptr; a.ld_res = cs.Cout;
   a.y = dy; a.ldy = ldy; a.c_off = cs.c_off; a.out_f32 = cs.f32; a.relu = cs.relu;
   // channels [c_off, c_off+Cout) of an ldy-wide buffer; keep Cout+c_off <= ldy
@@ -123,44 +128,55 @@ static int run(const Case& cs) {
   float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
   ms /= 20;
 
-  if (getenv("TS")) {  // per-CTA timeline of one launch (3rd of 3 back to back)
-    unsigned long long* dts;
+  if (getenv("TS")) {  // per-CTA timelines of launches 2 and 3 of 3 back to back (globaltimer)
     const int nct = 148 * 2;
-    cudaMalloc(&dts, nct * 64 * 8);
-    cudaMemset(dts, 0, nct * 64 * 8);
-    a.ts = dts;
-    for (int i = 0; i < 3; ++i) launch_conv_gemm(a, mode, 0);
+    unsigned long long* dts[2];
+    for (auto& d : dts) {
+      cudaMalloc(&d, nct * 64 * 8);
+      cudaMemset(d, 0, nct * 64 * 8);
+    }
+    launch_conv_gemm(a, mode, 0);
+    for (int i = 0; i < 2; ++i) {
+      a.ts = dts[i];
+      launch_conv_gemm(a, mode, 0);
+    }
     cudaDeviceSynchronize();
-    std::vector<unsigned long long> h(nct * 64);
-    cudaMemcpy(h.data(), dts, h.size() * 8, cudaMemcpyDeviceToHost);
+    std::vector<unsigned long long> h[2];
+    for (int i = 0; i < 2; ++i) {
+      h[i].resize(nct * 64);
+      cudaMemcpy(h[i].data(), dts[i], h[i].size() * 8, cudaMemcpyDeviceToHost);
+      cudaFree(dts[i]);
+    }
     a.ts = nullptr;
-    cudaFree(dts);
-    unsigned long long g0 = ~0ull, g1 = 0;
-    int ctas = 0;
+    unsigned long long t0 = ~0ull;  // earliest entry of launch 3
     for (int c = 0; c < nct; ++c)
-      if (h[c * 64]) { g0 = std::min(g0, h[c * 64]); g1 = std::max(g1, h[c * 64]); ++ctas; }
-    printf("  timeline: %d CTAs, entry spread %.2f us (globaltimer)\n", ctas, (g1 - g0) * 1e-3);
-    auto stat = [&](int k, const char* name) {
+      if (h[1][c * 64 + 4]) t0 = std::min(t0, h[1][c * 64 + 4]);
+    auto stat = [&](int l, int k, const char* name) {
       std::vector<double> v;
-      for (int c = 0; c < ctas; ++c)
-        if (h[c * 64 + k]) v.push_back((h[c * 64 + k] - h[c * 64 + 4]) / 1965.0);
+      for (int c = 0; c < nct; ++c)
+        if (h[l][c * 64 + k]) v.push_back((static_cast<double>(h[l][c * 64 + k]) - t0) * 1e-3);
       if (v.empty()) return;
       std::sort(v.begin(), v.end());
-      printf("  %-22s n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", name, v.size(), v[0],
+      printf("  %-26s n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", name, v.size(), v[0],
              v[v.size() / 2], v.back());
     };
-    stat(1, "pdl_wait done");
+    printf("  timeline (us from launch 3's first CTA entry)\n");
+    stat(0, 2, "L2 MMA loop done");
+    stat(0, 3, "L2 exit barrier");
+    stat(1, 4, "entry");
+    stat(1, 5, "prologue done");
+    stat(1, 1, "pdl_wait done");
     for (int j = 0; j < 8; ++j) {
       char nm[64];
-      snprintf(nm, sizeof nm, "tile%d TMA issue", j); stat(40 + j, nm);
-      snprintf(nm, sizeof nm, "tile%d MMA first", j); stat(8 + j, nm);
-      snprintf(nm, sizeof nm, "tile%d MMA commit", j); stat(16 + j, nm);
-      snprintf(nm, sizeof nm, "tile%d epi start", j); stat(24 + j, nm);
-      snprintf(nm, sizeof nm, "tile%d halo0 done", j); stat(48 + j, nm);
-      snprintf(nm, sizeof nm, "tile%d epi end", j); stat(32 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d TMA issue", j); stat(1, 40 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d MMA first", j); stat(1, 8 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d MMA commit", j); stat(1, 16 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d epi start", j); stat(1, 24 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d halo0 done", j); stat(1, 48 + j, nm);
+      snprintf(nm, sizeof nm, "tile%d epi end", j); stat(1, 32 + j, nm);
     }
-    stat(2, "MMA loop done");
-    stat(3, "exit barrier");
+    stat(1, 2, "MMA loop done");
+    stat(1, 3, "exit barrier");
   }
 
   if (pd) {
@@ -224,6 +240,7 @@ int main(int argc, char** argv) {
       {"mbv1 pw2 bs128", 128, 56, 56, 64, 1, 1, 1, 1, 0, 0, 128, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 pw7 bs128", 128, 14, 14, 512, 1, 1, 1, 1, 0, 0, 512, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 pw5 bs128", 128, 28, 28, 256, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"mbv1 fc bs128", 128, 1, 1, 1024, 1, 1, 1, 1, 0, 0, 1000, 64, ConvLoadMode::kTmaA, false, true, false, 0, 0},
       {"mbv1 pw4 bs128", 128, 28, 28, 128, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
   };
   // Optional filter: substring of the case name; "--no-check" skips the CPU reference.
