@@ -44,9 +44,6 @@ constexpr int kABytes = kConvBM * kConvBK * 2;  // 16 KiB per stage
 // Output staging for the TMA-store epilogue: per epilogue warp two buffers
 // of 32 rows x 128 B (64 bf16 or 32 fp32 columns, 128 B-swizzled).
 constexpr int kYStageBytes = 32 * 128;
-// kPwDw: per epilogue team one zero-bordered halo buffer of up to 16 x 16
-// pixels x 64 channels (the two fill the sixteen warps' output staging)
-constexpr int kPdHaloBytes = 16 * 16 * 128;
 // Staging buffers per epilogue warp: two (the next group fills while the
 // last one's TMA store reads), one when sixteen warps drain (smem for the ring).
 __host__ __device__ constexpr int y_bufs(int epi_warps) { return epi_warps > 8 ? 1 : 2; }
@@ -61,29 +58,26 @@ constexpr int kTmaWarp = 16;      // weight (and A) TMA producer, TMEM owner
 // warp 17: tcgen05.mma issuer (the role branch's final else)
 
 struct SmemLayout {
-  uint32_t a_off, b_off, box_off, win_off, y_off, bar_off, bias_off, total;
+  uint32_t a_off, b_off, win_off, y_off, bar_off, bias_off, total;
 };
 
 // b_res_blocks > 0: the layer's whole weight matrix (num_kb blocks of
 // BN x 64) stays resident in shared memory for all tiles (one N tile, small
 // K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
-                                                  int b_res_blocks = 0, int mt = 1,
-                                                  int box_bytes = 0, int win_bytes = 0) {
+                                                  int b_res_blocks = 0, int mt = 1, int win_bytes = 0) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * mt * kABytes;  // stage = mt A sub-tiles
   const int b_blocks = b_res_blocks > 0 ? b_res_blocks : stages;
-  L.box_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;  // kDwFused halo boxes
-  // (box slots rounded to 1 KiB: the 128 B-swizzled staging after them needs it)
-  L.y_off = L.box_off + static_cast<uint32_t>(stages) * ((box_bytes + 1023) / 1024 * 1024);
+  L.y_off = L.b_off + static_cast<uint32_t>(b_blocks) * BN * 128;
   // kWindow: raw[2] + chunk-major[2] halo boxes
   L.win_off = L.y_off;
   L.y_off += 4 * static_cast<uint32_t>((win_bytes + 1023) / 1024 * 1024);
   L.bar_off = L.y_off + epi_warps * y_bufs(epi_warps) * kYStageBytes;
   // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
-  // box_full[stages], win barriers[8], tmem slot, residual-staging barriers[2 x 16 warps]
-  L.bias_off = L.bar_off + ((3 * stages + 2 * kMaxAcc + 2 + 8 + 32) * 8 + 15) / 16 * 16;
+  // win barriers[8], tmem slot, residual-staging barriers[2 x 16 warps]
+  L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 2 + 8 + 32) * 8 + 15) / 16 * 16;
   // bias padded so a 32-column epilogue slice never reads past it
   L.total = L.bias_off + static_cast<uint32_t>((cout + 63) / 64 * 64 + 64) * 4;
   return L;
@@ -249,127 +243,6 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
 __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// Depthwise-fused producer (kDwFused): the tile is a TH x TW block of output
-// pixels of one image (A row r = pixel (r / TW, r % TW); rows past TH*TW are
-// never stored). For each K block (cb <= 64 channels) the TMA warp lands the
-// block's input halo box {cb, IW, IH} in smem (padding reads as zeros); the
-// gather warps compute A = relu(dw3x3(x) + b) from it, two horizontally
-// adjacent outputs x 8 channels per item with FHFMA.BF16 (the same fp32 fma
-// sequence as the standalone depthwise kernels, so the bf16 A equals their
-// stored output bit for bit), straight into the 128 B-swizzled A stage. The
-// depthwise activation never goes to HBM.
-__device__ __forceinline__ float dw_fma_lo(uint32_t x, uint32_t w, float c) {
-  float d;
-  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
-      "mov.b32 {xl, xh}, %1;\n\t"
-      "mov.b32 {wl, wh}, %2;\n\t"
-      "fma.rn.f32.bf16 %0, xl, wl, %3;}"
-      : "=f"(d)
-      : "r"(x), "r"(w), "f"(c));
-  return d;
-}
-
-__device__ __forceinline__ float dw_fma_hi(uint32_t x, uint32_t w, float c) {
-  float d;
-  asm("{.reg .b16 xl, xh, wl, wh;\n\t"
-      "mov.b32 {xl, xh}, %1;\n\t"
-      "mov.b32 {wl, wh}, %2;\n\t"
-      "fma.rn.f32.bf16 %0, xh, wh, %3;}"
-      : "=f"(d)
-      : "r"(x), "r"(w), "f"(c));
-  return d;
-}
-
-__device__ __forceinline__ void dw_fma8(float (&acc)[8], const uint4& x, const uint4& w) {
-  acc[0] = dw_fma_lo(x.x, w.x, acc[0]);
-  acc[1] = dw_fma_hi(x.x, w.x, acc[1]);
-  acc[2] = dw_fma_lo(x.y, w.y, acc[2]);
-  acc[3] = dw_fma_hi(x.y, w.y, acc[3]);
-  acc[4] = dw_fma_lo(x.z, w.z, acc[4]);
-  acc[5] = dw_fma_hi(x.z, w.z, acc[5]);
-  acc[6] = dw_fma_lo(x.w, w.w, acc[6]);
-  acc[7] = dw_fma_hi(x.w, w.w, acc[7]);
-}
-
-__device__ __forceinline__ uint4 relu_pack8(const float (&v)[8]) {
-  return make_uint4(pack2_bf16(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)),
-                    pack2_bf16(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)),
-                    pack2_bf16(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)),
-                    pack2_bf16(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
-}
-
-// A producer thread's depthwise items (fixed for every tile and K block: the
-// tile shape is fixed): two horizontally adjacent outputs x one 8-channel group
-// each, as the uint4 offset of the items' top-left input in the box and the
-// A row of the first output.
-struct DwItems {
-  int n;
-  int box_off[2];
-  int row_a[2];
-};
-
-__device__ __forceinline__ DwItems dw_items(const ConvGemmArgs& a, int tid, int S) {
-  DwItems d{0, {0, 0}, {0, 0}};
-  const int groups = a.dw_cb >> 3;
-  const int g = tid & (groups - 1);
-  const int half_tw = a.dw_tw >> 1;
-  const int items = a.dw_th * half_tw * groups;
-  for (int it = tid; it < items && d.n < 2; it += kGatherWarps * 32, ++d.n) {
-    const int strip = it / groups;
-    const int ty = strip / half_tw;
-    const int tx = (strip - ty * half_tw) * 2;
-    d.box_off[d.n] = (ty * S * a.dw_iw + tx * S) * groups + g;
-    // A row of pixel (ty, tx): warp ty / rw, lane (ty % rw) * tw + tx
-    d.row_a[d.n] = (ty / a.dw_rw) * 32 + (ty % a.dw_rw) * a.dw_tw + tx;
-  }
-  return d;
-}
-
-// One K block of one tile: box (smem, [IH][IW][groups] uint4) -> A stage.
-template <int S>
-__device__ __forceinline__ void dw_box_to_a(const ConvGemmArgs& a, const uint4* box, uint32_t a_stage,
-                                            int kb, int tid, const DwItems& di) {
-  constexpr int XN = S + 3;  // input columns of two adjacent outputs
-  const int groups = a.dw_cb >> 3;
-  const int g = tid & (groups - 1);  // fixed per thread (groups divides the thread count)
-  const int cg_all = a.C >> 3;
-  const int gg = kb * groups + g;
-  uint4 w[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(a.dw_w) + k * cg_all + gg);
-  const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg);
-  const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.dw_b) + 2 * gg + 1);
-  const int row_stride = a.dw_iw * groups;  // uint4 per box row
-#pragma unroll 2
-  for (int i = 0; i < di.n; ++i) {
-    float acc[2][8];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      acc[q][0] = b0.x; acc[q][1] = b0.y; acc[q][2] = b0.z; acc[q][3] = b0.w;
-      acc[q][4] = b1.x; acc[q][5] = b1.y; acc[q][6] = b1.z; acc[q][7] = b1.w;
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const uint4* row = box + di.box_off[i] + r * row_stride;
-      uint4 xv[XN];
-#pragma unroll
-      for (int u = 0; u < XN; ++u) xv[u] = row[u * groups];
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) dw_fma8(acc[q], xv[q * S + c], w[r * 3 + c]);
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int row_a = di.row_a[i] + q;
-      const uint32_t rowp = a_stage + row_a * 128;
-      ptx::sts128(rowp + ((g ^ (row_a & 7)) << 4), relu_pack8(acc[q]));
-      if (groups == 4)  // 32-channel layer: the K block's upper half is zero
-        ptx::sts128(rowp + (((g + 4) ^ (row_a & 7)) << 4), make_uint4(0u, 0u, 0u, 0u));
-    }
-  }
 }
 
 // Stem producer (kStemU8): the stem conv reads the u8 images [n][H][W][3]
@@ -645,179 +518,19 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
   }
 }
 
-// Depthwise 3x3 (+bias, ReLU) of one 64-channel round from the halo buffer:
-// items are (output row, strip of kPdQ outputs, 4-channel group g4); each
-// input vector of a strip row is loaded once and feeds up to three outputs,
-// in the standalone kernels' per-output fma order (row r outer, tap s inner).
-constexpr int kPdQ = 7;
-
-__device__ __forceinline__ void dw_fma4(float (&acc)[4], const uint2& x, const uint2& w) {
-  acc[0] = dw_fma_lo(x.x, w.x, acc[0]);
-  acc[1] = dw_fma_hi(x.x, w.x, acc[1]);
-  acc[2] = dw_fma_lo(x.y, w.y, acc[2]);
-  acc[3] = dw_fma_hi(x.y, w.y, acc[3]);
-}
-
-template <int S>
-__device__ __forceinline__ void pwdw_strips(uint32_t halo, uint32_t wp, uint32_t bp, int cout, int hp_w,
-                                            int hd, int wd, int g4, int tid, __nv_bfloat16* yimg, int ldy) {
-  const int strips = wd / kPdQ;
-  const int items = hd * strips * 16;
-  const int chunk = g4 >> 1, half = (g4 & 1) * 8;  // 8 B half of a 16 B halo chunk
-  for (int it = tid; it < items; it += 256) {
-    const int rest = it >> 4;
-    const int oy = rest / strips, strip = rest - (rest / strips) * strips;
-    float a[kPdQ][4];
-    {
-      uint4 b;
-      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "r"(bp));
-#pragma unroll
-      for (int q = 0; q < kPdQ; ++q) {
-        a[q][0] = __uint_as_float(b.x); a[q][1] = __uint_as_float(b.y);
-        a[q][2] = __uint_as_float(b.z); a[q][3] = __uint_as_float(b.w);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      uint2 w[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) w[c] = ptx::lds64(wp + (r * 3 + c) * cout * 2);
-      const int h0 = (oy * S + r) * hp_w + strip * kPdQ * S;
-#pragma unroll
-      for (int u = 0; u < (kPdQ - 1) * S + 3; ++u) {
-        const int hq = h0 + u;
-        const uint2 x = ptx::lds64(halo + hq * 128 + ((chunk ^ (hq & 7)) << 4) + half);
-        // outputs q with q * S + c == u, taps c in ascending order
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if ((u - c) >= 0 && (u - c) % S == 0 && (u - c) / S < kPdQ) dw_fma4(a[(u - c) / S], x, w[c]);
-      }
-    }
-    __nv_bfloat16* yp = yimg + (static_cast<size_t>(oy) * wd + strip * kPdQ) * ldy;
-#pragma unroll
-    for (int q = 0; q < kPdQ; ++q)
-      *reinterpret_cast<uint2*>(yp + q * ldy) =
-          make_uint2(pack2_bf16(fmaxf(a[q][0], 0.f), fmaxf(a[q][1], 0.f)),
-                     pack2_bf16(fmaxf(a[q][2], 0.f), fmaxf(a[q][3], 0.f)));
-  }
-}
-
-// kPwDw epilogue. Two teams of eight warps take alternate tiles (tile j ->
-// team j % 2, accumulator j % n_acc); a tile is one image's Ho x Wo pixels
-// (mt 128-row sub-tiles) x BN pointwise channels. Per 64-channel round the
-// team's warps move TMEM (warp: lane quarter w % 4 of sub-tile (w / 4) % 2,
-// two 32-column slices) + bias, ReLU, bf16 into the team's zero-bordered halo
-// buffer [(Ho + 2) x (Wo + 2) pixels][64 ch] (16 B chunk c of pixel p at
-// c ^ (p & 7): conflict-free), then compute the depthwise 3x3 (stride
-// dw_stride, pad 1) + bias + ReLU of those 64 channels straight to HBM with
-// the standalone kernels' fma order, so the result is bit-identical to the
-// two-kernel path. The pointwise output never leaves shared memory.
-__device__ __forceinline__ void pwdw_epilogue(const ConvGemmArgs& args, uint8_t* halo_base, uint32_t dwp,
-                                           const float* bias_s, uint32_t tmem_base, uint32_t acc_stride,
-                                           uint64_t* tmem_full, uint64_t* tmem_empty, int n_acc,
-                                           int acc_log2, int n_tiles, int warp, int lane) {
-  const int team = warp >> 3;
-  const int quarter = warp & 3;
-  const int sub = (warp >> 2) & 1;
-  const int tid = threadIdx.x & 255;  // thread index in the team
-  const int hw = args.Ho * args.Wo;
-  const int hp_w = args.Wo + 2;  // halo row pitch (pixels)
-  const int S = args.dw_stride;
-  const int hd = (args.Ho - 1) / S + 1, wd = (args.Wo - 1) / S + 1;
-  const uint32_t halo = ptx::smem_u32(halo_base) + team * kPdHaloBytes;
-  const int barrier_id = 2 + team;
-  // depthwise weights [9][Cout] bf16 then bias [Cout] fp32, staged in smem at dwp
-  const uint32_t dw_bias = dwp + 9 * args.Cout * 2;
-  const int p = sub * kConvBM + quarter * 32 + lane;  // this lane's pixel in the image
-  const bool row_ok = sub < args.mt && p < hw;
-  const int py = p / args.Wo, px = p - (p / args.Wo) * args.Wo;
-  const int hpix = (py + 1) * hp_w + px + 1;
-  // (CTA pairs: units of (image pair, N block); this CTA's image is 2 * pair + rank)
-  const int cl = args.cluster > 1 ? 2 : 1;
-  const int images = args.M / hw;
-  TileWalk tw(n_tiles, cl);
-  const int walk_count = n_tiles * ((images + cl - 1) / cl);
-  uint32_t j = 0;
-  for (int tile = blockIdx.x / cl; tile < walk_count; tile += gridDim.x / cl, ++j, tw.next()) {
-    if (static_cast<int>(j & 1) != team) continue;
-    const bool img_ok = tw.mb < images;
-    const int n0 = tw.nb * args.BN;
-    const uint32_t acc = j & (n_acc - 1);
-    ptx::mbar_wait(&tmem_full[acc], (j >> acc_log2) & 1);
-    ptx::tc_fence_after();
-    const bool stamp = args.ts && (warp & 7) == 0 && lane == 0 && j < 8;
-    if (stamp) ts_mark(args.ts, 24 + j);
-    const int rounds = args.BN / 64;
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int c0 = n0 + rd * 64;  // first pointwise / depthwise channel of the round
-      if (sub < args.mt && img_ok) {
-        const uint32_t t_row = tmem_base + acc * acc_stride + sub * args.BN + rd * 64 +
-                               (static_cast<uint32_t>(quarter * 32) << 16);
-#pragma unroll
-        for (int sl = 0; sl < 2; ++sl) {
-          uint32_t raw[32];
-          ptx::tmem_ld_32x32b_x32(t_row + sl * 32, raw);
-          ptx::tmem_ld_wait();
-          if (row_ok) {
-            const float* b = bias_s + c0 + sl * 32;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(raw[8 * k + e]) + b[8 * k + e];
-              ptx::sts128(halo + hpix * 128 + (((sl * 4 + k) ^ (hpix & 7)) << 4), relu_pack8(v));
-            }
-          }
-        }
-      }
-      if (rd == rounds - 1) {  // this warp's TMEM reads of the tile are done
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (cl > 1 && tw.rank != 0)
-            ptx::mbar_arrive_cluster(&tmem_empty[acc], 0);  // the leader's MMA reuses it
-          else
-            ptx::mbar_arrive(&tmem_empty[acc]);
-        }
-      }
-      if (!img_ok) continue;  // (odd image count: the pair's second CTA has no image)
-      asm volatile("bar.sync %0, 256;" ::"r"(barrier_id) : "memory");  // halo complete
-      if (stamp && rd == 0) ts_mark(args.ts, 48 + j);
-      const int g4 = tid & 15;    // this thread's 4-channel group of the round
-      const int ch = c0 + g4 * 4;
-      __nv_bfloat16* yimg = static_cast<__nv_bfloat16*>(args.y) +
-                            static_cast<size_t>(tw.mb) * hd * wd * args.ldy + ch;
-      if (S == 1)
-        pwdw_strips<1>(halo, dwp + ch * 2, dw_bias + ch * 4, args.Cout, hp_w, hd, wd, g4, tid, yimg,
-                       args.ldy);
-      else
-        pwdw_strips<2>(halo, dwp + ch * 2, dw_bias + ch * 4, args.Cout, hp_w, hd, wd, g4, tid, yimg,
-                       args.ldy);
-      asm volatile("bar.sync %0, 256;" ::"r"(barrier_id) : "memory");  // halo reads done
-    }
-    if (stamp) ts_mark(args.ts, 32 + j);
-  }
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_gemm_kernel(const __grid_constant__ ConvGemmArgs args) {
   // kPairTmaA: a TMA-A conv on CTA pairs, one M = 256 pair MMA per K step
   // (cta_group::2 throughout), each CTA holding half of every B block
-  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA) ||
-                        MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
-  // kPwDw: a 1x1 conv whose tile is one whole image (<= 256 pixels) x BN
-  // channels, and whose epilogue runs the following depthwise 3x3 on it
-  constexpr bool kPD = MODE == static_cast<int>(ConvLoadMode::kPwDw) ||
-                      MODE == static_cast<int>(ConvLoadMode::kPairPwDw);
+  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA);
   // kIm2col: R x S / strided convs whose A blocks are TMA im2col loads (one per
   // (tap, 64-channel block)); otherwise the TMA-A machinery
   constexpr bool kI2C = MODE == static_cast<int>(ConvLoadMode::kIm2col);
-  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kPD || kI2C;
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kI2C;
   // residual adds are compiled into the 1x1 modes only (the runtime routes
   // every residual conv there); the other modes carry none of that state
-  constexpr bool kRes = kTmaA && !kPD;
+  constexpr bool kRes = kTmaA;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128 B swizzle atoms must sit on 1 KiB boundaries.
   // (offsetting smem_raw, rather than masking the generic address, keeps the
@@ -826,7 +539,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (threadIdx.x == 0) ts_mark(args.ts, 4);
   constexpr long long ts0 = 0;
   const int epi_warps = 4 * args.teams;
-  constexpr bool kDw = MODE == static_cast<int>(ConvLoadMode::kDwFused);
   // kWindowT: kWindow with the transposed (C % 64 != 0) halo boxes, its own
   // instantiation so the default in-place mode carries none of that code
   constexpr bool kWinT = MODE == static_cast<int>(ConvLoadMode::kWindowT);
@@ -836,16 +548,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // instantiation keeps the single-box stem kernel's registers lean
   constexpr bool kS2W = MODE == static_cast<int>(ConvLoadMode::kS2DWide);
   constexpr bool kS2 = MODE == static_cast<int>(ConvLoadMode::kS2D) || kS2W;
-  constexpr bool kBlk = kDw || kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
+  constexpr bool kBlk = kWin || kS2;  // 2-D pixel-block tiles, 4-D TMA-store epilogue
   // (kWindow's A operands live in the halo boxes: its ring stages carry B only)
   // (kS2D ring stages are sized for two sub-tiles: a halo box of a 64-row
   // block is still under 32 KiB)
   const SmemLayout L = smem_layout(kPair ? args.BN / 2 : args.BN, args.stages, args.Cout, epi_warps, args.b_res,
                                    kWin ? 1 : kS2 ? 2 : args.mt,
-                                   kDw ? static_cast<int>(args.dw_box_bytes) : 0,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0);
   const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
-  const uint32_t box_stride = (args.dw_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
   const uint32_t a_stage = static_cast<uint32_t>(kS2 ? 2 : mt) * kABytes;
   // kS2D: per 16-channel block one halo box, 1 KiB apart in the stage
@@ -858,11 +568,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* tmem_full = empty + args.stages;  // [n_acc]
   uint64_t* tmem_empty = tmem_full + kMaxAcc;  // [n_acc]
   uint64_t* b_full = tmem_empty + kMaxAcc;    // resident B landed (b_res)
-  uint64_t* box_full = b_full + 1;            // [stages] kDwFused halo box landed
   // kWindow barriers [8]: transposing mode raw_full[2] raw_free[2] cm_full[2]
   // cm_empty[2]; direct mode (128 B-swizzled box read in place) slot_full[4]
   // slot_free[4]
-  uint64_t* raw_full = box_full + args.stages;  // [2] kWindow: pixel-major box landed
+  uint64_t* raw_full = b_full + 1;              // [2] kWindow: pixel-major box landed
   uint64_t* raw_free = raw_full + 2;            // [2] ... transposed (gather warps)
   uint64_t* cm_full = raw_free + 2;             // [2] chunk-major box ready
   uint64_t* cm_empty = cm_full + 2;             // [2] all taps of its K block consumed
@@ -876,7 +585,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
-  const int tile_rows = kPD ? args.Ho * args.Wo : kConvBM * mt;
+  const int tile_rows = kConvBM * mt;
   // kDwFused: M blocks are TH x TW pixel blocks of one image
   const int dw_blocks_per_img = args.dw_tiles_y * args.dw_tiles_x;
   const int m_blocks = kBlk ? (args.M / (args.Ho * args.Wo)) * dw_blocks_per_img
@@ -888,7 +597,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int cl = args.cluster > 1 ? args.cluster : 1;
   const int walk_first = blockIdx.x / cl, walk_stride = gridDim.x / cl;
   const int walk_count = cl == 1 ? tiles : n_tiles * ((m_blocks + cl - 1) / cl);
-  const uint16_t cl_mask = static_cast<uint16_t>((1u << cl) - 1u);
   const int n_acc = args.n_acc;  // power of two
   const int acc_log2 = __ffs(n_acc) - 1;
   const uint32_t acc_stride = args.tmem_cols / n_acc;
@@ -904,8 +612,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
         // (cluster multicast: both CTAs' MMAs consume a B slot; pairs: the
         // leader's commit arrives in both CTAs once)
-        ptx::mbar_init(&empty[s], kPair ? 1 : cl);
-        ptx::mbar_init(&box_full[s], 1);
+        ptx::mbar_init(&empty[s], 1);
       }
       ptx::mbar_init(b_full, 1);
       for (int b = 0; b < 2; ++b) {
@@ -917,8 +624,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
         // one arrival per warp of the owning teams (pairs: of both CTAs' teams)
-        ptx::mbar_init(&tmem_empty[b], (kPD ? 8 : 4 * (args.teams > n_acc ? args.teams / n_acc : 1)) *
-                                           (kPair ? 2 : 1));
+        ptx::mbar_init(&tmem_empty[b], 4 * (args.teams > n_acc ? args.teams / n_acc : 1) * (kPair ? 2 : 1));
       }
       if (kRes && args.res_tma)
         for (int b = 0; b < 2 * epi_warps; ++b) ptx::mbar_init(&res_bar[b], 1);
@@ -959,26 +665,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // critical path of the first tile's loads and MMAs.
     for (int i = threadIdx.x; i < cout_pad; i += epi_warps * 32)
       bias_s[i] = i < args.Cout ? __ldg(args.bias + i) : 0.0f;
-    if constexpr (kPD) {  // zero the halo buffers once: their borders are the padding
-      for (int i = threadIdx.x; i < 2 * kPdHaloBytes / 16; i += epi_warps * 32)
-        ptx::sts128(ptx::smem_u32(smem + L.y_off) + i * 16, make_uint4(0, 0, 0, 0));
-      // depthwise weights [9][Cout] and bias [Cout] after the layout
-      const uint32_t dwp = ptx::smem_u32(smem + L.total);
-      for (int i = threadIdx.x; i < 9 * args.Cout / 8; i += epi_warps * 32)
-        ptx::sts128(dwp + i * 16, __ldg(reinterpret_cast<const uint4*>(args.dw_w) + i));
-      for (int i = threadIdx.x; i < args.Cout / 4; i += epi_warps * 32) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(args.dw_b) + i);
-        ptx::sts128(dwp + 9 * args.Cout * 2 + i * 16,
-                    make_uint4(__float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z),
-                               __float_as_uint(b.w)));
-      }
-    }
     asm volatile("bar.sync 1, %0;" ::"r"(epi_warps * 32) : "memory");
-    if constexpr (kPD) {
-      pwdw_epilogue(args, smem + L.y_off, ptx::smem_u32(smem + L.total), bias_s, tmem_base, acc_stride,
-                    tmem_full, tmem_empty, n_acc,
-                    acc_log2, n_tiles, warp, lane);
-    } else {
     const int quarter = warp & 3;
     // teams per accumulator: with more teams than accumulators, tpa teams
     // share each tile, team t taking column part t % tpa
@@ -1145,7 +832,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (args.ts && quarter == 0 && lane == 0 && j < 8) ts_mark(args.ts, 32 + j, ts0);
     }
     if (lane == 0) ptx::bulk_wait<0>();
-    }  // (not kPD)
   } else if (warp < kGatherWarp0) {
     // (with a single epilogue team, warps 4-7 have no role)
   } else if (warp < kGatherWarp0 + kGatherWarps) {
@@ -1201,34 +887,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
       }
-    } else if constexpr (kDw) {
-      const int tid = threadIdx.x - kGatherWarp0 * 32;
-      const DwItems di = dw_items(args, tid, args.dw_stride);
-      RingPos rp;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
-          const uint32_t s = rp.slot;
-          if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
-          ptx::mbar_wait(&box_full[s], rp.lap & 1);
-          const uint4* box = reinterpret_cast<const uint4*>(smem + L.box_off + s * box_stride);
-          const uint32_t a_st = ptx::smem_u32(smem + L.a_off) + s * a_stage;
-          if (args.dw_stride == 1)
-            dw_box_to_a<1>(args, box, a_st, kb, tid, di);
-          else
-            dw_box_to_a<2>(args, box, a_st, kb, tid, di);
-          ptx::fence_proxy_async_smem();  // generic smem writes -> tensor-core reads
-          ptx::mbar_arrive(&full[s]);
-        }
-      }
     } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
         const int m0 = tw.mb * kConvBM;
-        if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather16))
-          gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
-        else if constexpr (MODE == static_cast<int>(ConvLoadMode::kGather8))
-          gather_a_tile<4>(args, smem + L.a_off, full, empty, m0, rp);
+        gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
       }
     }
   } else if (warp == kTmaWarp && kS2) {
@@ -1238,7 +902,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int kb = 0; kb < args.num_kb; ++kb)
         ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
                          kb * kConvBK, 0);
-      const int taps = args.R * args.S;
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
@@ -1246,7 +909,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int blk = tw.mb - img * dw_blocks_per_img;
         const int by = SmallDiv(args.dw_tiles_x).div(blk);
         const int bx = blk - by * args.dw_tiles_x;
-        if (args.win_iw > 0) {  // one halo box per block holds every tap's window
+        {  // one halo box per block holds every tap's window
           const uint32_t s = rp.slot;
           if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
           // one box per 16-channel block (C = 16 or 32), origin shifted by the
@@ -1262,23 +925,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 "r"(bx * args.dw_tw - args.pad_w), "r"(by * args.dw_th - args.pad_h), "r"(img)
                 : "memory");
           rp.next(args.stages);
-          continue;
-        }
-        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
-          const uint32_t s = rp.slot;
-          if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
-          const int nt = min(4, taps - kb * 4);  // taps of this K block (16 channels each)
-          ptx::mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nt) * args.win_box_bytes);
-          for (int tl = 0; tl < nt; ++tl) {
-            const int t = kb * 4 + tl, dr = t / args.S, dc = t - (t / args.S) * args.S;
-            asm volatile(
-                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
-                    ptx::smem_u32(smem + L.a_off + s * a_stage + tl * args.win_box_bytes)),
-                "l"(&args.tmap_a), "r"(ptx::smem_u32(&full[s])), "r"(0),
-                "r"(bx * args.dw_tw + dc), "r"(by * args.dw_th + dr), "r"(img)
-                : "memory");
-          }
         }
       }
     }
@@ -1336,7 +982,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
                            kb * kConvBK, 0);
       }
-      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0) + (kDw ? 1u : 0u);
+      const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0);
       uint32_t j = 0;
       RingPos rp;
       TileWalk tw(n_tiles, cl);
@@ -1354,22 +1000,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
           if (args.ts && kb == 0 && j < 8) ts_mark(args.ts, 40 + j, ts0);
-          if constexpr (kDw) {  // the K block's halo box
-            const int img = SmallDiv(dw_blocks_per_img).div(tw.mb);
-            const int blk = tw.mb - img * dw_blocks_per_img;
-            const int by = SmallDiv(args.dw_tiles_x).div(blk);
-            const int bx = blk - by * args.dw_tiles_x;
-            ptx::mbar_arrive_expect_tx(&box_full[s], args.dw_box_bytes);
-            asm volatile(
-                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
-                    ptx::smem_u32(smem + L.box_off + s * box_stride)),
-                "l"(&args.tmap_a), "r"(ptx::smem_u32(&box_full[s])), "r"(kb * args.dw_cb),
-                "r"(bx * args.dw_tw * args.dw_stride - 1), "r"(by * args.dw_th * args.dw_stride - 1),
-                "r"(img)
-                : "memory");
-            if (b_res) continue;
-          }
           if constexpr (kPair) {
             // both CTAs' bytes count on the leader's full barrier
             if (tw.rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * tx);
@@ -1380,13 +1010,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                     &full[s], kb * kConvBK, m0 + q * kConvBM);
             continue;
           }
-          ptx::mbar_arrive_expect_tx(&full[s], tx - (kDw ? 1u : 0u));
-          if (!b_res && cl > 1) {  // this CTA's half of the B block, to both CTAs
-            const uint32_t half = b_bytes / cl;
-            ptx::tma_load_2d_mc(ptx::smem_u32(smem + L.b_off + s * b_bytes + tw.rank * half),
-                                &args.tmap_b, &full[s], kb * kConvBK,
-                                n0 + tw.rank * (args.BN / cl), cl_mask);
-          } else if (!b_res) {
+          ptx::mbar_arrive_expect_tx(&full[s], tx);
+          if (!b_res) {
             ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                              kb * kConvBK, n0);
           }
@@ -1431,8 +1056,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
-        if (args.win_iw > 0) {  // windows of the block's halo box: tap (dr, dc) starts at
-                                // pixel (16 q + dr) * IW + dc, pixel rows sbo = IW * 32 B apart
+        {  // windows of the block's halo box: tap (dr, dc) starts at
+           // pixel (16 q + dr) * IW + dc, pixel rows sbo = IW * 32 B apart
           const uint32_t s = rp.slot;
           ptx::mbar_wait(&full[s], rp.lap & 1);
           ptx::tc_fence_after();
@@ -1464,7 +1089,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                       k != 0);
                 }
           };
-          const bool fast = (mt == 2 || mt == 4) && !(args.debug_flags & 16);
+          const bool fast = mt == 2 || mt == 4;
           using I1 = std::integral_constant<int, 1>;
           using I2 = std::integral_constant<int, 2>;
           using I3 = std::integral_constant<int, 3>;
@@ -1488,7 +1113,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
           }
           const int ncb = kS2W ? args.C >> 4 : 1;
-          for (int t = 0, dr = 0, dc = 0; t < (done ? 0 : taps) && !(args.debug_flags & 16);
+          for (int t = 0, dr = 0, dc = 0; t < (done ? 0 : taps);
                ++t, dc = dc + 1 == args.S ? 0 : dc + 1, dr = dc == 0 ? dr + 1 : dr) {
             for (int cb = 0; cb < ncb; ++cb) {
               const int k = t * ncb + cb;
@@ -1505,23 +1130,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           ptx::umma_commit_warp(&empty[s]);
           rp.next(args.stages);
           ptx::umma_commit_warp(&tmem_full[acc]);
-          continue;
         }
-        for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
-          const uint32_t s = rp.slot;
-          ptx::mbar_wait(&full[s], rp.lap & 1);
-          ptx::tc_fence_after();
-          const uint64_t db = ptx::umma_desc_sw128_kmajor(ptx::smem_u32(smem + L.b_off + kb * b_bytes));
-          const int nt = min(4, taps - kb * 4);
-          for (int tl = 0; tl < nt && !(args.debug_flags & 16); ++tl)  // (flag 16: bring-up)
-            for (int q = 0; q < mt; ++q) {
-              const uint64_t da = ptx::umma_desc_sw32_kmajor(ptx::smem_u32(
-                  smem + L.a_off + s * a_stage + tl * args.win_box_bytes + q * kConvBM * 32));
-              ptx::umma_bf16_warp(d + q * args.BN, da, db + 2 * tl, idesc, (kb | tl) != 0);
-            }
-          ptx::umma_commit_warp(&empty[s]);
-        }
-        ptx::umma_commit_warp(&tmem_full[acc]);
       }
     }
     __syncwarp();
@@ -1535,26 +1144,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t lbo = npix * 16, sbo = static_cast<uint32_t>(args.win_iw) * 16;
       uint32_t j = 0, u = 0;
       RingPos rp;
-      unsigned long long t_acc = 0, t_box = 0, t_all = clock64();  // (flag 32: probe)
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
         const uint32_t acc = j & (n_acc - 1);
-        unsigned long long t0 = clock64();
         if (j >= static_cast<uint32_t>(n_acc))
           ptx::mbar_wait(&tmem_empty[acc], ((j >> acc_log2) - 1) & 1);
-        t_acc += clock64() - t0;
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * acc_stride;
         bool first = true;
         for (int kb = 0; kb < win_cblocks; ++kb, ++u) {
           const bool direct = win_direct;
           const uint32_t b = direct ? u & 3 : u & 1;
-          t0 = clock64();
           if (direct) {
             ptx::mbar_wait(&slot_full[b], (u >> 2) & 1);
           } else {
             ptx::mbar_wait(&cm_full[b], (u >> 1) & 1);
           }
-          t_box += clock64() - t0;
           ptx::tc_fence_after();
           const uint32_t cm =
               ptx::smem_u32(smem + L.win_off + (direct ? b : 2 + b) * win_stride);
@@ -1629,9 +1233,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         ptx::umma_commit_warp(&tmem_full[acc]);
       }
-      if ((args.debug_flags & 32) && blockIdx.x < 2 && lane == 0)
-        printf("kWindow MMA cta %d: tiles %u, cycles %llu, waiting box %llu, waiting acc %llu\n",
-               blockIdx.x, j, clock64() - t_all, t_box, t_acc);
     }
     __syncwarp();
   } else {  // kMmaWarp: MMA issuer (whole warp: uniform descriptors, elected issue)
@@ -1672,8 +1273,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // the K block's four K=16 steps (+32 B in the swizzle row each), per sub-tile
           if constexpr (kPair) {
             ptx::umma_bf16_pair_k64(d, da, db, idesc, kb != 0);
-            if (mt == 2)  // (kPairPwDw: both CTAs' second image sub-tile)
-              ptx::umma_bf16_pair_k64(d + args.BN, da + (kABytes >> 4), db, idesc, kb != 0);
             ptx::umma_commit_pair_warp(&empty[s], 3);  // both CTAs' slots
             continue;
           }
@@ -1685,10 +1284,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               ptx::umma_bf16_warp_k64(d + q * args.BN, da + static_cast<uint64_t>(q) * (kABytes >> 4),
                                       db, idesc, kb != 0);
           }
-          if (cl > 1)
-            ptx::umma_commit_mc_warp(&empty[s], cl_mask);  // both CTAs read this B slot
-          else
-            ptx::umma_commit_warp(&empty[s]);
+          ptx::umma_commit_warp(&empty[s]);
         }
         if constexpr (kPair)
           ptx::umma_commit_pair_warp(&tmem_full[acc], 3);
@@ -1896,49 +1492,6 @@ size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_r
   return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt).total + 1024;  // + alignment slack
 }
 
-bool conv_gemm_pwdw_ok(int ho, int wo, int cout, int bn, int dw_stride) {
-  // whole image per tile (<= 2 sub-tiles, halo <= 16 x 16), 64-channel
-  // rounds, two accumulators for the two epilogue teams
-  const int acc_cols = static_cast<int>(pow2_at_least(((ho * wo + kConvBM - 1) / kConvBM) * bn));
-  const int wd = (wo - 1) / dw_stride + 1;  // depthwise output width: strips of kPdQ
-  return ho * wo <= 2 * kConvBM && (ho + 2) * (wo + 2) * 128 <= kPdHaloBytes && bn % 64 == 0 &&
-         wd % kPdQ == 0 &&
-         bn <= 256 && cout % bn == 0 && 512 / acc_cols >= 2 && (dw_stride == 1 || dw_stride == 2);
-}
-
-bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
-                       int& box_bytes) {
-  if (c < 32 || (c & (c - 1)) != 0 || (stride != 1 && stride != 2)) return false;
-  cb = std::min(c, 64);
-  th = tw = 0;
-  if (stride == 1) {
-    if (wo % 16 == 0) {
-      th = 8, tw = 16;
-    } else if (wo % 14 == 0) {
-      tw = 14, th = 8;
-    }
-  } else {
-    if (wo % 8 == 0) {
-      th = 8, tw = 8;
-    } else if (wo % 14 == 0) {
-      th = 4, tw = 14;
-    }
-  }
-  if (th == 0) return false;
-  const int rw = 32 / tw;  // pixel rows per epilogue warp (TMA store box)
-  if (th % rw != 0 || th / rw > 4) return false;
-  const int iw = (tw - 1) * stride + 3, ih = (th - 1) * stride + 3;
-  box_bytes = iw * ih * cb * 2;
-  // a ring of >= 2 stages of A + box (+ B per stage when it cannot stay resident)
-  const int bn = cout <= 256 ? (cout + 15) / 16 * 16 : 256;
-  const int n_tiles = (cout + bn - 1) / bn;
-  const int kpad = (c + 63) / 64 * 64;
-  const bool b_res = n_tiles == 1 && (kpad / 64) * bn * 128 <= 64 * 1024;
-  const int per_stage = kABytes + (box_bytes + 1023) / 1024 * 1024 + (b_res ? 0 : bn * 128);
-  const int fixed = (b_res ? (kpad / 64) * bn * 128 : 0) + 8 * 2 * 4096 + 8 * 1024;  // + staging
-  return (227 * 1024 - fixed) / per_stage >= 2;
-}
-
 // kWindow ring sizing (shared by the launcher and conv_gemm_window_ok).
 bool window_rings(int R, int S, int C, int cout, int BN, int box_bytes, int& b_res, int& teams,
                   int& stages) {
@@ -1947,7 +1500,7 @@ bool window_rings(int R, int S, int C, int cout, int BN, int box_bytes, int& b_r
   const int res_bytes = cblocks * taps * BN * 128;
   const int n_tiles = (cout + BN - 1) / BN;
   auto fits = [&](int res_blocks, int tm, int st) {
-    const int total = static_cast<int>(smem_layout(BN, st, cout, 4 * tm, res_blocks, 1, 0, box_bytes).total);
+    const int total = static_cast<int>(smem_layout(BN, st, cout, 4 * tm, res_blocks, 1, box_bytes).total);
     (void)win;
     return total + 1024 <= 227 * 1024;
   };
@@ -1989,44 +1542,11 @@ cudaError_t conv_gemm_init() {
   // once, outside any stream capture.
   static cudaError_t status = [] {
     const int cap = 227 * 1024;
-    cudaError_t e = cudaFuncSetAttribute(conv_gemm_kernel<0>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_gemm_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               cap);
+    cudaError_t e = cudaSuccess;
+    for (auto* k : {conv_gemm_kernel<0>, conv_gemm_kernel<2>, conv_gemm_kernel<4>, conv_gemm_kernel<5>,
+                    conv_gemm_kernel<6>, conv_gemm_kernel<7>, conv_gemm_kernel<10>, conv_gemm_kernel<11>,
+                    conv_gemm_kernel<12>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     return e;
   }();
   return status;
@@ -2046,38 +1566,30 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
   ConvGemmArgs args = in_args;
   args.span = launch_span();
-  const bool pair = mode == ConvLoadMode::kPairTmaA || mode == ConvLoadMode::kPairPwDw;
-  const bool pd = mode == ConvLoadMode::kPwDw || mode == ConvLoadMode::kPairPwDw;
-  if (pd && !conv_gemm_pwdw_ok(args.Ho, args.Wo, args.Cout, args.BN, args.dw_stride))
-    return cudaErrorInvalidValue;
+  const bool pair = mode == ConvLoadMode::kPairTmaA;
   if (pair) {
     // CTA pairs: each CTA's B half is BN / 2 rows of 128 B swizzle atoms
-    // (kPairPwDw: each CTA of the pair takes its own image)
     if (args.BN % 16 != 0 || args.BN > 256) return cudaErrorInvalidValue;
     args.cluster = 2;
+  } else {
+    args.cluster = 1;
   }
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
   // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
   // one ring stage, one accumulator (mt x BN columns) and one trip through
   // the barriers, amortising the per-tile MMA-issue / barrier latency that
-  // bounds small-N layers. DS_CONV_MT=1 forces single sub-tiles (A/B).
-  auto env_int = [](const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::max(1, std::min(4, std::atoi(e))) : dflt;
-  };
-  const int mt_stem = env_int("DS_CONV_MT", 4), mt_tma = env_int("DS_CONV_MT_TMA", 2),
-                   teams_tma = env_int("DS_CONV_TEAMS_TMA", 4);
+  // bounds small-N layers.
+  const int mt_stem = 4, mt_tma = 2, teams_tma = 4;
   const int mt_cap = mode == ConvLoadMode::kWindow ? std::max(1, in_args.mt)
                      : (mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide)
-                         ? (in_args.win_iw > 0 ? std::max(2, in_args.dw_th / 16) : 2)
+                         ? std::max(2, in_args.dw_th / 16)
                      : mode == ConvLoadMode::kStemU8 ? mt_stem
                      : (mode == ConvLoadMode::kTmaA || mode == ConvLoadMode::kIm2col) ? mt_tma
                                                    : 1;
   args.mt = 1;
   while (args.mt * 2 <= mt_cap && args.mt * 2 * static_cast<int>(pow2_at_least(args.BN)) <= 256)
     args.mt *= 2;
-  if (pd) args.mt = (args.Ho * args.Wo + kConvBM - 1) / kConvBM;  // one image per tile
   // TMEM: as many accumulators as 512 columns hold (2..kMaxAcc), so the MMA
   // runs ahead of the epilogue; epilogue teams: 2, or 4 when the gather warps
   // are idle (TMA-A) and tiles are single small ones, never more than the
@@ -2089,14 +1601,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.teams = std::min((tmaa || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
   if (args.teams == 3) args.teams = 2;  // a power of two
-  if (pd) args.teams = 4;  // sixteen epilogue warps = two teams of eight (pwdw_epilogue)
   // wide TMA-A tiles with two accumulators: the idle gather warps join and
   // two teams split each tile's columns (DS_CONV_TPA=0: off)
-  const int res_prefetch = [] {  // bring-up A/B: 0 none, 1 this tile, 2 a tile ahead
-    const char* e = std::getenv("DS_RES_PREFETCH");
-    return e ? std::atoi(e) : 1;
-  }();
-  args.res_prefetch = res_prefetch;
+  args.res_prefetch = 1;  // (epilogue L2 prefetch of this tile's residual rows)
   const bool tpa_on = [] {
     const char* e = std::getenv("DS_CONV_TPA");
     return !(e && e[0] == '0');
@@ -2111,8 +1618,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   {
     const char* e = std::getenv("DS_Y_NARROW");
     const bool on = !(e && e[0] == '0');
-    const bool blk_mode = mode == ConvLoadMode::kDwFused || mode == ConvLoadMode::kWindow ||
-                          mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide || pd;
+    const bool blk_mode = mode == ConvLoadMode::kWindow || mode == ConvLoadMode::kS2D ||
+                          mode == ConvLoadMode::kS2DWide;
     if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8 &&
         encode_tmap_out_narrow(&args.tmap_y, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
                                static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
@@ -2134,39 +1641,18 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   // B resident in smem when the layer has one N tile and a small K: no
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
-  const bool b_res_on = [] {
-    const char* e = std::getenv("DS_B_RESIDENT");
-    return !(e && e[0] == '0');
-  }();
-  args.b_res = b_res_on && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
-  if (args.cluster > 1) args.b_res = 0;  // (multicast B streams through the ring)
-  const int bres = args.b_res;
-  args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, bres, args.mt);
-  const bool dw = mode == ConvLoadMode::kDwFused;
-  const int box = dw ? static_cast<int>(args.dw_box_bytes) : 0;
-  if (dw) {
-    // the ring carries A, the halo box (and B unless resident); the epilogue
-    // stores each warp's pixel rows through the 4-D output map
-    if (!args.y_tma) return cudaErrorInvalidValue;
-    const int per_stage = kABytes + (box + 1023) / 1024 * 1024 + (bres > 0 ? 0 : args.BN * 128);
-    const int fixed =
-        static_cast<int>(smem_layout(args.BN, 0, args.Cout, 4 * args.teams, bres, 1, box).total) +
-        64 * 8 + 1024;
-    args.stages = std::min(4, (227 * 1024 - fixed) / per_stage);
-    if (args.stages < 2) return cudaErrorInvalidValue;
-  }
+  args.b_res = !pair && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
+  args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, args.b_res, args.mt);
   if (mode == ConvLoadMode::kStemU8) {
     // one private slot per producer group (stem_slot); drop to one epilogue
     // team if that is what makes the slots fit
     const int groups = kGatherWarps / args.mt;
     if (args.stages < groups) {
       args.teams = 1;
-      args.stages = conv_gemm_stages(args.BN, args.Cout, 4, bres, args.mt);
+      args.stages = conv_gemm_stages(args.BN, args.Cout, 4, args.b_res, args.mt);
     }
     if (args.stages < groups) return cudaErrorInvalidValue;
     args.stages = groups;
-  }
-  if (mode == ConvLoadMode::kStemU8) {
     if (args.taps > 64 || args.R > 15 || args.S > 15) return cudaErrorInvalidValue;
     for (int t = 0; t < 64; ++t) {
       const int r = t < args.taps ? t / args.S : 0, c = t < args.taps ? t % args.S : 0;
@@ -2175,9 +1661,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   }
   const bool s2 = mode == ConvLoadMode::kS2D || mode == ConvLoadMode::kS2DWide;
   if (s2) {
-    // pixel blocks of dw_th x 8 (halo box) or 16 x 16 (tap boxes) = dw_th / 16
-    // 128-row sub-tiles; all weights resident
-    args.mt = args.win_iw > 0 ? args.dw_th / 16 : 2;
+    // pixel blocks of dw_th x 8 (one halo box each) = dw_th / 16 128-row
+    // sub-tiles; all weights resident
+    args.mt = args.dw_th / 16;
     if (args.mt != 2 && args.mt != 4) return cudaErrorInvalidValue;
     if (!args.y_tma || n_tiles != 1 || args.num_kb * args.BN * 128 > 64 * 1024)
       return cudaErrorInvalidValue;
@@ -2202,79 +1688,45 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
                       args.b_res, args.teams, args.stages))
       return cudaErrorInvalidValue;
   }
-  const int bres2 = args.b_res;
-  // kPwDw: the depthwise weights and bias sit after the layout
-  const size_t pd_extra = pd ? static_cast<size_t>(args.Cout) * (9 * 2 + 4) : 0;
-  if (pd) {
-    const int bn_s = pair ? args.BN / 2 : args.BN;  // B rows staged per CTA
-    const int per_stage = args.mt * kABytes + (bres > 0 ? 0 : bn_s * kConvBK * 2);
-    const int fixed = static_cast<int>(smem_layout(bn_s, 0, args.Cout, 16, bres, args.mt).total +
-                                       pd_extra) + 64 * 8 + 1024;
-    args.stages = std::min(kConvMaxStages, (227 * 1024 - fixed) / per_stage);
-    if (args.stages < 2) return cudaErrorInvalidValue;
-  }
   const size_t smem =
-      dw ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres, 1, box).total + 1024
-      : win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, bres2, 1, 0,
-                          static_cast<int>(args.win_box_bytes)).total + 1024
-            : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
-                                   bres, s2 ? 2 : args.mt) +
-              pd_extra;
-  const bool blk = dw || win || s2;
-  const int tiles =
-      blk  ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
-      : pd ? n_tiles * (args.M / (args.Ho * args.Wo))
-           : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
+      win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, args.b_res, 1,
+                        static_cast<int>(args.win_box_bytes)).total + 1024
+          : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
+                                 args.b_res, s2 ? 2 : args.mt);
+  const int tiles = win || s2 ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
+                              : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
   const int per_sm = std::max(1, std::min(by_smem, by_tmem));
-  if (args.cluster > 1) {  // pairs of CTAs over (M-block pair, N block) units
-    if ((mode != ConvLoadMode::kTmaA && !pair) || args.b_res > 0 || args.cluster != 2 ||
-        (pair && !pd && args.mt != 1))
-      return cudaErrorInvalidValue;
-    const int m_blocks = pd ? args.M / (args.Ho * args.Wo)  // (images)
-                            : (args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt);
+  if (pair) {  // CTA pairs over (M-block pair, N block) units
+    if (args.mt != 1) return cudaErrorInvalidValue;
+    const int m_blocks = (args.M + kConvBM - 1) / kConvBM;
     const int units = n_tiles * ((m_blocks + 1) / 2);
     const int ctas = std::min(2 * units, conv_gemm_sm_count() * per_sm) / 2 * 2;
-    return launch_pdl_cluster(mode == ConvLoadMode::kPairPwDw ? conv_gemm_kernel<9>
-                              : pair                          ? conv_gemm_kernel<7>
-                                                              : conv_gemm_kernel<2>,
-                              dim3(ctas), dim3(kConvThreads), smem, stream, 2, args);
+    return launch_pdl_cluster(conv_gemm_kernel<7>, dim3(ctas), dim3(kConvThreads), smem, stream, 2, args);
   }
-  args.cluster = 1;
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
   switch (mode) {
     case ConvLoadMode::kGather16:
       return launch_pdl(conv_gemm_kernel<0>, grid, dim3(kConvThreads), smem, stream, args);
-    case ConvLoadMode::kGather8:
-      return launch_pdl(conv_gemm_kernel<1>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kTmaA:
       return launch_pdl(conv_gemm_kernel<2>, grid, dim3(kConvThreads), smem, stream, args);
-    case ConvLoadMode::kDwFused:
-      return launch_pdl(conv_gemm_kernel<3>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kStemU8:
       return launch_pdl(conv_gemm_kernel<4>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kWindow:
       if (!args.win_direct)
         return launch_pdl(conv_gemm_kernel<11>, grid, dim3(kConvThreads), smem, stream, args);
       return launch_pdl(conv_gemm_kernel<5>, grid, dim3(kConvThreads), smem, stream, args);
-    case ConvLoadMode::kWindowT:
-      return cudaErrorInvalidValue;  // (selected through kWindow + win_direct = 0)
     case ConvLoadMode::kS2D:
       return launch_pdl(conv_gemm_kernel<6>, grid, dim3(kConvThreads), smem, stream, args);
     case ConvLoadMode::kS2DWide:
       return launch_pdl(conv_gemm_kernel<10>, grid, dim3(kConvThreads), smem, stream, args);
-    case ConvLoadMode::kPairTmaA:
-      break;  // (launched above)
-    case ConvLoadMode::kPwDw:
-      return launch_pdl(conv_gemm_kernel<8>, grid, dim3(kConvThreads), smem, stream, args);
-    case ConvLoadMode::kPairPwDw:
-      break;  // (launched above)
     case ConvLoadMode::kIm2col:
       return launch_pdl(conv_gemm_kernel<12>, grid, dim3(kConvThreads), smem, stream, args);
+    default:
+      return cudaErrorInvalidValue;  // (kWindowT is selected through kWindow + win_direct = 0)
   }
-  return cudaGetLastError();
 }
 
 }  // namespace ds

@@ -46,8 +46,8 @@ struct ConvGemmArgs {
   int teams, n_acc;
   int b_res;  // > 0: all num_kb weight blocks resident in smem (one N tile)
   int mt;     // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
-  int cluster;  // kTmaA: 2 = CTA pairs share (multicast) every weight block; tmap_b box
-                // rows are then BN / 2 (each CTA loads one half for both)
+  int cluster;  // 2 = CTA pairs (kPairTmaA; launch_conv_gemm sets it): tmap_b box rows
+                // are then BN / 2 (each CTA loads its half of every weight block)
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;
@@ -60,19 +60,13 @@ struct ConvGemmArgs {
   // relative to kernel entry, see conv_gemm.cu ts_mark(); nullptr in the runtime
   unsigned long long* ts;
   unsigned long long* span;  // live per-kernel timing slot (pdl.cuh span_mark), or nullptr
-  // kDwFused: A[m, c] = relu(dw3x3(x)[m, c] + dw_b[c]), computed in the
-  // producer from the depthwise input x ([H][W][C], pad 1, stride dw_stride);
-  // Ho/Wo are the depthwise output dims, R = S = 1. Tiles are dw_th x dw_tw
-  // pixel blocks of one image; tmap_a is the 4-D halo-box map over x
-  // (box {dw_cb, dw_iw, (dw_th-1)*stride+3, 1}), see conv_gemm_dw_plan.
-  const __nv_bfloat16* dw_w;  // [9][C] bf16
-  const float* dw_b;          // [C]
-  int dw_stride;
-  int dw_th, dw_tw, dw_cb, dw_iw, dw_tiles_y, dw_tiles_x;
-  int dw_rw;  // pixel rows per epilogue warp: TMEM lane l of warp q <-> pixel (q*rw + l/tw, l%tw)
-  uint32_t dw_box_bytes;
+  // Pixel-block tiles (kWindow, kS2D, kS2DWide): dw_th x dw_tw output pixels
+  // of one image, dw_tiles_y x dw_tiles_x blocks per image; epilogue warp q
+  // stores pixel rows q*dw_rw .. (TMEM lane l <-> pixel (q*rw + l/tw, l%tw)).
+  int dw_th, dw_tw, dw_tiles_y, dw_tiles_x;
+  int dw_rw;
   // kWindow (stride-1 R x S conv, no im2col): tiles are 16 x 8 output-pixel
-  // blocks (dw_th/dw_tw/dw_rw/dw_tiles_* as above); per 64-channel K block
+  // blocks; per 64-channel K block
   // the TMA lands the halo box {min(64, C), win_iw, win_ih} (pixel-major), the
   // gather warps transpose it to chunk-major (16 B channel chunks x pixels),
   // and every tap (r, s) is one MMA operand read straight out of that box
@@ -92,18 +86,13 @@ struct ConvGemmArgs {
 
 enum class ConvLoadMode : int {
   kGather16 = 0,  // cp.async gather, 8 channels (16 B) per granule, C % 8 == 0
-  kGather8 = 1,   // cp.async gather, 4 channels (8 B) per granule, C == 4 (stem)
   kTmaA = 2,      // 1x1 stride-1 conv: A is a plain 2D tile, loaded by TMA
-  kDwFused = 3,   // depthwise 3x3 + bias + ReLU computed into A, then the 1x1 GEMM
   kStemU8 = 4,    // stem conv over the u8 images, input staging fused into the producer
   kWindow = 5,    // stride-1 R x S conv as shifted-window MMAs over a per-K-block halo box
-  kS2D = 6,       // stride-2 stem over its space-to-depth input: per tap one TMA box, no
-                  // producer warps (A arrives in the MMA's 32 B-swizzled layout)
+  kS2D = 6,       // stride-2 stem over its space-to-depth input: one 32 B-swizzled halo box
+                  // per pixel block, every tap an MMA window of it; no producer warps
   kPairTmaA = 7,  // kTmaA on CTA pairs: one M = 256 cta_group::2 MMA per K step, each CTA
                   // loading its 128 A rows and half of the B block (tmap_b box rows BN / 2)
-  kPwDw = 8,      // 1x1 conv + the following depthwise 3x3 (dw_w / dw_b / dw_stride): a
-                  // tile is one image x BN channels; y / ldy are the depthwise output
-  kPairPwDw = 9,  // kPwDw on CTA pairs (two images per pair MMA, B halves as kPairTmaA)
   kS2DWide = 10,  // kS2D window MMAs for 16 / 32-channel stride-1 3x3 convs (one halo box
                   // per 16-channel block, padding as negative box coordinates)
   kWindowT = 11,  // (internal) kWindow with transposed boxes: launch as kWindow, win_direct 0
@@ -115,10 +104,6 @@ enum class ConvLoadMode : int {
 // 64-channel x 128-output-pixel blocks, 128 B swizzle.
 bool encode_tmap_im2col(CUtensorMap* map, const void* base, int n, int h, int w, int c, int r, int s,
                         int stride_h, int stride_w, int pad_h, int pad_w);
-
-// Whether a 1x1 conv (ho x wo output, cout channels, N tile bn) and its
-// depthwise successor can run as one kPwDw launch.
-bool conv_gemm_pwdw_ok(int ho, int wo, int cout, int bn, int dw_stride);
 
 // Encodes a 2D bf16 tensor map [rows][cols] (cols contiguous, row stride in
 // elements) with a {64, box_rows} box and 128 B swizzle.
@@ -157,12 +142,6 @@ bool conv_gemm_stem_fits(int R, int S, int cout);
 int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0, int mt = 1);
 uint32_t conv_gemm_tmem_cols(int BN);
 
-// Tile plan of a depthwise-fused 1x1 conv (kDwFused): output block th x tw
-// (<= 128 pixels, tw even), channel block cb per K block, halo box bytes;
-// false when the layer is not fused (the runtime runs the two kernels).
-bool conv_gemm_dw_plan(int ho, int wo, int c, int stride, int cout, int& th, int& tw, int& cb,
-                       int& box_bytes);
-
 // Whether a conv runs as kWindow: stride 1, R*S > 1, C % 16 == 0, and the
 // operand rings fit in shared memory next to the epilogue staging.
 bool conv_gemm_window_ok(int r, int s, int c, int cout);
@@ -174,7 +153,7 @@ bool encode_tmap_nhwc_sw32(CUtensorMap* map, const void* base, int n, int h, int
 
 // 4-D output map {C, W, H, N} over an NHWC activation (channel slice at
 // `base`, row stride ld channels) with a {64, box_w, box_h, 1} box and 128 B
-// swizzle: the kDwFused epilogue stores each warp's pixel rows with it.
+// swizzle: the pixel-block epilogues store each warp's pixel rows with it.
 bool encode_tmap_out4d(CUtensorMap* map, void* base, int n, int h, int w, int cols, int ld,
                        int box_w, int box_h);
 

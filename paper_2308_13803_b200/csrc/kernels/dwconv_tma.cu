@@ -243,131 +243,6 @@ __global__ void __launch_bounds__(kDwMaxThreads) dw_tma_kernel(
   }
 }
 
-// The same walk with 4-channel groups (8 B per vector, half the registers per
-// thread: acc[Q][4], w[9] as bf16 pairs), for the 14 x 14 maps where the
-// 8-channel kernel's ~100 registers held occupancy at two CTAs per SM.
-// Per output the same fma order, so results are bit-identical.
-template <int S, int Q>
-__global__ void __launch_bounds__(kDwMaxThreads) dw_tma4_kernel(
-    const __grid_constant__ CUtensorMap in_map, const __grid_constant__ DwKernelArgs a) {
-  constexpr int XN = (Q - 1) * S + 3;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * a.box_bytes);
-  const int glog2 = a.glog2 + 1;  // 4-channel groups per box pixel
-  const int groups = 1 << glog2;
-  const int cb = groups * 4;
-  auto coords = [&](int t, int& cbk, int& tx, int& ty, int& tn) {
-    cbk = static_cast<int>(a.div_sp.div(static_cast<uint32_t>(t)));
-    int r = t - cbk * static_cast<int>(a.div_sp.d);
-    const int q = static_cast<int>(a.div_tx.div(static_cast<uint32_t>(r)));
-    tx = r - q * a.tiles_x;
-    tn = static_cast<int>(a.div_ty.div(static_cast<uint32_t>(q)));
-    ty = q - tn * a.tiles_y;
-  };
-  auto issue = [&](int t, int stage) {
-    int cbk, tx, ty, tn;
-    coords(t, cbk, tx, ty, tn);
-    ptx::mbar_arrive_expect_tx(&full[stage], a.box_bytes);
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(smem + stage * a.box_bytes)),
-        "l"(&in_map), "r"(ptx::smem_u32(&full[stage])), "r"(cbk * cb), "r"(tx * a.tw * S - 1),
-        "r"(ty * a.th * S - 1), "r"(tn * a.nb)
-        : "memory");
-  };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < a.stages; ++s) ptx::mbar_init(&full[s], 1);
-    ptx::fence_barrier_init();
-    ptx::tma_prefetch_desc(&in_map);
-  }
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();
-  span_mark(a.span);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < a.stages; ++s) {
-      const int t = blockIdx.x + s * gridDim.x;
-      if (t < a.tiles) issue(t, s);
-    }
-  }
-  const int cg_all = a.c >> 2;  // 4-channel groups of the tensor
-  const int spr = a.tw / Q;
-  const int items = (spr * a.th * a.nb) << glog2;
-  const bool active = static_cast<int>(threadIdx.x) < items;
-  const int g = threadIdx.x & (groups - 1);
-  int sx, oyl, nbl;
-  {
-    int strip = threadIdx.x >> glog2;
-    sx = strip % spr;
-    strip /= spr;
-    oyl = strip % a.th;
-    nbl = strip / a.th;
-  }
-  const uint2* my_box = reinterpret_cast<const uint2*>(smem) +
-                        (((nbl * a.ih + oyl * S) * a.iw + sx * Q * S) << glog2) + g;
-  const int box_vecs = static_cast<int>(a.box_bytes >> 3);
-  uint2 w[9];
-  float bias[4];
-  int cur_cbk = -1;
-  uint32_t j = 0;
-  int stage = 0;
-  uint32_t phase = 0;  // (ring position advanced without divisions)
-  for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++j) {
-    int cbk, tx, ty, tn;
-    coords(t, cbk, tx, ty, tn);
-    const int oy = ty * a.th + oyl;
-    const int img = tn * a.nb + nbl;
-    const int gg = cbk * groups + g;
-    if (cbk != cur_cbk) {
-      cur_cbk = cbk;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) w[k] = __ldg(reinterpret_cast<const uint2*>(a.w) + k * cg_all + gg);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias) + gg);
-      bias[0] = b.x; bias[1] = b.y; bias[2] = b.z; bias[3] = b.w;
-    }
-    ptx::mbar_wait(&full[stage], phase);
-    if (active && oy < a.ho && img < a.n) {
-      float acc[Q][4];
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[q][e] = bias[e];
-      const uint2* box = my_box + stage * box_vecs;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const uint2* row = box + ((r * a.iw) << glog2);
-        uint2 xv[XN];
-#pragma unroll
-        for (int u = 0; u < XN; ++u) xv[u] = row[u << glog2];
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-          for (int s = 0; s < 3; ++s) {
-            const uint2 x = xv[q * S + s], wk = w[r * 3 + s];
-            acc[q][0] = fma_bf16_lo(x.x, wk.x, acc[q][0]);
-            acc[q][1] = fma_bf16_hi(x.x, wk.x, acc[q][1]);
-            acc[q][2] = fma_bf16_lo(x.y, wk.y, acc[q][2]);
-            acc[q][3] = fma_bf16_hi(x.y, wk.y, acc[q][3]);
-          }
-      }
-      uint2* yp = reinterpret_cast<uint2*>(a.y) +
-                  ((static_cast<long long>(img) * a.ho + oy) * a.wo + tx * a.tw + sx * Q) * cg_all + gg;
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-        yp[q * cg_all] = make_uint2(relu_pack2(acc[q][0], acc[q][1]),
-                                    relu_pack2(acc[q][2], acc[q][3]));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int nt = t + a.stages * static_cast<int>(gridDim.x);
-      if (nt < a.tiles) issue(nt, stage);
-    }
-    if (++stage == a.stages) {
-      stage = 0;
-      phase ^= 1u;
-    }
-  }
-}
 
 int sm_count() {
   static int n = [] {
@@ -379,30 +254,12 @@ int sm_count() {
   return budgeted_sms(n);
 }
 
-// (bring-up knob: DS_DW14_ROWS overrides the 14x14 tile height)
-int dw14_rows() {
-  const int r = [] {
-    const char* e = std::getenv("DS_DW14_ROWS");
-    return e ? std::max(1, std::atoi(e)) : 14;
-  }();
-  return r;
-}
-
 // Tile shape per layer (output width, stride, channels): a strip of Q outputs
 // per thread, TW | wo, and (TW/Q)*TH*NB*groups close to a multiple of 32 <= 256.
 struct DwPlan {
   int q, tw, th, nb, cb;
   bool ok;
-  bool g4 = false;  // dw_tma4_kernel (4-channel groups)
 };
-
-// DS_DW_G4=1: the 14 x 14 stride-1 layers on 4-channel groups (opt-in: twice
-// the occupancy but twice the shared-memory load instructions; measured 18.4
-// vs 16.4 us per layer at bs 128 on B200).
-bool dw_g4_on() {
-  const char* e = std::getenv("DS_DW_G4");
-  return e && e[0] == '1';
-}
 
 DwPlan dw_plan(int ho, int wo, int c, int stride) {
   const int cb = std::min(c, 64);
@@ -415,9 +272,7 @@ DwPlan dw_plan(int ho, int wo, int c, int stride) {
     if (wo % 16 == 0 && wo >= 64) set(4, 16, cb >= 64 ? 8 : 16, 1);  // 112x112
     else if (wo % 8 == 0 && wo >= 48) set(4, 8, 14, 1);              // 56x56
     else if (wo % 4 == 0 && wo >= 20) set(4, wo, 4, 1);              // 28x28
-    else if (wo % 7 == 0 && wo >= 14 && dw_g4_on() && ho % 7 == 0 && cb == 64) {  // 14x14, 4-ch groups
-      if ((wo / 7) * 7 * 16 <= kDwMaxThreads) p = DwPlan{7, wo, 7, 1, cb, true, true};
-    } else if (wo % 7 == 0 && wo >= 14) set(7, wo, std::min(ho, dw14_rows()), 1);  // 14x14
+    else if (wo % 7 == 0 && wo >= 14) set(7, wo, std::min(ho, 14), 1);  // 14x14
     else if (wo == 7) set(7, 7, 7, 4);                                // 7x7
   } else {
     if (wo % 8 == 0 && wo >= 48) set(2, 8, 8, 1);                     // 112 -> 56
@@ -450,29 +305,19 @@ DwKernelArgs make_args(const DwPlan& p, int n, int h, int w, int c, int stride) 
   a.div_ty = make_fastdiv(static_cast<uint32_t>(a.tiles_y));
   a.div_sp = make_fastdiv(static_cast<uint32_t>(a.tiles_x * a.tiles_y * a.tiles_n));
   a.box_bytes = static_cast<uint32_t>(a.iw * a.ih * p.nb * p.cb * 2);
-  // 2-4 boxes in flight, <= ~72 KB per CTA so three CTAs share an SM.
-  // (A/B knobs; garbage or out-of-range values fall back to the defaults, and
-  // the ring always fits the 200 KB dynamic shared memory set in launch_plan)
-  auto env_int = [](const char* name, int def, int lo, int hi) {
-    const char* e = std::getenv(name);
-    if (!e || !*e) return def;
-    char* end = nullptr;
-    const long v = std::strtol(e, &end, 10);
-    return (end && *end == 0 && v >= lo && v <= hi) ? static_cast<int>(v) : def;
-  };
-  const int budget = env_int("DS_DW_STAGE_KB", 72, 8, 192) * 1024;
-  const int max_st = env_int("DS_DW_MAX_STAGES", 4, 2, 8);
-  constexpr int kSmemCap = 200 * 1024;
-  int st = std::max(2, std::min(max_st, static_cast<int>(budget / a.box_bytes)));
+  // 2-4 boxes in flight, <= ~72 KB per CTA so three CTAs share an SM (the
+  // ring always fits the 200 KB dynamic shared memory set in launch_plan)
+  constexpr int kBudget = 72 * 1024, kMaxStages = 4, kSmemCap = 200 * 1024;
+  int st = std::max(2, std::min(kMaxStages, static_cast<int>(kBudget / a.box_bytes)));
   while (st > 2 && st * static_cast<int>(a.box_bytes) + 8 * st + 16 > kSmemCap) --st;
   a.stages = st;
   return a;
 }
 
-template <int S, int Q, bool G4 = false>
+template <int S, int Q>
 cudaError_t launch_plan(const CUtensorMap& map, DwKernelArgs a, const DwPlan& p,
                         cudaStream_t stream) {
-  auto kernel = G4 ? dw_tma4_kernel<S, Q> : dw_tma_kernel<S, Q>;
+  auto kernel = dw_tma_kernel<S, Q>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -480,7 +325,7 @@ cudaError_t launch_plan(const CUtensorMap& map, DwKernelArgs a, const DwPlan& p,
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int items = ((p.tw / Q) * p.th * p.nb) * (p.cb / (p.g4 ? 4 : 8));
+  const int items = ((p.tw / Q) * p.th * p.nb) * (p.cb / 8);
   const int threads = std::min(kDwMaxThreads, (items + 31) / 32 * 32);
   const size_t smem = static_cast<size_t>(a.stages) * a.box_bytes + 8 * a.stages + 16;
   int per_sm = 1;
@@ -515,7 +360,6 @@ cudaError_t launch_dwconv3x3_tma(const CUtensorMap& in_map, const __nv_bfloat16*
   a.y = reinterpret_cast<uint4*>(y);
   if (stride == 1) {
     if (p.q == 4) return launch_plan<1, 4>(in_map, a, p, stream);
-    if (p.g4) return launch_plan<1, 7, true>(in_map, a, p, stream);
     return launch_plan<1, 7>(in_map, a, p, stream);
   }
   if (p.q == 2) return launch_plan<2, 2>(in_map, a, p, stream);

@@ -38,20 +38,6 @@ inline unsigned grid_for(long long work) {
   return static_cast<unsigned>((work + kBlock - 1) / kBlock);
 }
 
-__global__ void stage_input_kernel(const uint8_t* __restrict__ img, uint2* __restrict__ out,
-                                   long long pixels, unsigned long long* span) {
-  pdl_trigger();
-  pdl_wait();
-  span_mark(span);
-  const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= pixels) return;
-  const uint8_t* s = img + 3 * p;
-  float v[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) v[c] = (static_cast<float>(s[c]) - 127.5f) / 63.75f;
-  out[p] = make_uint2(pack2(v[0], v[1]), pack2(v[2], 0.0f));
-}
-
 // Space-to-depth staging for stride-2 stems (kS2D): S[n][Y][X][16] bf16 with
 // channel (a*2 + b)*4 + c = x(2Y + a - pad, 2X + b - pad, c) normalised as
 // above (zero outside the image and for c == 3). A stride-2 R x S conv over x
@@ -93,181 +79,15 @@ __global__ void stage_s2d_kernel(const uint8_t* __restrict__ img, uint4* __restr
   out[2 * i + 1] = make_uint4(v[4], v[5], v[6], v[7]);
 }
 
-// Depthwise 3x3, register-blocked: a thread owns 8 channels (one 16 B
-// vector) x kDwCols consecutive output columns of one output row, so each
-// loaded input vector feeds up to 3 outputs from registers; consecutive
-// threads take consecutive channel groups (coalesced 16 B loads/stores along
-// C). Weights come through the read-only path (L1-resident per block).
-constexpr int kDwCols = 4;
-
-template <int STRIDE>
-__global__ void __launch_bounds__(kBlock) dwconv3x3_kernel(
-    const uint4* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-    const float* __restrict__ bias, uint4* __restrict__ y, int h, int wd, int c, int ho, int wo,
-    int cg_log2, int xq_per_row, unsigned long long* span) {
-  pdl_trigger();
-  pdl_wait();
-  span_mark(span);
-  // grid.y = output row (image * ho + oy); x covers (column quad, channel group)
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cg = 1 << cg_log2;
-  const int g = i & (cg - 1);
-  const int xq = i >> cg_log2;
-  if (xq >= xq_per_row) return;
-  const int row = blockIdx.y;
-  const int n = row / ho;
-  const int oy = row - n * ho;
-  const int ox0 = xq * kDwCols;
-  constexpr int IN_COLS = (kDwCols - 1) * STRIDE + 3;
-  const int ix0 = ox0 * STRIDE - 1;
-
-  float acc[kDwCols][8];
-  const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * g);
-  const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias) + 2 * g + 1);
-  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-  for (int q = 0; q < kDwCols; ++q)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[q][e] = bv[e];
-  const uint4* wv = reinterpret_cast<const uint4*>(w);
-  // All weight vectors, then each stencil row's input vectors, are issued
-  // before first use so several loads are in flight per thread (the loop was
-  // latency-bound on load -> use). Taps outside the image are skipped, not
-  // multiplied by zero, to keep the FMA sequence of the fused path.
-  uint4 wraw[9];
-#pragma unroll
-  for (int t = 0; t < 9; ++t) wraw[t] = __ldg(wv + t * cg + g);
-
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int iy = oy * STRIDE - 1 + r;
-    const bool row_ok = iy >= 0 && iy < h;
-    const uint4* xrow = x + (static_cast<long long>(n) * h + (row_ok ? iy : 0)) * wd * cg + g;
-    uint4 raw[IN_COLS];
-    bool ok[IN_COLS];
-#pragma unroll
-    for (int col = 0; col < IN_COLS; ++col) {
-      const int ix = ix0 + col;
-      ok[col] = row_ok && ix >= 0 && ix < wd;
-      raw[col] = ok[col] ? __ldg(xrow + static_cast<long long>(ix) * cg) : make_uint4(0, 0, 0, 0);
-    }
-    float wr[3][8];
-#pragma unroll
-    for (int s = 0; s < 3; ++s) unpack8(wraw[r * 3 + s], wr[s]);
-#pragma unroll
-    for (int col = 0; col < IN_COLS; ++col) {
-      if (!ok[col]) continue;
-      float xv[8];
-      unpack8(raw[col], xv);
-#pragma unroll
-      for (int q = 0; q < kDwCols; ++q) {
-        const int s = col - q * STRIDE;  // tap of output q that reads this column
-        if (s < 0 || s > 2) continue;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[q][e] = fmaf(xv[e], wr[s][e], acc[q][e]);
-      }
-    }
-  }
-  uint4* yrow = y + (static_cast<long long>(n) * ho + oy) * wo * cg + g;
-#pragma unroll
-  for (int q = 0; q < kDwCols; ++q) {
-    if (ox0 + q >= wo) break;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[q][e] = fmaxf(acc[q][e], 0.0f);
-    yrow[static_cast<long long>(ox0 + q) * cg] = pack8(acc[q]);
-  }
-}
-
-// One output pixel x 8 channels per thread (stride-2 layers, where a
-// column is shared by at most two outputs and blocking does not pay).
-__global__ void dwconv3x3_px_kernel(const uint4* __restrict__ x, const uint4* __restrict__ w,
-                                 const float4* __restrict__ bias, uint4* __restrict__ y, int h,
-                                 int wd, int cg, int ho, int wo, int stride, long long work, unsigned long long* span) {
-  pdl_trigger();
-  pdl_wait();
-  span_mark(span);
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= work) return;
-  const int g = static_cast<int>(i % cg);
-  long long pix = i / cg;
-  const int ox = static_cast<int>(pix % wo);
-  pix /= wo;
-  const int oy = static_cast<int>(pix % ho);
-  const int n = static_cast<int>(pix / ho);
-  float acc[8];
-  const float4 b0 = __ldg(bias + 2 * g), b1 = __ldg(bias + 2 * g + 1);
-  acc[0] = b0.x; acc[1] = b0.y; acc[2] = b0.z; acc[3] = b0.w;
-  acc[4] = b1.x; acc[5] = b1.y; acc[6] = b1.z; acc[7] = b1.w;
-  const int iy0 = oy * stride - 1, ix0 = ox * stride - 1;
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int iy = iy0 + r;
-    if (iy < 0 || iy >= h) continue;
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int ix = ix0 + s;
-      if (ix < 0 || ix >= wd) continue;
-      float xv[8], wv[8];
-      unpack8(__ldg(x + ((static_cast<long long>(n) * h + iy) * wd + ix) * cg + g), xv);
-      unpack8(__ldg(w + (r * 3 + s) * cg + g), wv);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = fmaf(xv[e], wv[e], acc[e]);
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = fmaxf(acc[e], 0.0f);
-  y[i] = pack8(acc);
-}
-
-__global__ void pool3x3_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int h, int w,
-                               int cg, int ho, int wo, int stride, int pad, int is_max, int ldo_g,
-                               int coff_g, long long work, unsigned long long* span) {
-  pdl_trigger();
-  pdl_wait();
-  span_mark(span);
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= work) return;
-  const int g = static_cast<int>(i % cg);
-  long long pix = i / cg;
-  const int ox = static_cast<int>(pix % wo);
-  pix /= wo;
-  const int oy = static_cast<int>(pix % ho);
-  const int n = static_cast<int>(pix / ho);
-  float acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = is_max ? -INFINITY : 0.0f;
-  const int iy0 = oy * stride - pad, ix0 = ox * stride - pad;
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int iy = iy0 + r;
-    if (iy < 0 || iy >= h) continue;
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int ix = ix0 + s;
-      if (ix < 0 || ix >= w) continue;
-      float xv[8];
-      unpack8(__ldg(x + ((static_cast<long long>(n) * h + iy) * w + ix) * cg + g), xv);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = is_max ? fmaxf(acc[e], xv[e]) : acc[e] + xv[e];
-    }
-  }
-  if (!is_max) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = acc[e] / 9.0f;
-  }
-  const long long opix = (static_cast<long long>(n) * ho + oy) * wo + ox;
-  y[opix * ldo_g + coff_g + g] = pack8(acc);
-}
 
 // 3x3 pooling on a 2-D grid: grid.y = output row (image, oy), x = (output
 // column, 8-channel group); 32-bit index arithmetic (the column / group split
 // through an exact float-reciprocal division). Max pooling compares the
 // packed bf16 pairs directly (max is exact in any precision); average pooling
 // accumulates with fma.rn.f32.bf16(x, 1.0, acc) == acc + float(x), one
-// instruction per element. Per output the taps are visited in the same order
-// as pool3x3_kernel (row outer, column inner, padding skipped) and averages
-// divide the fp32 sum by 9, so results are bit-identical to it
-// (DS_POOL_LEGACY=1 selects the old kernel).
+// instruction per element. Per output the taps are visited row outer, column
+// inner (padding skipped) and averages divide the fp32 sum by 9 — the
+// oracle's order, and the TMA pools' (pool_tma.cu, bit-identical).
 __device__ __forceinline__ float add_bf16_lo(uint32_t x, float c) {
   float d;
   asm("{.reg .b16 xl, xh, one;\n\t"
@@ -488,14 +308,6 @@ __global__ void softmax_kernel(const float* __restrict__ logits, float* __restri
 
 }  // namespace
 
-cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
-                               cudaStream_t stream) {
-  const long long pixels = static_cast<long long>(n) * h * w;
-  return launch_pdl(stage_input_kernel, dim3(grid_for(pixels)), dim3(kBlock), 0, stream, img,
-                    reinterpret_cast<uint2*>(out), pixels, launch_span());
-  return cudaGetLastError();
-}
-
 cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w, int hs,
                              int ws, int pad, cudaStream_t stream) {
   const long long pixels = static_cast<long long>(n) * hs * ws;
@@ -504,72 +316,25 @@ cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int 
                     reinterpret_cast<uint4*>(out), h, w, hs, ws, pad, pixels, launch_span());
 }
 
-cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
-                             __nv_bfloat16* y, int n, int h, int wd, int c, int stride,
-                             cudaStream_t stream) {
-  const int ho = (h + 2 - 3) / stride + 1, wo = (wd + 2 - 3) / stride + 1;
-  const int cg = c / 8;
-  int cg_log2 = 0;
-  while ((1 << cg_log2) < cg) ++cg_log2;
-  if ((1 << cg_log2) != cg) return cudaErrorInvalidValue;  // channel groups must be a power of 2
-  const int rows = n * ho;
-  if (rows > 65535) return cudaErrorInvalidValue;
-  auto block_for = [](int per_row) { return std::min(kBlock, (per_row + 31) / 32 * 32); };
-  if (stride == 1) {
-    const int xq = (wo + kDwCols - 1) / kDwCols;
-    const int bt = block_for(xq * cg);
-    return launch_pdl(dwconv3x3_kernel<1>, dim3((xq * cg + bt - 1) / bt, rows), dim3(bt), 0, stream,
-                      reinterpret_cast<const uint4*>(x), w, bias, reinterpret_cast<uint4*>(y), h,
-                      wd, c, ho, wo, cg_log2, xq, launch_span());
-  } else {
-    const long long pw = static_cast<long long>(n) * ho * wo * cg;
-    return launch_pdl(dwconv3x3_px_kernel, dim3(grid_for(pw)), dim3(kBlock), 0, stream,
-                      reinterpret_cast<const uint4*>(x), reinterpret_cast<const uint4*>(w),
-                      reinterpret_cast<const float4*>(bias), reinterpret_cast<uint4*>(y), h, wd,
-                      cg, ho, wo, stride, pw, launch_span());
-  }
-  return cudaGetLastError();
-}
-
 cudaError_t launch_pool3x3(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int h, int w, int c,
                            int stride, int pad, bool is_max, int ldo, int c_off,
                            cudaStream_t stream) {
+  // (the fallback of the TMA pools, pool_tma.cu, for layouts they cannot box)
   const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
   const int cg = c / 8;
-  const bool legacy = [] {
-    const char* e = std::getenv("DS_POOL_LEGACY");
-    return e && e[0] == '1';
-  }();
-  const char* rows_env = std::getenv("DS_POOL_ROWS");  // output rows per thread: 1 or 2 (A/B)
-  const int prows = rows_env ? std::atoi(rows_env) : 2;
-  const int yrows = n * ((ho + prows - 1) / prows);
-  if (!legacy && yrows <= 65535 && (stride == 1 || stride == 2) && wo * cg < (1 << 24)) {
-    const int per_row = wo * cg;
-    const int bt = std::min(kBlock, (per_row + 31) / 32 * 32);
-    const dim3 grid((per_row + bt - 1) / bt, yrows);
-    auto go = [&](auto kernel) {
-      return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
-                        reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8, launch_span());
-    };
-    if (prows == 1) {
-      if (stride == 1)
-        return is_max ? go(pool3x3_rows_kernel<1, true, 1>) : go(pool3x3_rows_kernel<1, false, 1>);
-      return is_max ? go(pool3x3_rows_kernel<2, true, 1>) : go(pool3x3_rows_kernel<2, false, 1>);
-    }
-    if (prows == 4) {
-      if (stride == 1)
-        return is_max ? go(pool3x3_rows_kernel<1, true, 4>) : go(pool3x3_rows_kernel<1, false, 4>);
-      return is_max ? go(pool3x3_rows_kernel<2, true, 4>) : go(pool3x3_rows_kernel<2, false, 4>);
-    }
-    if (stride == 1)
-      return is_max ? go(pool3x3_rows_kernel<1, true, 2>) : go(pool3x3_rows_kernel<1, false, 2>);
-    return is_max ? go(pool3x3_rows_kernel<2, true, 2>) : go(pool3x3_rows_kernel<2, false, 2>);
-  }
-  const long long work = static_cast<long long>(n) * ho * wo * cg;
-  return launch_pdl(pool3x3_kernel, dim3(grid_for(work)), dim3(kBlock), 0, stream,
-                    reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(y), h, w, cg, ho,
-                    wo, stride, pad, is_max ? 1 : 0, ldo / 8, c_off / 8, work, launch_span());
-  return cudaGetLastError();
+  constexpr int kRows = 2;  // output rows per thread
+  const int yrows = n * ((ho + kRows - 1) / kRows);
+  if (yrows > 65535 || (stride != 1 && stride != 2) || wo * cg >= (1 << 24)) return cudaErrorInvalidValue;
+  const int per_row = wo * cg;
+  const int bt = std::min(kBlock, (per_row + 31) / 32 * 32);
+  const dim3 grid((per_row + bt - 1) / bt, yrows);
+  auto go = [&](auto kernel) {
+    return launch_pdl(kernel, grid, dim3(bt), 0, stream, reinterpret_cast<const uint4*>(x),
+                      reinterpret_cast<uint4*>(y), h, w, cg, ho, wo, pad, ldo / 8, c_off / 8, launch_span());
+  };
+  if (stride == 1)
+    return is_max ? go(pool3x3_rows_kernel<1, true, kRows>) : go(pool3x3_rows_kernel<1, false, kRows>);
+  return is_max ? go(pool3x3_rows_kernel<2, true, kRows>) : go(pool3x3_rows_kernel<2, false, kRows>);
 }
 
 cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,

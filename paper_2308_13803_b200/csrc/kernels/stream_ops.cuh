@@ -10,22 +10,14 @@
 
 namespace ds {
 
-// u8 NHWC [n][h][w][3] images -> normalised bf16 NHWC [n][h][w][4] (channel 3
-// zero), x = (p - 127.5) / 63.75, the stem's 8-byte gather granule.
-cudaError_t launch_stage_input(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w,
-                               cudaStream_t stream);
-
 // Space-to-depth staging for stride-2 stems: u8 [n][h][w][3] -> bf16
-// [n][hs][ws][16], channel (a*2+b)*4+c = normalised x(2Y+a-pad, 2X+b-pad, c).
+// [n][hs][ws][16], channel (a*2+b)*4+c = normalised x(2Y+a-pad, 2X+b-pad, c),
+// x = (p - 127.5) / 63.75 (zero outside the image and for c == 3).
 cudaError_t launch_stage_s2d(const uint8_t* img, __nv_bfloat16* out, int n, int h, int w, int hs,
                              int ws, int pad, cudaStream_t stream);
 
-// Depthwise 3x3, pad 1, stride 1|2, + bias, ReLU. w: [9][C] bf16 (tap-major).
-cudaError_t launch_dwconv3x3(const __nv_bfloat16* x, const __nv_bfloat16* w, const float* bias,
-                             __nv_bfloat16* y, int n, int h, int wd, int c, int stride,
-                             cudaStream_t stream);
-
-// Depthwise 3x3 streamed by TMA halo boxes (dwconv_tma.cu); C must be a
+// Depthwise 3x3, pad 1, stride 1|2, + bias, ReLU, w: [9][C] bf16 (tap-major),
+// streamed by TMA halo boxes (dwconv_tma.cu); C must be a
 // power of two >= 8. The input map comes from dwconv_tma_input_map over the
 // (max-batch) input buffer.
 bool dwconv_tma_supported(int c);

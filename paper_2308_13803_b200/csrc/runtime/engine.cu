@@ -37,29 +37,6 @@ int choose_stages(int bn, int cout) { return conv_gemm_stages(bn, cout); }
 
 uint32_t tmem_cols_for(int bn) { return conv_gemm_tmem_cols(bn); }
 
-// DS_STEM_S2D_MODE=window: the s2d stem as a kWindow conv (one halo box per
-// 32 x 8 block, transposed by the gather warps) instead of kS2D (one TMA box
-// per tap in the MMA's layout, no producer warps; faster on B200). A/B switch.
-bool s2d_window() {
-  const bool on = [] {
-    const char* e = std::getenv("DS_STEM_S2D_MODE");
-    return e && std::string(e) == "window";
-  }();
-  return on;
-}
-
-// DS_CONV_CLUSTER=1: CTA pairs multicast the weight blocks of the 256-wide
-// TMA-A layers. Opt-in: measured no faster on B200 (L2 already merges the two
-// CTAs' near-simultaneous reads of a block; these layers are bound by shared-
-// memory traffic per MMA at 128 x 256 tiles, which 2-SM MMAs would halve).
-bool cluster_on() {
-  const bool on = [] {
-    const char* e = std::getenv("DS_CONV_CLUSTER");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 // DS_CONV_PAIR: TMA-A layers whose weights stream (not resident) run on CTA
 // pairs with M = 256 cta_group::2 MMAs, each CTA staging half of every B
 // block (a third less shared-memory traffic per MMA at 128 x 256 tiles).
@@ -70,18 +47,6 @@ bool pair_on(int bn) {
     return e ? std::atoi(e) : 1;
   }();
   return m == 1 && bn >= 128;
-}
-
-// DS_STEM_S2D_MODE=tap: the kS2D stem with one TMA box per tap instead of one
-// halo box per 32 x 8 block whose taps are MMA windows (the default: a
-// fraction of the TMA bytes, and with the taps unrolled the issue loop runs
-// at the tensor pipe's pace). A/B switch.
-bool s2d_tap_boxes() {
-  const bool on = [] {
-    const char* e = std::getenv("DS_STEM_S2D_MODE");
-    return e && std::string(e) == "tap";
-  }();
-  return on;
 }
 
 // Stride-1 R x S convs as kWindow (shifted-window MMAs, no im2col). Default:
@@ -208,21 +173,19 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
              "upload biases");
 
   plans_.resize(m.ops.size());
-  fused_ = fused_depthwise(m);
-  absorbed_ = pwdw_absorbed(m);
   stem_ = fused_stem(m);
-  kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (input or s2d staging +) softmax
+  if (stem_ < 0 && s2d_.op < 0)
+    throw std::logic_error("stem conv neither stride-2 (space-to-depth) nor a fused u8 stem");
+  kernels_per_forward_ = stem_ >= 0 ? 1 : 2;  // (s2d staging +) softmax
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
-    if (!fused_[i] && !absorbed_[i]) ++kernels_per_forward_;
-    if (op.kind == OpKind::kDwConv && !fused_[i] && !absorbed_[i]) {
+    ++kernels_per_forward_;
+    if (op.kind == OpKind::kDwConv) {
       const BufferSpec& din = m.buffers.at(op.in);
       dw_maps_.resize(m.ops.size());
-      dw_tma_.resize(m.ops.size(), false);
-      const char* legacy = std::getenv("DS_DW_LEGACY");
-      dw_tma_[i] = !(legacy && legacy[0] == '1') && dwconv_tma_plan_ok(din.h, din.w, din.c, op.sh) &&
-                   dwconv_tma_input_map(&dw_maps_[i], bufs_[op.in], max_bs, din.h, din.w, din.c,
-                                        op.sh);
+      if (!dwconv_tma_plan_ok(din.h, din.w, din.c, op.sh) ||
+          !dwconv_tma_input_map(&dw_maps_[i], bufs_[op.in], max_bs, din.h, din.w, din.c, op.sh))
+        throw CudaError("depthwise layer without a TMA plan (dwconv_tma.cu)");
     }
     if (op.kind == OpKind::kMaxPool || op.kind == OpKind::kAvgPool) {
       // TMA halo-box pooling (pool_tma.cu). A padded max pool reads its edge
@@ -282,54 +245,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.c_off = op.c_off;
     a.out_f32 = out.f32 ? 1 : 0;
     a.relu = op.relu ? 1 : 0;
-    if (i > 0 && fused_[i - 1]) {
-      // depthwise + this 1x1 conv in one launch: A is computed from the
-      // depthwise input; the depthwise output buffer is never written.
-      const OpSpec& dw = m.ops[i - 1];
-      const BufferSpec& dw_in = m.buffers.at(dw.in);
-      pl.mode = ConvLoadMode::kDwFused;
-      a.x = static_cast<const __nv_bfloat16*>(bufs_[dw.in]);
-      a.H = dw_in.h;
-      a.W = dw_in.w;
-      a.C = dw_in.c;
-      a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
-      a.dw_b = d_b_ + hp.b_off.at(dw.param);
-      a.dw_stride = dw.sh;
-      int box = 0;
-      if (!conv_gemm_dw_plan(out.h, out.w, dw_in.c, dw.sh, p.cout, a.dw_th, a.dw_tw, a.dw_cb, box))
-        throw std::logic_error("depthwise fusion without a tile plan");
-      a.dw_box_bytes = static_cast<uint32_t>(box);
-      a.dw_iw = (a.dw_tw - 1) * dw.sh + 3;
-      a.dw_rw = 32 / a.dw_tw;
-      a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
-      a.dw_tiles_x = (out.w + a.dw_tw - 1) / a.dw_tw;
-      if (!encode_tmap_nhwc(&a.tmap_a, bufs_[dw.in], max_bs, dw_in.h, dw_in.w, dw_in.c, a.dw_cb,
-                            a.dw_iw, (a.dw_th - 1) * dw.sh + 3, 1))
-        throw CudaError("cuTensorMapEncodeTiled failed (depthwise halo boxes)");
-    } else if (static_cast<int>(i) == s2d_.op && s2d_window()) {
-      // stride-2 stem as a stride-1 dr x ds window conv over the 16-channel
-      // s2d input (padding already inside it): one halo box per 32 x 8 block
-      pl.mode = ConvLoadMode::kWindow;
-      a.R = s2d_.dr;
-      a.S = s2d_.ds;
-      a.C = 16;
-      a.pad_h = a.pad_w = 0;
-      a.taps = s2d_.dr * s2d_.ds;
-      a.mt = 2;
-      a.dw_th = 16 * a.mt;
-      a.dw_tw = 8;
-      a.dw_rw = 4;
-      a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
-      a.dw_tiles_x = (out.w + 7) / 8;
-      a.win_iw = 8 + a.S - 1;
-      a.win_ih = a.dw_th + a.R - 1;
-      a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * 16 * 2);
-      if (!encode_tmap_nhwc(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, a.win_iw,
-                            a.win_ih, 1))
-        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem halo boxes)");
-    } else if (static_cast<int>(i) == s2d_.op && s2d_tap_boxes()) {
-      // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input,
-      // one 16 x 16 TMA box per tap
+    if (static_cast<int>(i) == s2d_.op) {
+      // stride-2 stem as a stride-1 dr x ds conv over the 16-channel s2d input
+      // (padding already inside it), one halo box per dw_th x 8 block: every
+      // tap is a window of it (8-pixel rows = the MMA's 8-row groups, SBO =
+      // box row pitch); 64-row blocks (four sub-tiles per tile) for the narrow
+      // stems, whose epilogue is bound by per-tile work
       pl.mode = ConvLoadMode::kS2D;
       a.R = s2d_.dr;
       a.S = s2d_.ds;
@@ -337,29 +258,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.pad_h = a.pad_w = 0;  // (the s2d buffer holds the stem's padding)
       a.taps = s2d_.dr * s2d_.ds;
       a.num_kb = s2d_.kpad / kConvBK;
-      a.dw_th = 16;
-      a.dw_tw = 16;
-      a.dw_rw = 2;
-      a.dw_tiles_y = (out.h + 15) / 16;
-      a.dw_tiles_x = (out.w + 15) / 16;
-      a.win_iw = 0;
-      a.win_box_bytes = 16 * 16 * 32;
-      if (!encode_tmap_nhwc_sw32(&a.tmap_a, d_s2d_, max_bs, s2d_.hs, s2d_.ws, 16, 16, 16))
-        throw CudaError("cuTensorMapEncodeTiled failed (s2d stem boxes)");
-    } else if (static_cast<int>(i) == s2d_.op) {
-      // the same, with one halo box per dw_th x 8 block: every tap is a window
-      // of it (8-pixel rows = the MMA's 8-row groups, SBO = box row pitch);
-      // 64-row blocks (four sub-tiles per tile) for the narrow stems, whose
-      // epilogue is bound by per-tile work (DS_S2D_ROWS=32|64 overrides)
-      pl.mode = ConvLoadMode::kS2D;
-      a.R = s2d_.dr;
-      a.S = s2d_.ds;
-      a.C = 16;
-      a.pad_h = a.pad_w = 0;  // (the s2d buffer holds the stem's padding)
-      a.taps = s2d_.dr * s2d_.ds;
-      a.num_kb = s2d_.kpad / kConvBK;
-      const char* rows_env = std::getenv("DS_S2D_ROWS");
-      a.dw_th = rows_env ? (std::atoi(rows_env) == 64 ? 64 : 32) : (p.cout <= 32 ? 64 : 32);
+      a.dw_th = p.cout <= 32 ? 64 : 32;
       a.dw_tw = 8;
       a.dw_rw = 4;
       a.dw_tiles_y = (out.h + a.dw_th - 1) / a.dw_th;
@@ -372,8 +271,6 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
         throw CudaError("cuTensorMapEncodeTiled failed (s2d stem halo boxes)");
     } else if (static_cast<int>(i) == stem_) {
       pl.mode = ConvLoadMode::kStemU8;  // a.img is bound per launch (input slot)
-    } else if (in.c == 4) {
-      pl.mode = ConvLoadMode::kGather8;
     } else if (in.c % 8 != 0) {
       throw std::logic_error("conv input channels must be a multiple of 8");
     } else if (narrow_window_on() && op.kind == OpKind::kConv && op.sh == 1 && op.sw == 1 &&
@@ -427,30 +324,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     } else {
       pl.mode = ConvLoadMode::kGather16;
     }
-    if (pl.mode == ConvLoadMode::kTmaA && i + 1 < m.ops.size() && absorbed_[i + 1]) {
-      // 1x1 conv + the following depthwise in one launch: a tile is one image
-      // x BN channels; the depthwise output is this launch's output
-      const OpSpec& dw = m.ops[i + 1];
-      const BufferSpec& dw_out = m.buffers.at(dw.out);
-      pl.mode = ConvLoadMode::kPwDw;
-      a.BN = pwdw_bn(p.cout);
-      a.dw_w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off.at(dw.param));
-      a.dw_b = d_b_ + hp.b_off.at(dw.param);
-      a.dw_stride = dw.sh;
-      a.y = bufs_[dw.out];
-      a.ldy = dw_out.c;
-      a.c_off = 0;
-    }
     if (op.residual >= 0 && pl.mode != ConvLoadMode::kTmaA)
       throw std::logic_error("residual adds are supported on 1x1 stride-1 convs only");
-    // wide TMA-A layers: CTA pairs may multicast each weight block (opt-in)
+    // streamed-weight TMA-A layers run on CTA pairs
     const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
-    a.cluster = pl.mode == ConvLoadMode::kTmaA && a.BN == 256 && !b_resident && cluster_on() ? 2 : 1;
-    if (pl.mode == ConvLoadMode::kPwDw && pair_on(a.BN)) {
-      pl.mode = ConvLoadMode::kPairPwDw;  // two images per pair MMA, B halves
-      a.cluster = 2;
-    }
-    if (pl.mode == ConvLoadMode::kTmaA && a.cluster == 1 && !b_resident && pair_on(a.BN)) {
+    a.cluster = 1;
+    if (pl.mode == ConvLoadMode::kTmaA && !b_resident && pair_on(a.BN)) {
       pl.mode = ConvLoadMode::kPairTmaA;
       a.cluster = 2;  // (tmap_b boxes of BN / 2 rows: each CTA's half)
     }
@@ -461,8 +340,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                                     a.BN / a.cluster)) {
       throw CudaError("cuTensorMapEncodeTiled failed (weights)");
     }
-    if (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA ||
-        pl.mode == ConvLoadMode::kPwDw || pl.mode == ConvLoadMode::kPairPwDw) {
+    if (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA) {
       const uint64_t rows = static_cast<uint64_t>(max_bs) * a.H * a.W;
       if (!encode_tmap_2d_bf16(&a.tmap_a, bufs_[op.in], rows, in.c, in.c, kConvBM))
         throw CudaError("cuTensorMapEncodeTiled failed (activations)");
@@ -473,10 +351,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       const size_t esz = out.f32 ? 4 : 2;
       void* base = static_cast<uint8_t*>(bufs_[op.out]) + static_cast<size_t>(op.c_off) * esz;
-      if (pl.mode == ConvLoadMode::kPwDw || pl.mode == ConvLoadMode::kPairPwDw)  // (direct stores)
-        a.y_tma = 0;
-      else if (pl.mode == ConvLoadMode::kDwFused || pl.mode == ConvLoadMode::kWindow ||
-          pl.mode == ConvLoadMode::kS2D || pl.mode == ConvLoadMode::kS2DWide)  // pixel-row boxes
+      if (pl.mode == ConvLoadMode::kWindow || pl.mode == ConvLoadMode::kS2D ||
+          pl.mode == ConvLoadMode::kS2DWide)  // pixel-row boxes
         a.y_tma = !out.f32 && encode_tmap_out4d(&a.tmap_y, base, max_bs, pl.ho, pl.wo, p.cout, out.c,
                                                 a.dw_tw, a.dw_rw)
                       ? 1
@@ -553,14 +429,8 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
                                 s2d_.pad, cur_stream_),
                "stage_s2d");
     record_mark();
-  } else if (stem_ < 0) {
-    check_cuda(launch_stage_input(d_images_[slot], static_cast<__nv_bfloat16*>(bufs_[0]), bs,
-                                  m.in_h, m.in_w, cur_stream_),
-               "stage_input");
-    record_mark();
   }
   for (size_t i = 0; i < m.ops.size(); ++i) {
-    if (fused_[i] || absorbed_[i]) continue;  // computed inside a neighbouring conv
     const OpSpec& op = m.ops[i];
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out = m.buffers[op.out];
@@ -573,22 +443,13 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
         ConvGemmArgs a = plans_[i].args;
         a.M = bs * plans_[i].ho * plans_[i].wo;
         if (static_cast<int>(i) == stem_) a.img = d_images_[slot];
-        if (const char* dbg = std::getenv("DS_CONV_DEBUG")) {  // bring-up: "op:flags"
-          int op_i = -1, flags = 0;
-          if (std::sscanf(dbg, "%d:%d", &op_i, &flags) == 2 && op_i == static_cast<int>(i))
-            a.debug_flags = flags;
-        }
         e = launch_conv_gemm(a, plans_[i].mode, cur_stream_);
         break;
       }
       case OpKind::kDwConv: {
         const auto* w = reinterpret_cast<const __nv_bfloat16*>(d_w_ + hp.w_off[op.param]);
-        if (i < dw_tma_.size() && dw_tma_[i])
-          e = launch_dwconv3x3_tma(dw_maps_[i], w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w,
-                                   in.c, op.sh, cur_stream_);
-        else
-          e = launch_dwconv3x3(x, w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c, op.sh,
-                               cur_stream_);
+        e = launch_dwconv3x3_tma(dw_maps_[i], w, d_b_ + hp.b_off[op.param], y, bs, in.h, in.w, in.c,
+                                 op.sh, cur_stream_);
         break;
       }
       case OpKind::kMaxPool:

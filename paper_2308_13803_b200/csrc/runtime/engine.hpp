@@ -107,14 +107,11 @@ class Instance {
   float* d_probs_ = nullptr;
   std::vector<void*> bufs_;
   std::vector<ConvPlan> plans_;  // indexed by op (conv/fc only)
-  std::vector<bool> fused_;      // depthwise ops folded into the next conv
-  std::vector<bool> absorbed_;   // depthwise ops computed in the previous conv's epilogue (kPwDw)
-  int stem_ = -1;                // stem conv reading the u8 images (kStemU8), or -1
+  int stem_ = -1;                // stride-1 stem conv reading the u8 images (kStemU8), or -1
   S2dPlan s2d_;                  // stride-2 stem over the space-to-depth input (kS2D)
   __nv_bfloat16* d_s2d_ = nullptr;     // [max_bs][hs][ws][16]
   __nv_bfloat16* d_stem_w_ = nullptr;  // stem weights re-laid for the s2d taps [cout][kpad]
   std::vector<CUtensorMap> dw_maps_;  // TMA halo maps of depthwise inputs (by op)
-  std::vector<bool> dw_tma_;          // depthwise op uses the TMA kernel
   std::vector<CUtensorMap> pool_maps_;  // TMA halo maps of pool inputs (by op)
   std::vector<bool> pool_tma_;          // pool op uses the TMA kernel (DS_POOL_TMA=0: off)
   std::map<int64_t, cudaGraphExec_t> graphs_;

@@ -314,65 +314,6 @@ ModelSpec inception_v3() {
 
 }  // namespace
 
-std::vector<bool> fused_depthwise(const ModelSpec& m) {
-  std::vector<bool> fused(m.ops.size(), false);
-  // Opt-in (DS_DW_FUSION=1): bit-exact, but on B200 the fused producer
-  // (depthwise FHFMA + halo boxes sharing the SM's shared-memory bandwidth with
-  // the GEMM) is still slower than the two tuned kernels back to back.
-  const char* on = std::getenv("DS_DW_FUSION");
-  if (!on || on[0] != '1') return fused;
-  for (size_t i = 0; i + 1 < m.ops.size(); ++i) {
-    const OpSpec& dw = m.ops[i];
-    const OpSpec& pw = m.ops[i + 1];
-    if (dw.kind != OpKind::kDwConv || pw.kind != OpKind::kConv || pw.in != dw.out) continue;
-    if (pw.r != 1 || pw.s != 1 || pw.sh != 1 || pw.sw != 1 || pw.ph != 0 || pw.pw != 0) continue;
-    bool other_reader = false;
-    for (size_t j = 0; j < m.ops.size(); ++j)
-      if (j != i + 1 && (m.ops[j].in == dw.out || m.ops[j].residual == dw.out)) other_reader = true;
-    const BufferSpec& out = m.buffers[dw.out];
-    int th, tw, cb, box;
-    if (!other_reader && conv_gemm_dw_plan(out.h, out.w, out.c, dw.sh, m.params[pw.param].cout, th,
-                                           tw, cb, box))
-      fused[i] = true;
-  }
-  return fused;
-}
-
-int pwdw_bn(int cout) { return cout % 128 == 0 ? 128 : 64; }
-
-std::vector<bool> pwdw_absorbed(const ModelSpec& m) {
-  std::vector<bool> absorbed(m.ops.size(), false);
-  // Opt-in (DS_PWDW=1): bit-exact, but on B200 about break-even with the two
-  // launches — one image per tile wastes 23 % of the 14 x 14 maps' MMA rows
-  // (196 of 256), and the depthwise phase's shared-memory traffic slows the
-  // MMA side, which is already shared-memory-bound at N = 128.
-  const char* e = std::getenv("DS_PWDW");
-  if (!e || e[0] != '1') return absorbed;
-  const std::vector<bool> fused = fused_depthwise(m);
-  for (size_t i = 1; i < m.ops.size(); ++i) {
-    const OpSpec& pw = m.ops[i - 1];
-    const OpSpec& dw = m.ops[i];
-    if (dw.kind != OpKind::kDwConv || pw.kind != OpKind::kConv || dw.in != pw.out || fused[i]) continue;
-    if (i >= 2 && fused[i - 2]) continue;  // (the 1x1 already consumes a fused depthwise)
-    if (pw.r != 1 || pw.s != 1 || pw.sh != 1 || pw.sw != 1 || pw.ph != 0 || pw.pw != 0 ||
-        pw.residual >= 0 || pw.c_off != 0 || !pw.relu || !dw.relu || dw.ph != 1 || dw.sh != dw.sw)
-      continue;
-    const BufferSpec& mid = m.buffers[pw.out];
-    const BufferSpec& in = m.buffers[pw.in];
-    if (mid.f32 || in.c % 8 != 0 || m.buffers[dw.out].c != mid.c) continue;
-    bool other_reader = false;
-    for (size_t j = 0; j < m.ops.size(); ++j)
-      if (j != i && (m.ops[j].in == pw.out || m.ops[j].residual == pw.out)) other_reader = true;
-    const int cout = m.params[pw.param].cout;
-    // (maps of at most 128 pixels waste most of the 128-row MMA tile: the two
-    // launches are faster there)
-    if (!other_reader && cout == mid.c && cout % 64 == 0 && mid.h * mid.w > 128 &&
-        conv_gemm_pwdw_ok(mid.h, mid.w, cout, pwdw_bn(cout), dw.sh))
-      absorbed[i] = true;
-  }
-  return absorbed;
-}
-
 namespace {
 // The op that reads the staged input (buffer 0), when it is a conv and its only reader.
 int stem_op(const ModelSpec& m) {
@@ -389,9 +330,6 @@ int stem_op(const ModelSpec& m) {
 
 S2dPlan stem_s2d(const ModelSpec& m) {
   S2dPlan p;
-  const char* e = std::getenv("DS_STEM_S2D");
-  const char* staged = std::getenv("DS_STEM_STAGED");
-  if ((e && e[0] == '0') || (staged && staged[0] == '1')) return p;
   const int stem = stem_op(m);
   if (stem < 0) return p;
   const OpSpec& op = m.ops[stem];
@@ -410,8 +348,6 @@ S2dPlan stem_s2d(const ModelSpec& m) {
 }
 
 int fused_stem(const ModelSpec& m) {
-  const char* staged = std::getenv("DS_STEM_STAGED");  // A/B switch for the parity test
-  if (staged && staged[0] == '1') return -1;
   if (stem_s2d(m).op >= 0) return -1;  // the space-to-depth stem wins where it applies
   int stem = -1;
   for (size_t i = 0; i < m.ops.size(); ++i) {
@@ -430,17 +366,12 @@ int fused_stem(const ModelSpec& m) {
 }
 
 std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
-  const std::vector<bool> fused = fused_depthwise(m);
-  const std::vector<bool> absorbed = pwdw_absorbed(m);
   const int stem = fused_stem(m);
   const S2dPlan s2d = stem_s2d(m);
   std::vector<KernelCost> out;
   const double px = static_cast<double>(m.in_h) * m.in_w;
   const double s2d_bytes = static_cast<double>(s2d.hs) * s2d.ws * 32;
-  if (s2d.op >= 0)
-    out.push_back({KernelKind::kStage, 0.0, px * 3 + s2d_bytes, 0.0});
-  else if (stem < 0)
-    out.push_back({KernelKind::kStage, 0.0, px * 3 + px * 4 * 2, 0.0});
+  if (s2d.op >= 0) out.push_back({KernelKind::kStage, 0.0, px * 3 + s2d_bytes, 0.0});
   for (const auto& op : m.ops) {
     const BufferSpec& in = m.buffers[op.in];
     const BufferSpec& out_b = m.buffers[op.out];
@@ -454,8 +385,8 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         const double out_elems = hw_out * p.cout;
         k.kind = KernelKind::kConvGemm;
         k.flops_per_image = 2.0 * out_elems * p.r * p.s * p.cin;
-        // the fused stem reads the u8 image (3 B per pixel) instead of the
-        // staged bf16 tensor
+        // the fused stem reads the u8 image (3 B per pixel); the s2d stem its
+        // space-to-depth tensor
         const int oi = static_cast<int>(&op - m.ops.data());
         const double in_bytes = oi == stem ? px * 3 : oi == s2d.op ? s2d_bytes : in_elems * 2;
         k.bytes_per_image = in_bytes + out_elems * (out_b.f32 ? 4 : 2) +
@@ -479,25 +410,6 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         k.kind = KernelKind::kGap;
         k.bytes_per_image = in_elems * 2 + in.c * 2.0;
         break;
-    }
-    const size_t i = &op - m.ops.data();
-    if (i > 0 && fused[i - 1]) {
-      // one launch: the depthwise input replaces the 1x1 input; both weights
-      const KernelCost dw = out.back();
-      out.pop_back();
-      const BufferSpec& dw_in = m.buffers[m.ops[i - 1].in];
-      k.flops_per_image += dw.flops_per_image;
-      k.bytes_per_image += static_cast<double>(dw_in.h) * dw_in.w * dw_in.c * 2 - in_elems * 2;
-      k.fixed_bytes += dw.fixed_bytes;
-    }
-    if (absorbed[i]) {
-      // one launch with the 1x1 before it: its output stays in shared memory
-      const KernelCost pw = out.back();
-      out.pop_back();
-      k.kind = KernelKind::kConvGemm;
-      k.flops_per_image += pw.flops_per_image;
-      k.bytes_per_image += pw.bytes_per_image - 2.0 * in_elems * 2;
-      k.fixed_bytes += pw.fixed_bytes;
     }
     out.push_back(k);
   }

@@ -67,29 +67,15 @@ struct KernelCost {
 };
 std::vector<KernelCost> kernel_costs(const ModelSpec& m);
 
-// Depthwise ops folded into the A producer of the 1x1 conv that consumes
-// them (conv_gemm kDwFused): true for op i when op i is a depthwise conv whose
-// output feeds only op i+1, a 1x1 stride-1 conv. Opt-in (DS_DW_FUSION=1):
-// correct (parity-tested) but its producer is still latency-bound.
-std::vector<bool> fused_depthwise(const ModelSpec& m);
-
-// Depthwise ops computed in the epilogue of the 1x1 conv before them (conv_gemm
-// kPwDw: one whole image x 128 or 64 channels per tile, the 1x1 output kept in
-// shared memory): true for op i when op i is a depthwise 3x3 whose input is
-// the output of op i-1, a 1x1 stride-1 conv read by nothing else, on maps of
-// at most 14 x 14 and more than 128 pixels. Opt-in: DS_PWDW=1. pwdw_bn: the conv's N tile.
-std::vector<bool> pwdw_absorbed(const ModelSpec& m);
-int pwdw_bn(int cout);
-
 // Index of the stem conv when it reads the u8 images directly (ConvLoadMode
-// kStemU8: staging fused into its producer), -1 when the staged bf16 input is
-// used (DS_STEM_STAGED=1, or buffer 0 has another reader).
+// kStemU8: staging fused into its producer), -1 when it is not a stride-1
+// conv that alone reads buffer 0 (or a stride-2 stem runs on the s2d input).
 int fused_stem(const ModelSpec& m);
 
 // Stride-2 stem over a space-to-depth input (ConvLoadMode kS2D): a staging
 // kernel writes S[n][hs][ws][16] (2 x 2 pixel blocks of the normalised image)
 // and the stem becomes a stride-1 dr x ds conv over it. Returns the stem op
-// index (and the geometry) or -1 (DS_STEM_S2D=0, or not a stride-2 stem).
+// index (and the geometry) or -1 (not a stride-2 stem).
 struct S2dPlan {
   int op = -1;
   int hs = 0, ws = 0, dr = 0, ds = 0, pad = 0, kpad = 0;

@@ -57,25 +57,19 @@ def test_device_free_entry_points():
         model_info("vgg16")
 
 
-def test_fusion_switches_change_the_launch_plan(monkeypatch):
-    """Host-side launch planning under the fusion switches (read per call, as
-    the backend reads them per plan): DS_PWDW=1 folds the six 14x14 depthwise
-    layers into their 1x1 convs (FLOPs unchanged, the 1x1 outputs no longer
-    cross HBM); DS_DW_FUSION=1 folds depthwise layers into the next 1x1."""
-    base = kernel_costs("mobilenet_v1")
-    monkeypatch.setenv("DS_PWDW", "1")
-    pwdw = kernel_costs("mobilenet_v1")
-    monkeypatch.delenv("DS_PWDW")
-    assert len(base) - len(pwdw) == 6
-    flops = lambda ks: sum(k["flops_per_image"] for k in ks)
-    nbytes = lambda ks: sum(k["bytes_per_image"] for k in ks)
-    assert abs(flops(base) - flops(pwdw)) < 1
-    # five 14x14x512 and one 14x14x512 (stride-2 consumer) 1x1 outputs, written and read once each
-    assert abs((nbytes(base) - nbytes(pwdw)) - 6 * 2 * 14 * 14 * 512 * 2) < 1
-    assert [k["kind"] for k in pwdw].count("dwconv") == [k["kind"] for k in base].count("dwconv") - 6
-    monkeypatch.setenv("DS_DW_FUSION", "1")
-    dwf = kernel_costs("mobilenet_v1")
-    assert len(dwf) < len(base) and abs(flops(dwf) - flops(base)) < 1
+def test_launch_plan_one_kernel_per_layer():
+    """Host-side launch plan: the space-to-depth staging kernel (stride-2
+    stems; the stride-1 synthetic stem reads the u8 images itself), one kernel
+    per layer, softmax; the kernel count and algorithmic FLOPs match the model."""
+    from paper_2308_13803_b200 import model_info
+    for model, staging in (("synthetic_cnn", 0), ("mobilenet_v1", 1), ("resnet50_v1", 1),
+                           ("inception_v3", 1)):
+        ks = kernel_costs(model)
+        assert [k["kind"] for k in ks].count("stage") == staging, model
+        assert ks[-1]["kind"] == "softmax"
+        assert abs(sum(k["flops_per_image"] for k in ks) - 2 * model_info(model).macs_per_image) < 1
+    kinds = [k["kind"] for k in kernel_costs("mobilenet_v1")]
+    assert kinds.count("dwconv") == 13 and kinds.count("conv_gemm") == 15
 
 
 def test_device_calls_fail_loudly_without_gpu():

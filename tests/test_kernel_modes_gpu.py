@@ -29,41 +29,6 @@ def test_forward_deterministic_and_batch_invariant():
     assert np.array_equal(a, one)
 
 
-@pytest.mark.parametrize("bs", [1, 4, 7])
-def test_depthwise_fusion_matches_unfused(monkeypatch, bs):
-    """The kDwFused conv (depthwise computed from TMA halo boxes in the 1x1
-    conv's producer, TH x TW pixel-block tiles, direct-store epilogue) and the
-    two-kernel path round the depthwise output to bf16 at the same point with
-    the same FMA order, so their logits agree bit for bit."""
-    imgs = generate_images("mobilenet_v1", 7, bs)
-    monkeypatch.setenv("DS_DW_FUSION", "1")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        fused = be.forward(imgs)
-        k_fused = be.stats()["kernels_per_forward"]
-    monkeypatch.setenv("DS_DW_FUSION", "0")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        plain = be.forward(imgs)
-        k_plain = be.stats()["kernels_per_forward"]
-    assert np.array_equal(plain, fused)
-    assert k_fused < k_plain
-
-
-@pytest.mark.parametrize("bs", [1, 3, 5])
-def test_depthwise_tma_matches_register_kernels(monkeypatch, bs):
-    """The TMA-streamed depthwise kernel (FHFMA.BF16 on packed halves, strips
-    of Q outputs, NB-image boxes on the 7x7 tail) and the register-blocked
-    unpack-then-fmaf kernels accumulate the same products in the same order,
-    so logits agree bit for bit, including batches that leave NB boxes ragged."""
-    imgs = generate_images("mobilenet_v1", 11, bs)
-    monkeypatch.setenv("DS_DW_FUSION", "0")  # standalone depthwise kernels on every layer
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        tma = be.forward(imgs)
-    monkeypatch.setenv("DS_DW_LEGACY", "1")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        legacy = be.forward(imgs)
-    assert np.array_equal(tma, legacy)
-
-
 @pytest.mark.parametrize("model,bs", [("resnet50_v1", 3), ("inception_v3", 2)])
 def test_window_conv_matches_im2col_gather(monkeypatch, model, bs, oracle_mod):
     """kWindow on every eligible conv (stride-1 R x S convs as shifted-window
@@ -83,74 +48,6 @@ def test_window_conv_matches_im2col_gather(monkeypatch, model, bs, oracle_mod):
     ref = oracle_mod.forward(model, imgs, bf16_storage=True)
     assert row_rel_err(win, ref).max() <= REL_TOL
     assert row_rel_err(gather, ref).max() <= REL_TOL
-
-
-@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 5), ("resnet50_v1", 3)])
-def test_cluster_multicast_matches_single_cta(monkeypatch, model, bs):
-    """CTA pairs sharing multicast weight blocks (DS_CONV_CLUSTER=1: each CTA
-    loads half of every B block for both, empty slots need both MMAs'
-    commits) compute exactly the single-CTA tiles: bit-identical logits."""
-    imgs = generate_images(model, 13, bs)
-    monkeypatch.setenv("DS_CONV_CLUSTER", "1")
-    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
-        pair = be.forward(imgs)
-    monkeypatch.setenv("DS_CONV_CLUSTER", "0")
-    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
-        single = be.forward(imgs)
-    assert np.array_equal(pair, single)
-
-
-@pytest.mark.parametrize("model", ["synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"])
-def test_fused_stem_matches_staged_input(monkeypatch, model):
-    """The stem conv reading u8 images directly (kStemU8: the staging
-    normalisation through a table of the exact staged bf16 values) against
-    the staging kernel + bf16-input stem: identical A operands, so identical
-    logits; one launch fewer per forward."""
-    imgs = generate_images(model, 3, 3)
-    monkeypatch.setenv("DS_STEM_S2D", "0")  # (the space-to-depth stem has its own test)
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        fused = be.forward(imgs)
-        k_fused = be.stats()["kernels_per_forward"]
-    monkeypatch.setenv("DS_STEM_STAGED", "1")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        staged = be.forward(imgs)
-        k_staged = be.stats()["kernels_per_forward"]
-    assert np.array_equal(fused, staged)
-    assert k_staged == k_fused + 1
-
-
-@pytest.mark.parametrize("mode", ["box", "tap", "window"])
-@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2), ("inception_v3", 2)])
-def test_s2d_stem_matches_staged_input(monkeypatch, model, bs, mode):
-    """Stride-2 stems over the space-to-depth input (kS2D: per-tap TMA boxes in
-    the MMA's 32 B-swizzled layout, 16 x 16 pixel blocks) against the staged
-    bf16 input + im2col gather: identical products, K summed in another
-    order, so logits agree to fp32-accumulation rounding."""
-    imgs = generate_images(model, 9, bs)
-    monkeypatch.setenv("DS_STEM_S2D_MODE", mode)  # kS2D halo box | kS2D tap boxes | kWindow
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        s2d = be.forward(imgs)
-    monkeypatch.setenv("DS_STEM_STAGED", "1")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        staged = be.forward(imgs)
-    assert np.isfinite(s2d).all()
-    assert row_rel_err(s2d, staged).max() <= REL_TOL
-
-
-@pytest.mark.parametrize("model,bs", [("mobilenet_v1", 3), ("resnet50_v1", 2)])
-def test_s2d_halo_box_windows_match_tap_boxes(monkeypatch, model, bs):
-    """kS2D with one 32 B-swizzled halo box per 32 x 8 block, each tap an MMA
-    window starting at an arbitrary 32 B row of it (explicit SBO = box row
-    pitch), against one TMA box per tap: same operands, same MMA order, so
-    bit-identical logits."""
-    imgs = generate_images(model, 21, bs)
-    monkeypatch.setenv("DS_STEM_S2D_MODE", "box")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        box = be.forward(imgs)
-    monkeypatch.setenv("DS_STEM_S2D_MODE", "tap")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        tap = be.forward(imgs)
-    assert np.array_equal(box, tap)
 
 
 def test_softmax_probs():
@@ -181,45 +78,6 @@ def test_pair_mma_matches_single_cta(monkeypatch, model, bs):
     assert np.array_equal(pair, single)
 
 
-@pytest.mark.parametrize("pair", ["0", "1"])
-@pytest.mark.parametrize("bs", [1, 3, 6])
-def test_pwdw_fusion_matches_two_kernels(monkeypatch, bs, pair):
-    """1x1 conv + depthwise in one launch on the 14 x 14 maps (kPwDw: a tile
-    is one image x 128 channels, the 1x1 output rounded to bf16 into a
-    shared-memory halo buffer, the depthwise in strips with the standalone
-    kernels' per-output fma order; stride 1 and the stride-2 14 -> 7 layer)
-    against the two launches: bit-identical logits, and six launches fewer
-    per MobileNet forward. pair=1: kPairPwDw, two images per cta_group::2
-    MMA (odd batches leave the last pair's second CTA without an image)."""
-    imgs = generate_images("mobilenet_v1", 23, bs)
-    monkeypatch.setenv("DS_CONV_PAIR", pair)
-    monkeypatch.setenv("DS_PWDW", "1")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        fused = be.forward(imgs)
-        k_fused = be.stats()["kernels_per_forward"]
-    monkeypatch.setenv("DS_PWDW", "0")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        plain = be.forward(imgs)
-        k_plain = be.stats()["kernels_per_forward"]
-    assert np.array_equal(fused, plain)
-    assert k_plain - k_fused == 6
-
-
-@pytest.mark.parametrize("model,bs", [("resnet50_v1", 3), ("inception_v3", 2)])
-def test_row_pool_kernel_matches_per_pixel_kernel(monkeypatch, model, bs):
-    """Register-blocked 3x3 pooling (four output columns per thread, each input
-    vector loaded once per row) against the per-pixel kernel: the same taps in
-    the same order per output, so bit-identical logits."""
-    imgs = generate_images(model, 29, bs)
-    monkeypatch.setenv("DS_POOL_LEGACY", "0")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        rows = be.forward(imgs)
-    monkeypatch.setenv("DS_POOL_LEGACY", "1")
-    with GpuBackend(model, Config(abs_max_bs=4, max_mtl=1)) as be:
-        legacy = be.forward(imgs)
-    assert np.array_equal(rows, legacy)
-
-
 def test_narrow_window_convs_match_gather(monkeypatch):
     """Inception's 16/32-channel stride-1 3x3 convs as kS2D window MMAs (one
     32 B-swizzled halo box per 16-channel block, padding as negative box
@@ -233,21 +91,6 @@ def test_narrow_window_convs_match_gather(monkeypatch):
     with GpuBackend("inception_v3", Config(abs_max_bs=4, max_mtl=1)) as be:
         gather = be.forward(imgs)
     assert np.array_equal(win, gather)
-
-
-@pytest.mark.parametrize("bs", [1, 5])
-def test_depthwise_4channel_groups_match_8channel(monkeypatch, bs):
-    """The 14 x 14 depthwise layers with 4-channel thread groups (half the
-    registers, twice the occupancy) against 8-channel groups: the same fma
-    order per output, so bit-identical logits."""
-    imgs = generate_images("mobilenet_v1", 37, bs)
-    monkeypatch.setenv("DS_DW_G4", "1")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        g4 = be.forward(imgs)
-    monkeypatch.setenv("DS_DW_G4", "0")
-    with GpuBackend("mobilenet_v1", Config(abs_max_bs=8, max_mtl=1)) as be:
-        g8 = be.forward(imgs)
-    assert np.array_equal(g4, g8)
 
 
 def test_residual_tma_staging_matches_register_loads(monkeypatch):
