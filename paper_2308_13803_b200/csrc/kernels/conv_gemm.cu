@@ -47,6 +47,11 @@ constexpr int kYStageBytes = 32 * 128;
 // Staging buffers per epilogue warp: two (the next group fills while the
 // last one's TMA store reads), one when sixteen warps drain (smem for the ring).
 __host__ __device__ constexpr int y_bufs(int epi_warps) { return epi_warps > 8 ? 1 : 2; }
+// Staging bytes per epilogue warp: narrow (32-column slices, two 2 KiB 64 B-
+// swizzled buffers) or wide (64-column groups, y_bufs 4 KiB buffers).
+__host__ __device__ constexpr int y_warp_bytes(int epi_warps, bool narrow) {
+  return narrow ? kYStageBytes : y_bufs(epi_warps) * kYStageBytes;
+}
 
 // Warp roles (kConvThreads = 18 warps).
 constexpr int kEpiWarps = 8;      // warps 0-7: epilogue (two teams of four)
@@ -65,7 +70,8 @@ struct SmemLayout {
 // BN x 64) stays resident in shared memory for all tiles (one N tile, small
 // K); otherwise each ring stage carries its own B block.
 __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, int epi_warps,
-                                                  int b_res_blocks = 0, int mt = 1, int win_bytes = 0) {
+                                                  int b_res_blocks = 0, int mt = 1, int win_bytes = 0,
+                                                  bool narrow = false) {
   SmemLayout L;
   L.a_off = 0;
   L.b_off = static_cast<uint32_t>(stages) * mt * kABytes;  // stage = mt A sub-tiles
@@ -74,7 +80,7 @@ __host__ __device__ inline SmemLayout smem_layout(int BN, int stages, int cout, 
   // kWindow: raw[2] + chunk-major[2] halo boxes
   L.win_off = L.y_off;
   L.y_off += 4 * static_cast<uint32_t>((win_bytes + 1023) / 1024 * 1024);
-  L.bar_off = L.y_off + epi_warps * y_bufs(epi_warps) * kYStageBytes;
+  L.bar_off = L.y_off + epi_warps * y_warp_bytes(epi_warps, narrow);
   // full[stages], empty[stages], tmem_full[kMaxAcc], tmem_empty[kMaxAcc], b_full,
   // win barriers[8], tmem slot, residual-staging barriers[2 x 16 warps]
   L.bias_off = L.bar_off + ((2 * stages + 2 * kMaxAcc + 2 + 8 + 32) * 8 + 15) / 16 * 16;
@@ -179,8 +185,10 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
   const int r0 = t / GPR;
 
   // Output coordinates of this thread's rows m0+r0+p*RPP, by one division
-  // for the first row and carries after that (rows are consecutive pixels).
-  int pix[PASSES], hi0[PASSES], wi0[PASSES];
+  // for the first row and carries after that (rows are consecutive pixels):
+  // per row the element offset of its window origin (may lie in the padding)
+  // and the origin itself for the bounds checks.
+  int base[PASSES], hi0[PASSES], wi0[PASSES];
   {
     const int HoWo = a.Ho * a.Wo;
     const int m_first = m0 + r0;
@@ -191,9 +199,9 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
       const bool live = m_first + p * RPP < a.M;
-      pix[p] = n * a.H * a.W;
       hi0[p] = live ? ho * a.stride_h - a.pad_h : -(1 << 28);  // dead rows read zeros
       wi0[p] = wo * a.stride_w - a.pad_w;
+      base[p] = live ? ((n * a.H + hi0[p]) * a.W + wi0[p]) * a.C : 0;
       wo += RPP;
       while (wo >= a.Wo) {
         wo -= a.Wo;
@@ -211,15 +219,22 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
   // (row & 7) is fixed per thread.
   const uint32_t lane_off = static_cast<uint32_t>(r0) * 128 +
                             ((((col_bytes >> 4) ^ (r0 & 7)) << 4) | (col_bytes & 15));
+  // This thread's K position k = kb * 64 + gi * G as (kernel row r, kernel
+  // column sx, channel c), divided once and then advanced by 64 per K block
+  // with carries (the per-K-block integer divisions were the gather warps'
+  // critical path: ~190 instructions per K block, now ~40).
+  int c = gi * G, r = 0, sx = 0;
+  {
+    const int tap = c / a.C;
+    c -= tap * a.C;
+    r = tap / a.S;
+    sx = tap - r * a.S;
+  }
   for (int kb = 0; kb < a.num_kb; ++kb, rp.next(a.stages)) {
     const uint32_t s = rp.slot;
     if (rp.lap > 0) ptx::mbar_wait(&empty[s], (rp.lap - 1) & 1);
-    const int k = kb * kConvBK + gi * G;
-    const int tap = k / a.C;
-    const int c = k - tap * a.C;
-    const int r = tap / a.S;
-    const int sx = tap - r * a.S;
-    const bool kvalid = tap < a.taps;
+    const bool kvalid = r < a.R;  // (K padding past the last tap reads zeros)
+    const int delta = (r * a.W + sx) * a.C + c;
     const uint32_t sbase = smem_base + s * kABytes + lane_off;
 #pragma unroll
     for (int p = 0; p < PASSES; ++p) {
@@ -227,8 +242,7 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
       const int wi = wi0[p] + sx;
       const bool v = kvalid && static_cast<unsigned>(hi) < static_cast<unsigned>(a.H) &&
                      static_cast<unsigned>(wi) < static_cast<unsigned>(a.W);
-      const __nv_bfloat16* src =
-          v ? a.x + (static_cast<size_t>(pix[p] + hi * a.W + wi) * a.C + c) : a.x;
+      const __nv_bfloat16* src = v ? a.x + (base[p] + delta) : a.x;
       const uint32_t off = static_cast<uint32_t>(p * RPP * 128);
       if constexpr (GB == 16) {
         ptx::cp_async_16(sbase + off, src, v ? 16u : 0u);
@@ -237,6 +251,14 @@ __device__ __forceinline__ void gather_a_tile(const ConvGemmArgs& a, uint8_t* sm
       }
     }
     ptx::cp_async_mbar_arrive_noinc(&full[s]);
+    c += kConvBK;
+    while (c >= a.C) {
+      c -= a.C;
+      if (++sx == a.S) {
+        sx = 0;
+        ++r;
+      }
+    }
   }
 }
 
@@ -523,11 +545,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     conv_gemm_kernel(const __grid_constant__ ConvGemmArgs args) {
   // kPairTmaA: a TMA-A conv on CTA pairs, one M = 256 pair MMA per K step
   // (cta_group::2 throughout), each CTA holding half of every B block
-  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA);
+  // (kPairIm2col: the same over TMA im2col A loads)
+  // (kPairGather: over the cp.async im2col gather; the peer CTA's idle MMA
+  // warp forwards its gather completion to the leader's full barrier)
+  constexpr bool kPairG = MODE == static_cast<int>(ConvLoadMode::kPairGather);
+  constexpr bool kPair = MODE == static_cast<int>(ConvLoadMode::kPairTmaA) ||
+                         MODE == static_cast<int>(ConvLoadMode::kPairIm2col) || kPairG;
   // kIm2col: R x S / strided convs whose A blocks are TMA im2col loads (one per
   // (tap, 64-channel block)); otherwise the TMA-A machinery
-  constexpr bool kI2C = MODE == static_cast<int>(ConvLoadMode::kIm2col);
-  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || kPair || kI2C;
+  constexpr bool kI2C = MODE == static_cast<int>(ConvLoadMode::kIm2col) ||
+                        MODE == static_cast<int>(ConvLoadMode::kPairIm2col);
+  constexpr bool kTmaA = MODE == static_cast<int>(ConvLoadMode::kTmaA) || (kPair && !kPairG) || kI2C;
   // residual adds are compiled into the 1x1 modes only (the runtime routes
   // every residual conv there); the other modes carry none of that state
   constexpr bool kRes = kTmaA;
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // block is still under 32 KiB)
   const SmemLayout L = smem_layout(kPair ? args.BN / 2 : args.BN, args.stages, args.Cout, epi_warps, args.b_res,
                                    kWin ? 1 : kS2 ? 2 : args.mt,
-                                   kWin ? static_cast<int>(args.win_box_bytes) : 0);
+                                   kWin ? static_cast<int>(args.win_box_bytes) : 0, !kBlk && args.y_narrow != 0);
   const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
   const uint32_t a_stage = static_cast<uint32_t>(kS2 ? 2 : mt) * kABytes;
@@ -609,7 +637,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                    : MODE == static_cast<int>(ConvLoadMode::kStemU8)
                                        ? static_cast<uint32_t>(mt)  // lane 0 of each warp of the group
                                        : kGatherWarps * 32u;
-        ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
+        if constexpr (kPairG)  // leader: gather + its expect_tx + the peer's forward; peer: gather
+          ptx::mbar_init(&full[s], producers + (ptx::cluster_ctarank() == 0 ? 2u : 0u));
+        else
+          ptx::mbar_init(&full[s], producers + (kTmaA || kS2 || args.b_res == 0 ? 1u : 0u));
         // (cluster multicast: both CTAs' MMAs consume a B slot; pairs: the
         // leader's commit arrives in both CTAs once)
         ptx::mbar_init(&empty[s], 1);
@@ -676,11 +707,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int part_cols = args.BN / tpa;
     const int ybufs = y_bufs(epi_warps);
     const int sub_rows = kBlk ? kConvBM / args.dw_tw : 0;  // block rows per 128-row sub-tile
-    uint8_t* ystage = smem + L.y_off + warp * ybufs * kYStageBytes;
+    uint8_t* ystage = smem + L.y_off + warp * y_warp_bytes(epi_warps, !kBlk && args.y_narrow != 0);
     // store groups: one 128 B swizzle row per lane (64 bf16 / 32 fp32), or
     // with y_narrow (sixteen epilogue warps) 32 bf16 in two 2 KiB 64 B-swizzled
     // buffers, so the next slice fills while the last one's TMA store reads
-    const bool narrow = kTmaA && args.y_narrow != 0;  // (only the TMA-A modes have 16 epilogue warps)
+    const bool narrow = !kBlk && args.y_narrow != 0;
     const int group_cols = narrow || args.out_f32 ? 32 : 64;
     const int nbufs = narrow ? 2 : ybufs;
     const uint32_t buf_bytes = narrow ? kYStageBytes / 2 : kYStageBytes;
@@ -889,8 +920,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     } else if constexpr (!kTmaA) {  // (in TMA-A mode these warps are epilogue teams 2-3)
       RingPos rp;
-      TileWalk tw(n_tiles);
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
+      TileWalk tw(n_tiles, cl);
+      for (int tile = walk_first; tile < walk_count; tile += walk_stride, tw.next()) {
         const int m0 = tw.mb * kConvBM;
         gather_a_tile<8>(args, smem + L.a_off, full, empty, m0, rp);
       }
@@ -1005,9 +1036,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (tw.rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * tx);
             ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.b_off + s * b_bytes), &args.tmap_b, &full[s],
                                   kb * kConvBK, n0 + tw.rank * (args.BN / 2));
-            for (int q = 0; q < mt; ++q)
-              ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes), &args.tmap_a,
-                                    &full[s], kb * kConvBK, m0 + q * kConvBM);
+            if constexpr (kI2C) {  // this CTA's 128 output pixels' windows (mt == 1)
+              const int cbs = args.C >> 6;
+              const int t = kb / cbs, cb = kb - t * cbs;
+              const int tr = t / args.S, tc = t - tr * args.S;
+              const int hw_o = args.Ho * args.Wo;
+              const int n = m0 / hw_o, rem = m0 - n * hw_o;
+              const int ho = rem / args.Wo, wo = rem - ho * args.Wo;
+              ptx::tma_load_im2col_pair(ptx::smem_u32(smem + L.a_off + s * a_stage), &args.tmap_a, &full[s],
+                                        cb * 64, wo * args.stride_w - args.pad_w,
+                                        ho * args.stride_h - args.pad_h, n, tc, tr);
+            } else if constexpr (kTmaA) {
+              for (int q = 0; q < mt; ++q)
+                ptx::tma_load_2d_pair(ptx::smem_u32(smem + L.a_off + s * a_stage + q * kABytes), &args.tmap_a,
+                                      &full[s], kb * kConvBK, m0 + q * kConvBM);
+            }
             continue;
           }
           ptx::mbar_arrive_expect_tx(&full[s], tx);
@@ -1293,6 +1336,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (args.ts && lane == 0 && j < 8) ts_mark(args.ts, 16 + j, ts0);
       }
       if (args.ts && lane == 0) ts_mark(args.ts, 2, ts0);
+    } else if constexpr (kPairG) {
+      // peer CTA: forward each ring slot's gather completion (its 128 A rows
+      // landed in this CTA's smem) to the leader's full barrier
+      if (lane == 0) {
+        RingPos rp;
+        for (int tile = walk_first; tile < walk_count; tile += walk_stride)
+          for (int kb = 0; kb < args.num_kb; ++kb, rp.next(args.stages)) {
+            ptx::mbar_wait(&full[rp.slot], rp.lap & 1);
+            ptx::fence_proxy_async_smem();  // (cp.async writes -> the leader's tensor-core reads)
+            ptx::mbar_arrive_cluster(&full[rp.slot], 0);
+          }
+      }
     }
     __syncwarp();
   }
@@ -1479,17 +1534,18 @@ uint32_t pow2_at_least(int x) {
 }
 }  // namespace
 
-int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks, int mt) {
+int conv_gemm_stages(int BN, int cout, int epi_warps, int b_res_blocks, int mt, bool narrow) {
   const int ctas = 1;  // 18 warps: one CTA per SM
   const int per_stage = mt * kABytes + (b_res_blocks > 0 ? 0 : BN * kConvBK * 2);
   const int fixed =
-      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, b_res_blocks, mt).total) + 64 * 8 + 1024;
+      static_cast<int>(smem_layout(BN, 0, cout, epi_warps, b_res_blocks, mt, 0, narrow).total) + 64 * 8 + 1024;
   const int budget = (227 * 1024) / ctas - fixed;
   return std::max(1, std::min(kConvMaxStages, budget / per_stage));
 }
 
-size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks, int mt) {
-  return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt).total + 1024;  // + alignment slack
+size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps, int b_res_blocks, int mt,
+                            bool narrow) {
+  return smem_layout(BN, stages, cout, epi_warps, b_res_blocks, mt, 0, narrow).total + 1024;  // + alignment slack
 }
 
 // kWindow ring sizing (shared by the launcher and conv_gemm_window_ok).
@@ -1545,7 +1601,8 @@ cudaError_t conv_gemm_init() {
     cudaError_t e = cudaSuccess;
     for (auto* k : {conv_gemm_kernel<0>, conv_gemm_kernel<2>, conv_gemm_kernel<4>, conv_gemm_kernel<5>,
                     conv_gemm_kernel<6>, conv_gemm_kernel<7>, conv_gemm_kernel<10>, conv_gemm_kernel<11>,
-                    conv_gemm_kernel<12>})
+                    conv_gemm_kernel<12>, conv_gemm_kernel<13>,
+                    conv_gemm_kernel<14>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     return e;
   }();
@@ -1566,7 +1623,8 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   // A store group (64 bf16 / 32 fp32 columns) must not straddle two N tiles.
   ConvGemmArgs args = in_args;
   args.span = launch_span();
-  const bool pair = mode == ConvLoadMode::kPairTmaA;
+  const bool pair = mode == ConvLoadMode::kPairTmaA || mode == ConvLoadMode::kPairIm2col ||
+                    mode == ConvLoadMode::kPairGather;
   if (pair) {
     // CTA pairs: each CTA's B half is BN / 2 rows of 128 B swizzle atoms
     if (args.BN % 16 != 0 || args.BN > 256) return cudaErrorInvalidValue;
@@ -1598,7 +1656,10 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.n_acc = std::max(2, std::min(kMaxAcc, static_cast<int>(512 / acc_cols)));
   args.tmem_cols = pow2_at_least(args.n_acc * static_cast<int>(acc_cols));
   const bool tmaa = mode == ConvLoadMode::kTmaA || mode == ConvLoadMode::kIm2col;
-  args.teams = std::min((tmaa || pair) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
+  // (the gather modes' warps 8-15 produce A: at most two epilogue teams)
+  const bool gather = mode == ConvLoadMode::kGather16 || mode == ConvLoadMode::kPairGather;
+  const bool pair_t = pair && !gather;
+  args.teams = std::min((tmaa || pair_t) && args.BN <= 64 ? teams_tma : kEpiWarps / 4,
                         args.n_acc);
   if (args.teams == 3) args.teams = 2;  // a power of two
   // wide TMA-A tiles with two accumulators: the idle gather warps join and
@@ -1608,9 +1669,13 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const char* e = std::getenv("DS_CONV_TPA");
     return !(e && e[0] == '0');
   }();
-  if (tpa_on && (tmaa || pair) && args.BN >= 128 && args.n_acc == 2 &&
+  if (tpa_on && (tmaa || pair_t) && args.BN >= 128 && args.n_acc == 2 &&
       args.BN % (2 * group_cols) == 0)
     args.teams = 4;
+  if (const char* e = std::getenv("DS_DEV_TEAMS")) {
+    const int t = std::atoi(e);
+    if (t == 1 || t == 2 || (t == 4 && !gather)) args.teams = std::min(t, args.n_acc);
+  }
   // sixteen epilogue warps (one staging buffer each at 64-column groups):
   // store 32-column slices through a 64 B-swizzled map instead, two buffers
   // per warp (DS_Y_NARROW=0: off)
@@ -1620,7 +1685,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const bool on = !(e && e[0] == '0');
     const bool blk_mode = mode == ConvLoadMode::kWindow || mode == ConvLoadMode::kS2D ||
                           mode == ConvLoadMode::kS2DWide;
-    if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8 &&
+    const char* all = std::getenv("DS_DEV_NARROW_ALL");
+    const bool want = 4 * args.teams > 8 || (all && all[0] == '1' && mode != ConvLoadMode::kStemU8);
+    if (on && args.y_tma && !args.out_f32 && !blk_mode && want &&
         encode_tmap_out_narrow(&args.tmap_y, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
                                static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
                                static_cast<uint64_t>(args.ldy)))
@@ -1642,7 +1709,9 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   // per-tile weight loads (and no TMA hop on the operand ring's critical path)
   const int n_tiles = (args.Cout + args.BN - 1) / args.BN;
   args.b_res = !pair && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
-  args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, args.b_res, args.mt);
+  args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, args.b_res, args.mt,
+                                 args.y_narrow != 0);
+  if (const char* e = std::getenv("DS_DEV_STAGES")) args.stages = std::max(1, std::min(args.stages, std::atoi(e)));
   if (mode == ConvLoadMode::kStemU8) {
     // one private slot per producer group (stem_slot); drop to one epilogue
     // team if that is what makes the slots fit
@@ -1692,7 +1761,11 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, args.b_res, 1,
                         static_cast<int>(args.win_box_bytes)).total + 1024
           : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
-                                 args.b_res, s2 ? 2 : args.mt);
+                                 args.b_res, s2 ? 2 : args.mt, args.y_narrow != 0);
+  if (std::getenv("DS_DEV_PRINT"))
+    std::printf("conv_gemm mode %d BN %d mt %d teams %d n_acc %d stages %d narrow %d smem %zu\n",
+                static_cast<int>(mode), args.BN, args.mt, args.teams, args.n_acc, args.stages, args.y_narrow,
+                smem);
   const int tiles = win || s2 ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
                               : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.
@@ -1704,7 +1777,10 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const int m_blocks = (args.M + kConvBM - 1) / kConvBM;
     const int units = n_tiles * ((m_blocks + 1) / 2);
     const int ctas = std::min(2 * units, conv_gemm_sm_count() * per_sm) / 2 * 2;
-    return launch_pdl_cluster(conv_gemm_kernel<7>, dim3(ctas), dim3(kConvThreads), smem, stream, 2, args);
+    auto* k = mode == ConvLoadMode::kPairIm2col   ? conv_gemm_kernel<13>
+              : mode == ConvLoadMode::kPairGather ? conv_gemm_kernel<14>
+                                                  : conv_gemm_kernel<7>;
+    return launch_pdl_cluster(k, dim3(ctas), dim3(kConvThreads), smem, stream, 2, args);
   }
   const dim3 grid(std::min(tiles, conv_gemm_sm_count() * per_sm));
   switch (mode) {

@@ -98,6 +98,10 @@ enum class ConvLoadMode : int {
   kWindowT = 11,  // (internal) kWindow with transposed boxes: launch as kWindow, win_direct 0
   kIm2col = 12,   // R x S / strided convs with C % 64 == 0: A blocks by TMA im2col loads
                   // (tmap_a from encode_tmap_im2col), then the TMA-A pipeline
+  kPairGather = 14,  // kGather16 on CTA pairs (the peer's gather completion is forwarded to
+                     // the leader's full barrier by its otherwise idle MMA warp)
+  kPairIm2col = 13,  // kIm2col on CTA pairs (cta_group::2 M = 256 MMAs, each CTA loading
+                     // its 128 output pixels' im2col A block and half of the B block)
 };
 
 // Im2col map over an NHWC bf16 activation for an R x S conv (stride, padding):
@@ -129,7 +133,7 @@ bool encode_tmap_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, i
                       int box_w, int box_h, int box_n = 1, bool sw128 = false);
 
 size_t conv_gemm_smem_bytes(int BN, int stages, int cout, int epi_warps = 8, int b_res_blocks = 0,
-                            int mt = 1);
+                            int mt = 1, bool narrow = false);
 
 // kStemU8 needs eight operand-ring slots (one per producer warp) next to one
 // epilogue team; false when this stem cannot have them (the runtime then
@@ -139,7 +143,8 @@ bool conv_gemm_stem_fits(int R, int S, int cout);
 // Operand-ring depth for an N tile: as deep as kConvMaxStages allows within
 // the per-CTA budget, where two CTAs share an SM whenever their TMEM
 // (2 x BN accumulator columns each) fits.
-int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0, int mt = 1);
+int conv_gemm_stages(int BN, int cout, int epi_warps = 8, int b_res_blocks = 0, int mt = 1,
+                     bool narrow = false);
 uint32_t conv_gemm_tmem_cols(int BN);
 
 // Whether a conv runs as kWindow: stride 1, R*S > 1, C % 16 == 0, and the

@@ -462,6 +462,18 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
       : "memory");
 }
 
+// 4-D im2col load (64 channels x 128 output pixels of one (r, s) tap) into
+// this CTA's smem whose completion bytes count on the leader CTA's mbarrier.
+__device__ __forceinline__ void tma_load_im2col_pair(uint32_t dst, const void* tmap, uint64_t* bar, int c,
+                                                     int w, int h, int n, int off_w, int off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(tmap), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar) & 0xFEFFFFFFu),
+      "h"(static_cast<uint16_t>(off_w)), "h"(static_cast<uint16_t>(off_h))
+      : "memory");
+}
+
 // Arrive on the mbarrier at this offset in CTA `rank` (default semantics: the
 // caller has already waited for its TMEM loads, which is all the leader needs).
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {

@@ -49,6 +49,18 @@ bool pair_on(int bn) {
   return m == 1 && bn >= 128;
 }
 
+// Gather (and opt-in TMA im2col) convs on CTA pairs: M = 256 pair MMAs, each
+// CTA gathering its own 128 A rows and staging half of every weight block
+// (kPairGather; the peer's gather completion is forwarded to the leader).
+// Half the weight traffic and shared-memory writes per MMA: ResNet-50's
+// 3x3s at bs 256 77 -> 68 us (28^2), 51 -> 45 (14^2), 62 -> 54 (7^2).
+// Off with DS_CONV_PAIR=0 (all pairs) or DS_CONV_PAIR_GATHER=0.
+bool pair_gather_on(int bn) {
+  const char* p = std::getenv("DS_CONV_PAIR");
+  const char* e = std::getenv("DS_CONV_PAIR_GATHER");
+  return !(p && p[0] == '0') && !(e && e[0] == '0') && bn >= 64 && bn <= 256 && bn % 16 == 0;
+}
+
 // Stride-1 R x S convs as kWindow (shifted-window MMAs, no im2col). Default:
 // only where the halo box is read in place (C % 64 == 0) and the map is at
 // least 56 x 56: ResNet's 56^2 3x3s run in 44 % of the gather's time, but at
@@ -72,13 +84,14 @@ bool narrow_window_on() {
   return !(e && e[0] == '0');
 }
 
-// TMA im2col for convs with C % 64 == 0 on maps of at least 28 x 28 (ResNet's
-// 28^2 3x3s: 77 -> 70 us); on 17^2 and smaller maps the cp.async gather of
-// eight warps is faster than the TMA unit's per-pixel im2col walk (Inception
-// 17^2: 28.7 vs 36.9 us). DS_CONV_IM2COL=0: all on the gather.
+// TMA im2col A loads for convs with C % 64 == 0 on maps of at least 28 x 28
+// (opt-in, DS_CONV_IM2COL=1): since the gather's per-K-block address math
+// went incremental and the gather runs on CTA pairs, the cp.async gather is
+// faster on every map size (ResNet 28^2 3x3 at bs 256: 68 vs 88 us; the TMA
+// unit's per-pixel im2col walk bounds the im2col mode).
 bool im2col_on() {
   const char* e = std::getenv("DS_CONV_IM2COL");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 bool window_on(int c, int ho, int wo) {
@@ -332,6 +345,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     if (pl.mode == ConvLoadMode::kTmaA && !b_resident && pair_on(a.BN)) {
       pl.mode = ConvLoadMode::kPairTmaA;
       a.cluster = 2;  // (tmap_b boxes of BN / 2 rows: each CTA's half)
+    } else if (pl.mode == ConvLoadMode::kIm2col && pair_gather_on(a.BN)) {
+      pl.mode = ConvLoadMode::kPairIm2col;
+      a.cluster = 2;
+    } else if (pl.mode == ConvLoadMode::kGather16 && pair_gather_on(a.BN)) {
+      pl.mode = ConvLoadMode::kPairGather;
+      a.cluster = 2;
     }
     if (static_cast<int>(i) == s2d_.op) {
       if (!encode_tmap_2d_bf16(&a.tmap_b, d_stem_w_, p.cout, s2d_.kpad, s2d_.kpad, a.BN))

@@ -68,9 +68,23 @@ static int run(const Case& cs) {
   if (getenv("BN")) cs_bn.BN = atoi(getenv("BN"));
   const Case& cs2 = cs_bn;
 #define cs cs2
+  if (getenv("I2C") && cs.mode == ConvLoadMode::kGather16 && cs.C % 64 == 0) mode = ConvLoadMode::kIm2col;
   if (getenv("PAIR") && mode == ConvLoadMode::kTmaA) {  // cta_group::2 pair MMAs
     mode = ConvLoadMode::kPairTmaA;
     a.cluster = 2;
+  }
+  if (getenv("PAIR") && mode == ConvLoadMode::kGather16) {
+    mode = ConvLoadMode::kPairGather;
+    a.cluster = 2;
+  }
+  if (getenv("PAIR") && mode == ConvLoadMode::kIm2col) {
+    mode = ConvLoadMode::kPairIm2col;
+    a.cluster = 2;
+  }
+  if ((mode == ConvLoadMode::kIm2col || mode == ConvLoadMode::kPairIm2col) &&
+      !encode_tmap_im2col(&a.tmap_a, dx, cs.N, cs.H, cs.W, cs.C, cs.R, cs.S, cs.sh, cs.sw, cs.ph, cs.pw)) {
+    printf("%s: im2col map encode failed\n", cs.name);
+    return 1;
   }
   if (!encode_tmap_2d_bf16(&a.tmap_b, dw, cs.Cout, Kpad, Kpad,
                            cs.BN / a.cluster)) {
@@ -165,6 +179,13 @@ static int run(const Case& cs) {
     stat(1, 3, "exit barrier");
   }
 
+  if (getenv("NOCHECK")) {
+    const double flops = 2.0 * M * cs.Cout * K;
+    printf("%-28s M=%7d N=%5d K=%5d  mode %d  %.3f us  %.1f TFLOP/s (unchecked)\n", cs.name, M, cs.Cout, K,
+           static_cast<int>(mode), ms * 1e3, flops / (ms * 1e-3) / 1e12);
+    cudaFree(dx); cudaFree(dw); cudaFree(dr); cudaFree(db); cudaFree(dy);
+    return 0;
+  }
   std::vector<uint8_t> hy(ybytes);
   cudaMemcpy(hy.data(), dy, ybytes, cudaMemcpyDeviceToHost);
   double max_err = 0, max_ref = 0;
@@ -221,6 +242,17 @@ int main(int argc, char** argv) {
       {"mbv1 pw7 bs128", 128, 14, 14, 512, 1, 1, 1, 1, 0, 0, 512, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 pw5 bs128", 128, 28, 28, 256, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"mbv1 fc bs128", 128, 1, 1, 1024, 1, 1, 1, 1, 0, 0, 1000, 64, ConvLoadMode::kTmaA, false, true, false, 0, 0},
+      {"rn 28 3x3 bs256", 256, 28, 28, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"rn 14 3x3 bs256", 256, 14, 14, 256, 3, 3, 1, 1, 1, 1, 256, 256, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"rn 7 3x3 bs256", 256, 7, 7, 512, 3, 3, 1, 1, 1, 1, 512, 256, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"rn 56 1x1s2 bs256", 256, 56, 56, 256, 1, 1, 2, 2, 0, 0, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 17 1x7 c128 bs128", 128, 17, 17, 128, 1, 7, 1, 1, 0, 3, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 17 7x1 c192 bs128", 128, 17, 17, 192, 7, 1, 1, 1, 3, 0, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 8 3x3 c448 bs128", 128, 8, 8, 448, 3, 3, 1, 1, 1, 1, 384, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 8 1x3 c384 bs128", 128, 8, 8, 384, 1, 3, 1, 1, 0, 1, 384, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"small 3x3 c128 chk", 3, 10, 12, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"small 3x3s2 c64 chk", 3, 15, 13, 64, 3, 3, 2, 2, 1, 1, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"small 1x7 c192 chk", 2, 17, 17, 192, 1, 7, 1, 1, 0, 3, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"mbv1 pw4 bs128", 128, 28, 28, 128, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, false, false, true, 0, 0},
   };
   // Optional filter: substring of the case name; "--no-check" skips the CPU reference.
