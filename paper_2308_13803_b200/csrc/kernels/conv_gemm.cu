@@ -679,6 +679,34 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) ts_mark(args.ts, 5);
   pdl_trigger();
+  // The weights do not depend on earlier layers: before waiting for the
+  // previous grid, land resident weights in shared memory, or pull the first
+  // tile's streamed weight blocks into L2 (off the post-wait critical path).
+  if (warp == kTmaWarp && lane == 0) {
+    const uint32_t bb = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
+    if (kWin) {
+      const int ntap = args.R * args.S, ncb = (args.C + 63) / 64;
+      if (args.b_res > 0) {  // every (K block, tap) weight tile, once
+        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(ncb * ntap) * bb);
+        for (int kb = 0; kb < ncb; ++kb)
+          for (int t = 0; t < ntap; ++t)
+            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + (kb * ntap + t) * bb), &args.tmap_b, b_full,
+                             t * args.C + kb * 64, 0);
+      } else if (walk_first < walk_count) {
+        const int n0 = TileWalk(n_tiles).nb * args.BN;
+        for (int kb = 0; kb < ncb; ++kb)
+          for (int t = 0; t < ntap; ++t) ptx::tma_prefetch_2d(&args.tmap_b, t * args.C + kb * 64, n0);
+      }
+    } else if (args.b_res > 0) {  // the whole weight matrix, once
+      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * bb);
+      for (int kb = 0; kb < args.num_kb; ++kb)
+        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * bb), &args.tmap_b, b_full, kb * kConvBK, 0);
+    } else if (walk_first < walk_count) {
+      const TileWalk t0(n_tiles, cl);
+      const int n0 = t0.nb * args.BN + (kPair ? t0.rank * (args.BN / 2) : 0);
+      for (int kb = 0; kb < args.num_kb; ++kb) ptx::tma_prefetch_2d(&args.tmap_b, kb * kConvBK, n0);
+    }
+  }
   pdl_wait();  // activations (and the residual) come from earlier layers
   span_mark(args.span);
   if (args.ts && threadIdx.x == 0) {
@@ -927,12 +955,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else if (warp == kTmaWarp && kS2) {
-    if (lane == 0) {
-      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
-      for (int kb = 0; kb < args.num_kb; ++kb)
-        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
-                         kb * kConvBK, 0);
+    if (lane == 0) {  // (the resident weights were issued before pdl_wait)
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
@@ -962,14 +985,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == kTmaWarp && kWin) {
     if (lane == 0) {
       const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
-      const bool b_res = args.b_res > 0;
-      if (b_res) {  // every (K block, tap) weight tile, once
-        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(win_cblocks * win_taps) * b_bytes);
-        for (int kb = 0; kb < win_cblocks; ++kb)
-          for (int t = 0; t < win_taps; ++t)
-            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + (kb * win_taps + t) * b_bytes),
-                             &args.tmap_b, b_full, t * args.C + kb * 64, 0);
-      }
+      const bool b_res = args.b_res > 0;  // (resident weights issued before pdl_wait)
       RingPos rp;
       TileWalk tw(n_tiles);
       uint32_t u = 0;
@@ -1006,13 +1022,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == kTmaWarp) {
     if (lane == 0) {
       const uint32_t b_bytes = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
-      const bool b_res = args.b_res > 0;
-      if (b_res) {  // the whole weight matrix, once
-        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
-        for (int kb = 0; kb < args.num_kb; ++kb)
-          ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
-                           kb * kConvBK, 0);
-      }
+      const bool b_res = args.b_res > 0;  // (resident weights issued before pdl_wait)
       const uint32_t tx = (b_res ? 0u : b_bytes) + (kTmaA ? a_stage : 0);
       uint32_t j = 0;
       RingPos rp;

@@ -102,6 +102,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // ---------------------------------------------------------------- TMA
 // Bulk prefetch of a contiguous global range into L2 (16 B aligned, size a
 // multiple of 16).
+// L2 prefetch of one box of a 2-D tensor map (no shared-memory destination).
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(c0),
+               "r"(c1)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
