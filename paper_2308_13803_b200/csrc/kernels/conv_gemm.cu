@@ -1682,10 +1682,6 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   if (tpa_on && (tmaa || pair_t) && args.BN >= 128 && args.n_acc == 2 &&
       args.BN % (2 * group_cols) == 0)
     args.teams = 4;
-  if (const char* e = std::getenv("DS_DEV_TEAMS")) {
-    const int t = std::atoi(e);
-    if (t == 1 || t == 2 || (t == 4 && !gather)) args.teams = std::min(t, args.n_acc);
-  }
   // sixteen epilogue warps (one staging buffer each at 64-column groups):
   // store 32-column slices through a 64 B-swizzled map instead, two buffers
   // per warp (DS_Y_NARROW=0: off)
@@ -1695,9 +1691,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const bool on = !(e && e[0] == '0');
     const bool blk_mode = mode == ConvLoadMode::kWindow || mode == ConvLoadMode::kS2D ||
                           mode == ConvLoadMode::kS2DWide;
-    const char* all = std::getenv("DS_DEV_NARROW_ALL");
-    const bool want = 4 * args.teams > 8 || (all && all[0] == '1' && mode != ConvLoadMode::kStemU8);
-    if (on && args.y_tma && !args.out_f32 && !blk_mode && want &&
+    if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8 &&
         encode_tmap_out_narrow(&args.tmap_y, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
                                static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
                                static_cast<uint64_t>(args.ldy)))
@@ -1721,7 +1715,6 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   args.b_res = !pair && n_tiles == 1 && args.num_kb * args.BN * 128 <= 64 * 1024 ? args.num_kb : 0;
   args.stages = conv_gemm_stages(pair ? args.BN / 2 : args.BN, args.Cout, 4 * args.teams, args.b_res, args.mt,
                                  args.y_narrow != 0);
-  if (const char* e = std::getenv("DS_DEV_STAGES")) args.stages = std::max(1, std::min(args.stages, std::atoi(e)));
   if (mode == ConvLoadMode::kStemU8) {
     // one private slot per producer group (stem_slot); drop to one epilogue
     // team if that is what makes the slots fit
@@ -1772,10 +1765,6 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
                         static_cast<int>(args.win_box_bytes)).total + 1024
           : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
                                  args.b_res, s2 ? 2 : args.mt, args.y_narrow != 0);
-  if (std::getenv("DS_DEV_PRINT"))
-    std::printf("conv_gemm mode %d BN %d mt %d teams %d n_acc %d stages %d narrow %d smem %zu\n",
-                static_cast<int>(mode), args.BN, args.mt, args.teams, args.n_acc, args.stages, args.y_narrow,
-                smem);
   const int tiles = win || s2 ? n_tiles * (args.M / (args.Ho * args.Wo)) * args.dw_tiles_y * args.dw_tiles_x
                               : n_tiles * ((args.M + kConvBM * args.mt - 1) / (kConvBM * args.mt));
   // Resident CTAs per SM: shared memory and TMEM columns (512 per SM) decide.

@@ -245,7 +245,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.Cout = p.cout;
     // FC heads have one or two M tiles at serving batch sizes: narrow N tiles
     // spread their long K loop over 16+ SMs instead of 4
-    a.BN = op.kind == OpKind::kFc ? 64 : choose_bn(p.cout);
+    const int fc_bn = [] {
+      const char* e = std::getenv("DS_FC_BN");
+      const int v = e ? std::atoi(e) : 64;
+      return (v == 16 || v == 32 || v == 64 || v == 128) ? v : 64;
+    }();
+    a.BN = op.kind == OpKind::kFc ? fc_bn : choose_bn(p.cout);
     a.stages = choose_stages(a.BN, p.cout);
     a.tmem_cols = tmem_cols_for(a.BN);
     a.bias = d_b_ + hp.b_off.at(op.param);

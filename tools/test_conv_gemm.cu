@@ -250,6 +250,10 @@ int main(int argc, char** argv) {
       {"in 17 7x1 c192 bs128", 128, 17, 17, 192, 7, 1, 1, 1, 3, 0, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"in 8 3x3 c448 bs128", 128, 8, 8, 448, 3, 3, 1, 1, 1, 1, 384, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"in 8 1x3 c384 bs128", 128, 8, 8, 384, 1, 3, 1, 1, 0, 1, 384, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 35 5x5 c48 bs128", 128, 35, 35, 48, 5, 5, 1, 1, 2, 2, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 35 3x3 c96 bs128", 128, 35, 35, 96, 3, 3, 1, 1, 1, 1, 96, 96, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"in 35 3x3 c64 bs128", 128, 35, 35, 64, 3, 3, 1, 1, 1, 1, 96, 96, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"small 5x5 c48 chk", 2, 11, 9, 48, 5, 5, 1, 1, 2, 2, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3 c128 chk", 3, 10, 12, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3s2 c64 chk", 3, 15, 13, 64, 3, 3, 2, 2, 1, 1, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 1x7 c192 chk", 2, 17, 17, 192, 1, 7, 1, 1, 0, 3, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
