@@ -466,6 +466,13 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
   }
 }
 
+// Segment of output column n (fused sibling convs, nseg > 0).
+__device__ __forceinline__ int seg_of(const ConvGemmArgs& a, int n) {
+  int s = 0;
+  while (s + 1 < a.nseg && n >= a.seg_col[s + 1]) ++s;
+  return s;
+}
+
 // TMA-store epilogue for one 32-column slice of the warp's 32 rows: TMEM ->
 // registers, + bias (+ residual), ReLU, packed into the 128 B-swizzled
 // staging rows (lane = row, conflict-free 16 B stores). `col` is the slice's
@@ -474,7 +481,7 @@ template <bool RES>
 __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const float* bias_s, int m,
                                                    int n, const uint32_t (&raw)[32], uint8_t* group,
                                                    int col, int lane, const uint4 (&res)[4],
-                                                   bool narrow = false) {
+                                                   bool narrow, bool relu) {
   float v[32];
   const float4* b4 = reinterpret_cast<const float4*>(bias_s + n);  // n % 32 == 0
 #pragma unroll
@@ -504,11 +511,11 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
   }
   // (bf16 outputs: the ReLU runs on the packed pairs, after rounding — the
   // same values, one max.bf16x2 per pair instead of two FMNMX)
-  if (a.relu && a.out_f32) {
+  if (relu && a.out_f32) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
   }
-  const uint32_t relu_floor = a.relu ? 0u : 0xFF80FF80u;  // max with 0, or with -inf (identity)
+  const uint32_t relu_floor = relu ? 0u : 0xFF80FF80u;  // max with 0, or with -inf (identity)
   if (narrow) {  // 64 B rows, 64 B swizzle: 16 B chunk c of row r at c ^ ((r >> 1) & 3)
     uint8_t* row64 = group + lane * 64;
     const int sw64 = (lane >> 1) & 3;
@@ -537,6 +544,37 @@ __device__ __forceinline__ void epilogue_slice_tma(const ConvGemmArgs& a, const 
                      relu_pack_bf16(v[8 * q + 2], v[8 * q + 3], relu_floor),
                      relu_pack_bf16(v[8 * q + 4], v[8 * q + 5], relu_floor),
                      relu_pack_bf16(v[8 * q + 6], v[8 * q + 7], relu_floor));
+  }
+}
+
+// Before griddepcontrol.wait (the weights do not depend on earlier layers):
+// land resident weights in shared memory, or pull the first tile's streamed
+// weight blocks into L2, off the post-wait critical path. Out of line: one
+// thread runs it once, and inlined it cost the epilogue registers.
+template <bool kWin, bool kPair>
+__device__ __noinline__ void prewait_weights(const ConvGemmArgs& args, uint32_t b_smem, uint64_t* b_full,
+                                             int n_tiles, int cl, int walk_first, int walk_count) {
+  const uint32_t bb = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
+  if (kWin) {
+    const int ntap = args.R * args.S, ncb = (args.C + 63) / 64;
+    if (args.b_res > 0) {  // every (K block, tap) weight tile, once
+      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(ncb * ntap) * bb);
+      for (int kb = 0; kb < ncb; ++kb)
+        for (int t = 0; t < ntap; ++t)
+          ptx::tma_load_2d(b_smem + (kb * ntap + t) * bb, &args.tmap_b, b_full, t * args.C + kb * 64, 0);
+    } else if (walk_first < walk_count) {
+      const int n0 = TileWalk(n_tiles).nb * args.BN;
+      for (int kb = 0; kb < ncb; ++kb)
+        for (int t = 0; t < ntap; ++t) ptx::tma_prefetch_2d(&args.tmap_b, t * args.C + kb * 64, n0);
+    }
+  } else if (args.b_res > 0) {  // the whole weight matrix, once
+    ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * bb);
+    for (int kb = 0; kb < args.num_kb; ++kb)
+      ptx::tma_load_2d(b_smem + kb * bb, &args.tmap_b, b_full, kb * kConvBK, 0);
+  } else if (walk_first < walk_count) {
+    const TileWalk t0(n_tiles, cl);
+    const int n0 = t0.nb * args.BN + (kPair ? t0.rank * (args.BN / 2) : 0);
+    for (int kb = 0; kb < args.num_kb; ++kb) ptx::tma_prefetch_2d(&args.tmap_b, kb * kConvBK, n0);
   }
 }
 
@@ -590,7 +628,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t s2_box_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   float* bias_s = reinterpret_cast<float*>(smem + L.bias_off);
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
-  if (args.y_tma && threadIdx.x == 0) ptx::tma_prefetch_desc(&args.tmap_y);
+  if (args.y_tma && threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&args.tmap_y);
+    for (int sg = 0; sg < args.nseg; ++sg) ptx::tma_prefetch_desc(&args.tmap_seg[sg]);
+  }
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + args.stages;
   uint64_t* tmem_full = empty + args.stages;  // [n_acc]
@@ -682,31 +723,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // The weights do not depend on earlier layers: before waiting for the
   // previous grid, land resident weights in shared memory, or pull the first
   // tile's streamed weight blocks into L2 (off the post-wait critical path).
-  if (warp == kTmaWarp && lane == 0) {
-    const uint32_t bb = static_cast<uint32_t>(kPair ? args.BN / 2 : args.BN) * 128;
-    if (kWin) {
-      const int ntap = args.R * args.S, ncb = (args.C + 63) / 64;
-      if (args.b_res > 0) {  // every (K block, tap) weight tile, once
-        ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(ncb * ntap) * bb);
-        for (int kb = 0; kb < ncb; ++kb)
-          for (int t = 0; t < ntap; ++t)
-            ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + (kb * ntap + t) * bb), &args.tmap_b, b_full,
-                             t * args.C + kb * 64, 0);
-      } else if (walk_first < walk_count) {
-        const int n0 = TileWalk(n_tiles).nb * args.BN;
-        for (int kb = 0; kb < ncb; ++kb)
-          for (int t = 0; t < ntap; ++t) ptx::tma_prefetch_2d(&args.tmap_b, t * args.C + kb * 64, n0);
-      }
-    } else if (args.b_res > 0) {  // the whole weight matrix, once
-      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * bb);
-      for (int kb = 0; kb < args.num_kb; ++kb)
-        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * bb), &args.tmap_b, b_full, kb * kConvBK, 0);
-    } else if (walk_first < walk_count) {
-      const TileWalk t0(n_tiles, cl);
-      const int n0 = t0.nb * args.BN + (kPair ? t0.rank * (args.BN / 2) : 0);
-      for (int kb = 0; kb < args.num_kb; ++kb) ptx::tma_prefetch_2d(&args.tmap_b, kb * kConvBK, n0);
-    }
-  }
+  if (warp == kTmaWarp && lane == 0)
+    prewait_weights<kWin, kPair>(args, ptx::smem_u32(smem + L.b_off), b_full, n_tiles, cl, walk_first, walk_count);
   pdl_wait();  // activations (and the residual) come from earlier layers
   span_mark(args.span);
   if (args.ts && threadIdx.x == 0) {
@@ -814,6 +832,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const int g_end = (part + 1) * part_cols;
           for (int g0 = part * part_cols; g0 < g_end && n0 + g0 < args.Cout; g0 += group_cols) {
             uint8_t* group = ystage + (nbufs == 2 ? (groups & 1) * buf_bytes : 0);
+            // (fused siblings: a segment without ReLU, e.g. ResNet's projection)
+            bool relu_g = args.relu != 0;
+            if constexpr (!kBlk)
+              if (args.nseg > 0) relu_g = relu_g && !((args.seg_norelu >> seg_of(args, n0 + g0)) & 1);
             if (rtma) {
               // next slice's residual into the other buffer once its store has read it
               if (lane == 0 && g0 + group_cols < g_end && n0 + g0 + group_cols < args.Cout) {
@@ -854,7 +876,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               uint32_t raw[32];
               ptx::tmem_ld_32x32b_x32(t_row + g0 + c, raw);
               ptx::tmem_ld_wait();
-              epilogue_slice_tma<kRes>(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res, narrow);
+              epilogue_slice_tma<kRes>(args, bias_s, m, n0 + g0 + c, raw, group, c, lane, res, narrow,
+                                       relu_g);
             }
             ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> TMA engine
             __syncwarp();
@@ -865,7 +888,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                   ptx::tma_store_4d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, b_x * args.dw_tw,
                                     b_y * args.dw_th + yq, b_img);
               } else {
-                ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+                if (args.nseg > 0) {  // a fused sibling's columns go to its own buffer
+                  const int sg = seg_of(args, n0 + g0);
+                  ptx::tma_store_2d(&args.tmap_seg[sg], ptx::smem_u32(group), n0 + g0 - args.seg_col[sg],
+                                    m0 + quarter * 32);
+                } else {
+                  ptx::tma_store_2d(&args.tmap_y, ptx::smem_u32(group), n0 + g0, m0 + quarter * 32);
+                }
               }
               ptx::bulk_commit();
             }
@@ -1644,6 +1673,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   }
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
+  if (args.nseg > 0 && (!args.y_tma || args.nseg > 4)) return cudaErrorInvalidValue;  // (segments store by TMA)
   // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
   // one ring stage, one accumulator (mt x BN columns) and one trip through
   // the barriers, amortising the per-tile MMA-issue / barrier latency that
@@ -1691,11 +1721,20 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
     const bool on = !(e && e[0] == '0');
     const bool blk_mode = mode == ConvLoadMode::kWindow || mode == ConvLoadMode::kS2D ||
                           mode == ConvLoadMode::kS2DWide;
-    if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8 &&
-        encode_tmap_out_narrow(&args.tmap_y, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
-                               static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
-                               static_cast<uint64_t>(args.ldy)))
-      args.y_narrow = 1;
+    if (on && args.y_tma && !args.out_f32 && !blk_mode && 4 * args.teams > 8) {
+      CUtensorMap ty, tseg[4];
+      bool ok = encode_tmap_out_narrow(&ty, static_cast<__nv_bfloat16*>(args.y) + args.c_off,
+                                       static_cast<uint64_t>(args.M), static_cast<uint64_t>(args.Cout),
+                                       static_cast<uint64_t>(args.ldy));
+      for (int sg = 0; sg < args.nseg && ok; ++sg)
+        ok = encode_tmap_out_narrow(&tseg[sg], args.seg_y[sg], static_cast<uint64_t>(args.M),
+                                    static_cast<uint64_t>(args.seg_w[sg]), static_cast<uint64_t>(args.seg_ld[sg]));
+      if (ok) {
+        args.tmap_y = ty;
+        for (int sg = 0; sg < args.nseg; ++sg) args.tmap_seg[sg] = tseg[sg];
+        args.y_narrow = 1;
+      }
+    }
   }
   // ... and residual layers stage each residual slice into that buffer by TMA
   // (DS_RES_TMA=0: off)

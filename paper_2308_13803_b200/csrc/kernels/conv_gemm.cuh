@@ -48,6 +48,16 @@ struct ConvGemmArgs {
   int mt;     // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
   int cluster;  // 2 = CTA pairs (kPairTmaA; launch_conv_gemm sets it): tmap_b box rows
                 // are then BN / 2 (each CTA loads its half of every weight block)
+  // Fused sibling 1x1 convs (model.hpp fuse_sibling_1x1): nseg > 0 splits
+  // the N columns into segments [seg_col[s], seg_col[s + 1]) (multiples of
+  // 64), each stored through tmap_seg[s] into its own buffer / channel slice
+  // (clipped at its real width seg_w[s]); bit s of seg_norelu: no ReLU.
+  int nseg;
+  int seg_col[5];
+  int seg_norelu;
+  CUtensorMap tmap_seg[4];
+  void* seg_y[4];  // (host: segment bases, widths and row strides for re-encoding)
+  int seg_w[4], seg_ld[4];
   const float* bias;
   const __nv_bfloat16* residual;
   int ld_res;

@@ -128,6 +128,18 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     buf_off.push_back(
         take(static_cast<size_t>(max_bs) * b.h * b.w * b.c * (b.f32 ? sizeof(float) : 2)));
   const size_t probs_off = take(static_cast<size_t>(max_bs) * m.classes * sizeof(float));
+  // fused sibling 1x1 convs: concatenated weights / biases, each sibling's
+  // rows padded to a multiple of 64 (its store group never straddles two)
+  auto seg_rows = [&](int param) { return round_up(m.params.at(param).cout, 64); };
+  std::vector<size_t> fw_off(m.ops.size(), 0), fb_off(m.ops.size(), 0);
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    if (op.fused.empty()) continue;
+    int rows = seg_rows(op.param);
+    for (const auto& f : op.fused) rows += seg_rows(f.param);
+    fw_off[i] = take(static_cast<size_t>(rows) * hp.kpad.at(op.param) * 2);
+    fb_off[i] = take(static_cast<size_t>(rows) * sizeof(float));
+  }
   s2d_ = stem_s2d(m);
   size_t s2d_off = 0, stem_w_off = 0;
   if (s2d_.op >= 0) {
@@ -185,6 +197,31 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                              cudaMemcpyHostToDevice, stream_),
              "upload biases");
 
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    const OpSpec& op = m.ops[i];
+    if (op.fused.empty()) continue;
+    const int kpad = hp.kpad.at(op.param);
+    std::vector<int> params{op.param};
+    for (const auto& f : op.fused) params.push_back(f.param);
+    int rows = 0;
+    for (int p : params) rows += seg_rows(p);
+    std::vector<uint16_t> w(static_cast<size_t>(rows) * kpad, 0);
+    std::vector<float> b(rows, 0.0f);
+    int r0 = 0;
+    for (int p : params) {
+      if (hp.kpad.at(p) != kpad) throw std::logic_error("fused 1x1 siblings with different K");
+      const int co = m.params[p].cout;
+      std::copy(hp.w.begin() + hp.w_off.at(p), hp.w.begin() + hp.w_off.at(p) + static_cast<size_t>(co) * kpad,
+                w.begin() + static_cast<size_t>(r0) * kpad);
+      std::copy(hp.b.begin() + hp.b_off.at(p), hp.b.begin() + hp.b_off.at(p) + co, b.begin() + r0);
+      r0 += seg_rows(p);
+    }
+    check_cuda(cudaMemcpyAsync(base + fw_off[i], w.data(), w.size() * 2, cudaMemcpyHostToDevice, stream_),
+               "upload fused weights");
+    check_cuda(cudaMemcpyAsync(base + fb_off[i], b.data(), b.size() * 4, cudaMemcpyHostToDevice, stream_),
+               "upload fused biases");
+    check_cuda(cudaStreamSynchronize(stream_), "upload fused weights");
+  }
   plans_.resize(m.ops.size());
   stem_ = fused_stem(m);
   if (stem_ < 0 && s2d_.op < 0)
@@ -206,8 +243,11 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       // output (every input >= 0): the producer of op.in must apply ReLU.
       const BufferSpec& pin = m.buffers.at(op.in);
       bool relu_input = false;
-      for (size_t j = 0; j < i; ++j)
+      for (size_t j = 0; j < i; ++j) {
         if (m.ops[j].out == op.in) relu_input = m.ops[j].relu;
+        for (const auto& f : m.ops[j].fused)
+          if (f.out == op.in) relu_input = f.relu;
+      }
       const char* legacy = std::getenv("DS_POOL_TMA");
       const bool allow = !(legacy && legacy[0] == '0');
       pool_maps_.resize(m.ops.size());
@@ -244,11 +284,12 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.taps = op.r * op.s;
     a.Cout = p.cout;
     // FC heads have one or two M tiles at serving batch sizes: narrow N tiles
-    // spread their long K loop over 16+ SMs instead of 4
+    // spread their long K loop over 63 SMs (N = 16: MobileNet's FC 8.9 -> 7.9
+    // us at bs 128 against N = 64; DS_FC_BN = 16 / 32 / 64 / 128)
     const int fc_bn = [] {
       const char* e = std::getenv("DS_FC_BN");
-      const int v = e ? std::atoi(e) : 64;
-      return (v == 16 || v == 32 || v == 64 || v == 128) ? v : 64;
+      const int v = e ? std::atoi(e) : 16;
+      return (v == 16 || v == 32 || v == 64 || v == 128) ? v : 16;
     }();
     a.BN = op.kind == OpKind::kFc ? fc_bn : choose_bn(p.cout);
     a.stages = choose_stages(a.BN, p.cout);
@@ -383,6 +424,59 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
                       : 0;
       else
         a.y_tma = encode_tmap_out(&a.tmap_y, base, rows, p.cout, out.c, out.f32) ? 1 : 0;
+    }
+    if (!op.fused.empty()) {
+      // one launch over the concatenated weights; segment s's columns are
+      // stored into its own buffer / channel slice
+      if (pl.mode != ConvLoadMode::kTmaA && pl.mode != ConvLoadMode::kPairTmaA &&
+          pl.mode != ConvLoadMode::kGather16 && pl.mode != ConvLoadMode::kPairGather &&
+          pl.mode != ConvLoadMode::kIm2col && pl.mode != ConvLoadMode::kPairIm2col)
+        throw std::logic_error("fused 1x1 siblings need a TMA-A, im2col or gather conv");
+      std::vector<ConvSeg> segs{ConvSeg{op.param, op.out, op.c_off, op.relu}};
+      segs.insert(segs.end(), op.fused.begin(), op.fused.end());
+      const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
+      int col = 0;
+      a.nseg = static_cast<int>(segs.size());
+      a.seg_norelu = 0;
+      for (int sg = 0; sg < a.nseg; ++sg) {
+        const ConvSeg& f = segs[sg];
+        const int co = m.params[f.param].cout;
+        const BufferSpec& ob = m.buffers.at(f.out);
+        if (ob.h != out.h || ob.w != out.w || ob.f32) throw std::logic_error("fused sibling output shape");
+        a.seg_col[sg] = col;
+        a.seg_y[sg] = static_cast<uint8_t*>(bufs_[f.out]) + static_cast<size_t>(f.c_off) * 2;
+        a.seg_w[sg] = co;
+        a.seg_ld[sg] = ob.c;
+        if (!f.relu) a.seg_norelu |= 1 << sg;
+        if (!encode_tmap_out(&a.tmap_seg[sg], a.seg_y[sg], rows, co, ob.c, false))
+          throw CudaError("cuTensorMapEncodeTiled failed (fused sibling output)");
+        col += round_up(co, 64);
+      }
+      a.seg_col[a.nseg] = col;
+      a.relu = 1;  // (per segment through seg_norelu)
+      a.Cout = col;
+      a.BN = choose_bn(col);
+      a.stages = choose_stages(a.BN, col);
+      a.tmem_cols = tmem_cols_for(a.BN);
+      a.bias = reinterpret_cast<const float*>(base + fb_off[i]);
+      a.cluster = 1;
+      if (pl.mode == ConvLoadMode::kPairTmaA) pl.mode = ConvLoadMode::kTmaA;
+      if (pl.mode == ConvLoadMode::kPairGather) pl.mode = ConvLoadMode::kGather16;
+      if (pl.mode == ConvLoadMode::kPairIm2col) pl.mode = ConvLoadMode::kIm2col;
+      const bool b_res = (col + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
+      if (pl.mode == ConvLoadMode::kTmaA && !b_res && pair_on(a.BN)) {
+        pl.mode = ConvLoadMode::kPairTmaA;
+        a.cluster = 2;
+      } else if (pl.mode == ConvLoadMode::kGather16 && pair_gather_on(a.BN)) {
+        pl.mode = ConvLoadMode::kPairGather;
+        a.cluster = 2;
+      } else if (pl.mode == ConvLoadMode::kIm2col && pair_gather_on(a.BN)) {
+        pl.mode = ConvLoadMode::kPairIm2col;
+        a.cluster = 2;
+      }
+      if (!encode_tmap_2d_bf16(&a.tmap_b, base + fw_off[i], col, kpad, kpad, a.BN / a.cluster))
+        throw CudaError("cuTensorMapEncodeTiled failed (fused weights)");
+      if (!a.y_tma) throw CudaError("fused sibling 1x1 without a TMA-store epilogue");
     }
   }
   spans_bytes_ = sizeof(unsigned long long) * 2 * (kernels_per_forward_ + 1);

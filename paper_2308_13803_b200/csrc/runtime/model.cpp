@@ -392,6 +392,13 @@ std::vector<KernelCost> kernel_costs(const ModelSpec& m) {
         k.bytes_per_image = in_bytes + out_elems * (out_b.f32 ? 4 : 2) +
                             (op.residual >= 0 ? out_elems * 2 : 0.0);
         k.fixed_bytes = static_cast<double>(p.cout) * p.r * p.s * p.cin * 2 + p.cout * 4.0;
+        for (const auto& f : op.fused) {  // siblings: the input is read once
+          const ParamSpec& q = m.params[f.param];
+          const double oe = hw_out * q.cout;
+          k.flops_per_image += 2.0 * oe * q.cin;
+          k.bytes_per_image += oe * 2;
+          k.fixed_bytes += static_cast<double>(q.cout) * q.cin * 2 + q.cout * 4.0;
+        }
         break;
       }
       case OpKind::kDwConv: {
@@ -421,12 +428,49 @@ std::vector<std::string> model_ids() {
   return {"synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"};
 }
 
+void fuse_sibling_1x1(ModelSpec& m) {
+  auto is_1x1 = [&](const OpSpec& o) {
+    return o.kind == OpKind::kConv && o.r == 1 && o.s == 1 && o.ph == 0 && o.pw == 0 &&
+           o.residual < 0 && o.fused.empty() && !m.buffers[o.out].f32 && o.in != 0;
+  };
+  std::vector<OpSpec> out;
+  std::vector<char> taken(m.ops.size(), 0);
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    if (taken[i]) continue;
+    OpSpec op = m.ops[i];
+    if (is_1x1(op)) {
+      for (size_t j = i + 1; j < m.ops.size() && op.fused.size() < 3; ++j) {
+        const OpSpec& o = m.ops[j];
+        if (taken[j] || !is_1x1(o) || o.in != op.in || o.sh != op.sh || o.sw != op.sw) continue;
+        // moving op j up to i: nothing in between may read its output or
+        // write the buffer it reads
+        bool safe = true;
+        for (size_t k = i + 1; k < j && safe; ++k) {
+          const OpSpec& b = m.ops[k];
+          if (b.in == o.out || b.residual == o.out || b.out == o.in) safe = false;
+          for (const auto& f : b.fused)
+            if (f.out == o.in) safe = false;
+        }
+        if (!safe) continue;
+        op.fused.push_back(ConvSeg{o.param, o.out, o.c_off, o.relu});
+        taken[j] = 1;
+      }
+    }
+    out.push_back(op);
+  }
+  m.ops = std::move(out);
+}
+
 ModelSpec build_model(const std::string& id) {
-  if (id == "synthetic_cnn") return synthetic_cnn();
-  if (id == "mobilenet_v1") return mobilenet_v1();
-  if (id == "resnet50_v1") return resnet50_v1();
-  if (id == "inception_v3") return inception_v3();
-  throw std::invalid_argument("unknown model: " + id);
+  ModelSpec m;
+  if (id == "synthetic_cnn") m = synthetic_cnn();
+  else if (id == "mobilenet_v1") m = mobilenet_v1();
+  else if (id == "resnet50_v1") m = resnet50_v1();
+  else if (id == "inception_v3") m = inception_v3();
+  else throw std::invalid_argument("unknown model: " + id);
+  const char* e = std::getenv("DS_FUSE_1X1");
+  if (!(e && e[0] == '0')) fuse_sibling_1x1(m);
+  return m;
 }
 
 }  // namespace ds

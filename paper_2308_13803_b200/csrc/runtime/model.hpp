@@ -29,6 +29,16 @@ struct ParamSpec {
   bool fc = false;     // FC: std sqrt(1/fan_in), zero bias
 };
 
+// A sibling 1x1 conv fused into an op (same input, same stride): its weights
+// are concatenated after the op's own along N and its outputs go to its own
+// buffer / channel slice (fuse_sibling_1x1 below).
+struct ConvSeg {
+  int param = -1;
+  int out = 0;
+  int c_off = 0;
+  bool relu = true;
+};
+
 struct OpSpec {
   OpKind kind = OpKind::kConv;
   int in = 0;
@@ -38,6 +48,7 @@ struct OpSpec {
   int r = 1, s = 1, sh = 1, sw = 1, ph = 0, pw = 0;
   bool relu = true;
   int param = -1;
+  std::vector<ConvSeg> fused;  // siblings computed by this op's launch (after its own columns)
 };
 
 struct ModelSpec {
@@ -51,8 +62,16 @@ struct ModelSpec {
   double macs_per_image = 0.0;  // algorithmic multiply-accumulates (real channels)
 };
 
-// "synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3".
+// "synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3". Sibling
+// 1x1 convs are fused (fuse_sibling_1x1) unless DS_FUSE_1X1=0.
 ModelSpec build_model(const std::string& id);
+
+// Merges 1x1 convs that read the same buffer with the same stride (Inception's
+// branch heads, ResNet's first conv + projection shortcut) into the first of
+// them: one launch over the concatenated weights, each sibling's columns
+// stored to its own buffer. Same products in the same K order per output, so
+// bit-identical to the separate launches. At most 4 segments per op.
+void fuse_sibling_1x1(ModelSpec& m);
 
 // Algorithmic cost of every kernel of one forward, in launch order:
 // input staging, one entry per op, softmax. Bytes are the minimum DRAM

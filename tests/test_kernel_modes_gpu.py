@@ -140,3 +140,24 @@ def test_tma_pools_match_register_pools(monkeypatch, model, bs):
         regs = be.forward(imgs)
     assert np.isfinite(tma).all()
     assert np.array_equal(tma, regs)
+
+
+@pytest.mark.parametrize("model,bs", [("inception_v3", 3), ("resnet50_v1", 5)])
+def test_fused_sibling_1x1_matches_separate_launches(monkeypatch, model, bs):
+    """Sibling 1x1 convs fused into one launch (model.hpp fuse_sibling_1x1:
+    Inception's branch heads, ResNet's first conv + projection shortcut;
+    concatenated weights, per-segment output maps and ReLU) against the
+    separate launches: the same products in the same K order, so
+    bit-identical logits, and fewer kernels per forward."""
+    imgs = generate_images(model, 53, bs)
+    monkeypatch.setenv("DS_FUSE_1X1", "1")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        fused = be.forward(imgs)
+        k_fused = be.stats()["kernels_per_forward"]
+    monkeypatch.setenv("DS_FUSE_1X1", "0")
+    with GpuBackend(model, Config(abs_max_bs=8, max_mtl=1)) as be:
+        separate = be.forward(imgs)
+        k_sep = be.stats()["kernels_per_forward"]
+    assert np.isfinite(fused).all()
+    assert np.array_equal(fused, separate)
+    assert k_fused < k_sep
