@@ -466,13 +466,6 @@ __device__ __forceinline__ void epilogue_chunk(const ConvGemmArgs& a, const floa
   }
 }
 
-// Segment of output column n (fused sibling convs, nseg > 0).
-__device__ __forceinline__ int seg_of(const ConvGemmArgs& a, int n) {
-  int s = 0;
-  while (s + 1 < a.nseg && n >= a.seg_col[s + 1]) ++s;
-  return s;
-}
-
 // TMA-store epilogue for one 32-column slice of the warp's 32 rows: TMEM ->
 // registers, + bias (+ residual), ReLU, packed into the 128 B-swizzled
 // staging rows (lane = row, conflict-free 16 B stores). `col` is the slice's
@@ -630,7 +623,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int cout_pad = (args.Cout + 63) / 64 * 64 + 64;
   if (args.y_tma && threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&args.tmap_y);
-    for (int sg = 0; sg < args.nseg; ++sg) ptx::tma_prefetch_desc(&args.tmap_seg[sg]);
+    if constexpr (!kBlk)
+      for (int sg = 0; sg < args.nseg; ++sg) ptx::tma_prefetch_desc(&args.tmap_seg[sg]);
   }
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + args.stages;
@@ -723,7 +717,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // The weights do not depend on earlier layers: before waiting for the
   // previous grid, land resident weights in shared memory, or pull the first
   // tile's streamed weight blocks into L2 (off the post-wait critical path).
-  if (warp == kTmaWarp && lane == 0)
+  if (!kS2 && warp == kTmaWarp && lane == 0)  // (the stems load theirs after the wait: registers)
     prewait_weights<kWin, kPair>(args, ptx::smem_u32(smem + L.b_off), b_full, n_tiles, cl, walk_first, walk_count);
   pdl_wait();  // activations (and the residual) come from earlier layers
   span_mark(args.span);
@@ -833,9 +827,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int g0 = part * part_cols; g0 < g_end && n0 + g0 < args.Cout; g0 += group_cols) {
             uint8_t* group = ystage + (nbufs == 2 ? (groups & 1) * buf_bytes : 0);
             // (fused siblings: a segment without ReLU, e.g. ResNet's projection)
-            bool relu_g = args.relu != 0;
-            if constexpr (!kBlk)
-              if (args.nseg > 0) relu_g = relu_g && !((args.seg_norelu >> seg_of(args, n0 + g0)) & 1);
+            const bool relu_g = args.relu != 0 && (kBlk || !((args.norelu_g >> ((n0 + g0) >> 6)) & 1));
             if (rtma) {
               // next slice's residual into the other buffer once its store has read it
               if (lane == 0 && g0 + group_cols < g_end && n0 + g0 + group_cols < args.Cout) {
@@ -889,7 +881,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                     b_y * args.dw_th + yq, b_img);
               } else {
                 if (args.nseg > 0) {  // a fused sibling's columns go to its own buffer
-                  const int sg = seg_of(args, n0 + g0);
+                  const int sg = args.seg_g[(n0 + g0) >> 6];
                   ptx::tma_store_2d(&args.tmap_seg[sg], ptx::smem_u32(group), n0 + g0 - args.seg_col[sg],
                                     m0 + quarter * 32);
                 } else {
@@ -984,7 +976,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else if (warp == kTmaWarp && kS2) {
-    if (lane == 0) {  // (the resident weights were issued before pdl_wait)
+    if (lane == 0) {
+      const uint32_t b_bytes = static_cast<uint32_t>(args.BN) * 128;
+      ptx::mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(args.num_kb) * b_bytes);
+      for (int kb = 0; kb < args.num_kb; ++kb)
+        ptx::tma_load_2d(ptx::smem_u32(smem + L.b_off + kb * b_bytes), &args.tmap_b, b_full,
+                         kb * kConvBK, 0);
       RingPos rp;
       TileWalk tw(n_tiles);
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, tw.next()) {
@@ -1673,7 +1670,14 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   }
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
-  if (args.nseg > 0 && (!args.y_tma || args.nseg > 4)) return cudaErrorInvalidValue;  // (segments store by TMA)
+  if (args.nseg > 0 && (!args.y_tma || args.nseg > 4 || args.Cout > 32 * 64))
+    return cudaErrorInvalidValue;  // (segments store by TMA, 64-column group tables)
+  args.norelu_g = 0;
+  for (int sg = 0; sg < args.nseg; ++sg)
+    for (int g = args.seg_col[sg] / 64; g < args.seg_col[sg + 1] / 64; ++g) {
+      args.seg_g[g] = static_cast<uint8_t>(sg);
+      if ((args.seg_norelu >> sg) & 1) args.norelu_g |= 1u << g;
+    }
   // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
   // one ring stage, one accumulator (mt x BN columns) and one trip through
   // the barriers, amortising the per-tile MMA-issue / barrier latency that
