@@ -1670,13 +1670,13 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   }
   const int group_cols = args.out_f32 ? 32 : 64;
   if (args.y_tma && args.Cout > args.BN && args.BN % group_cols != 0) args.y_tma = 0;
-  if (args.nseg > 0 && (!args.y_tma || args.nseg > 4 || args.Cout > 32 * 64))
+  if (args.nseg > 0 && (!args.y_tma || args.nseg > 4 || args.Cout > 64 * 64))
     return cudaErrorInvalidValue;  // (segments store by TMA, 64-column group tables)
   args.norelu_g = 0;
   for (int sg = 0; sg < args.nseg; ++sg)
     for (int g = args.seg_col[sg] / 64; g < args.seg_col[sg + 1] / 64; ++g) {
       args.seg_g[g] = static_cast<uint8_t>(sg);
-      if ((args.seg_norelu >> sg) & 1) args.norelu_g |= 1u << g;
+      if ((args.seg_norelu >> sg) & 1) args.norelu_g |= 1ull << g;
     }
   // Sub-tiles per tile (TMA-A and stem modes): mt 128-row sub-tiles share
   // one ring stage, one accumulator (mt x BN columns) and one trip through

@@ -55,8 +55,8 @@ struct ConvGemmArgs {
   int nseg;
   int seg_col[5];
   int seg_norelu;
-  uint32_t norelu_g;    // bit g: no ReLU on 64-column group g (from seg_norelu)
-  uint8_t seg_g[32];    // segment of 64-column group g
+  unsigned long long norelu_g;  // bit g: no ReLU on 64-column group g (from seg_norelu)
+  uint8_t seg_g[64];            // segment of 64-column group g
   CUtensorMap tmap_seg[4];
   void* seg_y[4];  // (host: segment bases, widths and row strides for re-encoding)
   int seg_w[4], seg_ld[4];

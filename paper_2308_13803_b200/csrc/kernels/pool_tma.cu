@@ -105,6 +105,10 @@ struct PoolArgs {
   uint32_t box_bytes;     // TMA transaction bytes per box
   uint32_t stage_bytes;   // ring slot stride (box_bytes rounded up to 128 B: TMA destination alignment)
   unsigned long long* span;  // live timing slot (pdl.cuh span_mark)
+  // average pools after swap_avgpool_1x1 (model.hpp): + bias[channel] after
+  // the division, then ReLU if relu (nullptr: plain pool)
+  const float* bias;
+  int relu;
 };
 
 // Tile t -> (channel block [slowest], image, tile row, tile column).
@@ -216,6 +220,15 @@ __global__ void __launch_bounds__(kPoolMaxThreads) pool_tma_kernel(
           float* v = acc[q];
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] = div9(v[e]);
+          if (a.bias) {
+            const float4* b4 = reinterpret_cast<const float4*>(a.bias) + 2 * (cbk * groups + g);
+            const float4 b0 = __ldg(b4), b1 = __ldg(b4 + 1);
+            v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+            v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+            if (a.relu)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.0f);
+          }
           yp[q * a.ldo_g] = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]),
                                        pack2(v[6], v[7]));
         }
@@ -314,13 +327,16 @@ bool pool_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w
 
 cudaError_t launch_pool3x3_tma(const CUtensorMap& in_map, __nv_bfloat16* y, int n, int h, int w,
                                int c, int stride, int pad, bool is_max, int ldo, int c_off,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const float* post_bias, bool post_relu) {
   if (!pool_tma_plan_ok(h, w, c, stride, pad) || ldo % 8 != 0 || c_off % 8 != 0)
     return cudaErrorInvalidValue;
   const int ho = (h + 2 * pad - 3) / stride + 1, wo = (w + 2 * pad - 3) / stride + 1;
   const PoolPlan p = pool_plan(ho, wo, c, stride);
   PoolArgs a{};
   a.span = launch_span();
+  if (post_bias && is_max) return cudaErrorInvalidValue;
+  a.bias = post_bias;
+  a.relu = post_relu ? 1 : 0;
   a.y = reinterpret_cast<uint4*>(y);
   a.ldo_g = ldo / 8;
   a.coff_g = c_off / 8;

@@ -43,7 +43,8 @@ bool pool_tma_input_map(CUtensorMap* map, const void* x, int max_n, int h, int w
                         int stride, int pad);
 cudaError_t launch_pool3x3_tma(const CUtensorMap& in_map, __nv_bfloat16* y, int n, int h, int w,
                                int c, int stride, int pad, bool is_max, int ldo, int c_off,
-                               cudaStream_t stream);
+                               cudaStream_t stream, const float* post_bias = nullptr,
+                               bool post_relu = false);
 
 // Mean over all pixels: [n][hw][c] -> [n][c] bf16.
 cudaError_t launch_global_avgpool(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int hw, int c,

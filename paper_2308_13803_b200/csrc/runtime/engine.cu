@@ -132,6 +132,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
   // rows padded to a multiple of 64 (its store group never straddles two)
   auto seg_rows = [&](int param) { return round_up(m.params.at(param).cout, 64); };
   std::vector<size_t> fw_off(m.ops.size(), 0), fb_off(m.ops.size(), 0);
+  // zeros for bias-free convs (swap_avgpool_1x1: their bias is added after the pool)
+  const size_t zero_bias_off = take(4096 * sizeof(float));
   for (size_t i = 0; i < m.ops.size(); ++i) {
     const OpSpec& op = m.ops[i];
     if (op.fused.empty()) continue;
@@ -202,18 +204,24 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     if (op.fused.empty()) continue;
     const int kpad = hp.kpad.at(op.param);
     std::vector<int> params{op.param};
-    for (const auto& f : op.fused) params.push_back(f.param);
+    std::vector<char> nob{op.no_bias};
+    for (const auto& f : op.fused) {
+      params.push_back(f.param);
+      nob.push_back(f.no_bias);
+    }
     int rows = 0;
     for (int p : params) rows += seg_rows(p);
     std::vector<uint16_t> w(static_cast<size_t>(rows) * kpad, 0);
     std::vector<float> b(rows, 0.0f);
     int r0 = 0;
-    for (int p : params) {
+    for (size_t k = 0; k < params.size(); ++k) {
+      const int p = params[k];
       if (hp.kpad.at(p) != kpad) throw std::logic_error("fused 1x1 siblings with different K");
       const int co = m.params[p].cout;
       std::copy(hp.w.begin() + hp.w_off.at(p), hp.w.begin() + hp.w_off.at(p) + static_cast<size_t>(co) * kpad,
                 w.begin() + static_cast<size_t>(r0) * kpad);
-      std::copy(hp.b.begin() + hp.b_off.at(p), hp.b.begin() + hp.b_off.at(p) + co, b.begin() + r0);
+      if (!nob[k])  // (bias-free segments keep zeros)
+        std::copy(hp.b.begin() + hp.b_off.at(p), hp.b.begin() + hp.b_off.at(p) + co, b.begin() + r0);
       r0 += seg_rows(p);
     }
     check_cuda(cudaMemcpyAsync(base + fw_off[i], w.data(), w.size() * 2, cudaMemcpyHostToDevice, stream_),
@@ -294,7 +302,8 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     a.BN = op.kind == OpKind::kFc ? fc_bn : choose_bn(p.cout);
     a.stages = choose_stages(a.BN, p.cout);
     a.tmem_cols = tmem_cols_for(a.BN);
-    a.bias = d_b_ + hp.b_off.at(op.param);
+    a.bias = op.no_bias ? reinterpret_cast<const float*>(base + zero_bias_off) : d_b_ + hp.b_off.at(op.param);
+    if (op.no_bias && p.cout > 4096) throw std::logic_error("bias-free conv wider than the zero bias");
     if (op.residual >= 0) {
       a.residual = static_cast<const __nv_bfloat16*>(bufs_[op.residual]);
       a.ld_res = m.buffers.at(op.residual).c;
@@ -432,7 +441,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
           pl.mode != ConvLoadMode::kGather16 && pl.mode != ConvLoadMode::kPairGather &&
           pl.mode != ConvLoadMode::kIm2col && pl.mode != ConvLoadMode::kPairIm2col)
         throw std::logic_error("fused 1x1 siblings need a TMA-A, im2col or gather conv");
-      std::vector<ConvSeg> segs{ConvSeg{op.param, op.out, op.c_off, op.relu}};
+      std::vector<ConvSeg> segs{ConvSeg{op.param, op.out, op.c_off, op.relu, op.no_bias}};
       segs.insert(segs.end(), op.fused.begin(), op.fused.end());
       const uint64_t rows = static_cast<uint64_t>(max_bs) * pl.ho * pl.wo;
       int col = 0;
@@ -574,9 +583,12 @@ void Instance::enqueue_layers(int bs, const std::vector<cudaEvent_t>* marks, int
       case OpKind::kAvgPool:
         if (i < pool_tma_.size() && pool_tma_[i]) {
           e = launch_pool3x3_tma(pool_maps_[i], y, bs, in.h, in.w, in.c, op.sh, op.ph,
-                                 op.kind == OpKind::kMaxPool, out.c, op.c_off, cur_stream_);
+                                 op.kind == OpKind::kMaxPool, out.c, op.c_off, cur_stream_,
+                                 op.post_bias >= 0 ? d_b_ + hp.b_off[op.post_bias] : nullptr, op.relu);
           break;
         }
+        if (op.post_bias >= 0)  // (swap_avgpool_1x1 pools run on the TMA kernel only)
+          throw std::logic_error("average pool with a post-bias needs the TMA pool (DS_POOL_SWAP=0)");
         e = launch_pool3x3(x, y, bs, in.h, in.w, in.c, op.sh, op.ph, op.kind == OpKind::kMaxPool,
                            out.c, op.c_off, cur_stream_);
         break;

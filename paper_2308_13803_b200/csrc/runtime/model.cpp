@@ -428,6 +428,50 @@ std::vector<std::string> model_ids() {
   return {"synthetic_cnn", "mobilenet_v1", "resnet50_v1", "inception_v3"};
 }
 
+void swap_avgpool_1x1(ModelSpec& m) {
+  for (size_t i = 0; i < m.ops.size(); ++i) {
+    OpSpec& pool = m.ops[i];
+    if (pool.kind != OpKind::kAvgPool || pool.sh != 1 || pool.sw != 1 || pool.ph != 1 || pool.pw != 1 ||
+        pool.c_off != 0 || pool.post_bias >= 0)
+      continue;
+    const int t = pool.out;
+    int consumer = -1, uses = 0;
+    for (size_t j = 0; j < m.ops.size(); ++j) {
+      const OpSpec& o = m.ops[j];
+      if (o.in == t || o.residual == t) {
+        ++uses;
+        consumer = static_cast<int>(j);
+      }
+      if (j != i && o.out == t) uses = 99;  // (t written elsewhere)
+    }
+    if (uses != 1 || consumer <= static_cast<int>(i)) continue;
+    OpSpec conv = m.ops[consumer];
+    if (conv.kind != OpKind::kConv || conv.r != 1 || conv.s != 1 || conv.sh != 1 || conv.sw != 1 ||
+        conv.ph != 0 || conv.pw != 0 || conv.residual >= 0 || !conv.fused.empty() || conv.no_bias ||
+        m.buffers[conv.out].f32)
+      continue;
+    const BufferSpec x = m.buffers[pool.in];
+    const int cout = m.params[conv.param].cout;
+    if (cout % 8 != 0) continue;
+    m.buffers.push_back(BufferSpec{x.h, x.w, cout, false});
+    const int z = static_cast<int>(m.buffers.size()) - 1;
+    OpSpec c2 = conv;  // W x, no bias, no ReLU
+    c2.in = pool.in;
+    c2.out = z;
+    c2.c_off = 0;
+    c2.relu = false;
+    c2.no_bias = true;
+    OpSpec p2 = pool;  // pool the conv output, + b, ReLU, into the conv's slice
+    p2.in = z;
+    p2.out = conv.out;
+    p2.c_off = conv.c_off;
+    p2.post_bias = conv.param;
+    p2.relu = conv.relu;
+    m.ops[i] = c2;
+    m.ops[consumer] = p2;
+  }
+}
+
 void fuse_sibling_1x1(ModelSpec& m) {
   auto is_1x1 = [&](const OpSpec& o) {
     return o.kind == OpKind::kConv && o.r == 1 && o.s == 1 && o.ph == 0 && o.pw == 0 &&
@@ -452,7 +496,7 @@ void fuse_sibling_1x1(ModelSpec& m) {
             if (f.out == o.in) safe = false;
         }
         if (!safe) continue;
-        op.fused.push_back(ConvSeg{o.param, o.out, o.c_off, o.relu});
+        op.fused.push_back(ConvSeg{o.param, o.out, o.c_off, o.relu, o.no_bias});
         taken[j] = 1;
       }
     }
@@ -468,6 +512,8 @@ ModelSpec build_model(const std::string& id) {
   else if (id == "resnet50_v1") m = resnet50_v1();
   else if (id == "inception_v3") m = inception_v3();
   else throw std::invalid_argument("unknown model: " + id);
+  const char* sw = std::getenv("DS_POOL_SWAP");
+  if (!(sw && sw[0] == '0')) swap_avgpool_1x1(m);
   const char* e = std::getenv("DS_FUSE_1X1");
   if (!(e && e[0] == '0')) fuse_sibling_1x1(m);
   return m;

@@ -37,6 +37,7 @@ struct ConvSeg {
   int out = 0;
   int c_off = 0;
   bool relu = true;
+  bool no_bias = false;
 };
 
 struct OpSpec {
@@ -49,6 +50,10 @@ struct OpSpec {
   bool relu = true;
   int param = -1;
   std::vector<ConvSeg> fused;  // siblings computed by this op's launch (after its own columns)
+  // conv: skip the bias (it is added after a following average pool);
+  // average pool: add param's bias (then ReLU if relu) to the pooled values
+  bool no_bias = false;
+  int post_bias = -1;
 };
 
 struct ModelSpec {
@@ -72,6 +77,15 @@ ModelSpec build_model(const std::string& id);
 // stored to its own buffer. Same products in the same K order per output, so
 // bit-identical to the separate launches. At most 4 segments per op.
 void fuse_sibling_1x1(ModelSpec& m);
+
+// avgpool3x3(s1, p1, count_include_pad) followed by a 1x1 conv (bias b,
+// ReLU) equals ReLU(avgpool3x3(W x) + b): both are linear, the padding taps
+// are zeros either way. Rewrites such pairs to a bias-free 1x1 over the pool's
+// input (which then fuses with its siblings) and a pool over the conv's
+// Cout channels (Inception: 32-192 instead of 192-2048) that adds b and
+// applies the ReLU. Not bit-identical (bf16 rounding moves from the pooled
+// input to the conv output); within the oracle tolerance. DS_POOL_SWAP=0: off.
+void swap_avgpool_1x1(ModelSpec& m);
 
 // Algorithmic cost of every kernel of one forward, in launch order:
 // input staging, one entry per op, softmax. Bytes are the minimum DRAM

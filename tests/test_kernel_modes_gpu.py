@@ -132,6 +132,7 @@ def test_tma_pools_match_register_pools(monkeypatch, model, bs):
     register-blocked pool kernel: the same taps in the same order, so
     bit-identical logits."""
     imgs = generate_images(model, 47, bs)
+    monkeypatch.setenv("DS_POOL_SWAP", "0")  # (the register pools have no post-bias epilogue)
     monkeypatch.setenv("DS_POOL_TMA", "1")
     with GpuBackend(model, Config(abs_max_bs=max(8, bs), max_mtl=1)) as be:
         tma = be.forward(imgs)
@@ -161,3 +162,26 @@ def test_fused_sibling_1x1_matches_separate_launches(monkeypatch, model, bs):
     assert np.isfinite(fused).all()
     assert np.array_equal(fused, separate)
     assert k_fused < k_sep
+
+
+def test_avgpool_1x1_swap_within_oracle_bound(monkeypatch, oracle_mod):
+    """Inception's avgpool3x3 -> 1x1 branches computed as a bias-free 1x1 (fused
+    with its siblings) followed by a pool over its 32-192 channels that adds
+    the bias and applies the ReLU (model.hpp swap_avgpool_1x1; linear, so equal
+    up to where the bf16 rounding happens): both orders stay within the oracle
+    bound and close to each other, with fewer pooled channels."""
+    imgs = generate_images("inception_v3", 61, 4)
+    monkeypatch.setenv("DS_POOL_SWAP", "1")
+    with GpuBackend("inception_v3", Config(abs_max_bs=8, max_mtl=1)) as be:
+        swapped = be.forward(imgs)
+    monkeypatch.setenv("DS_POOL_SWAP", "0")
+    with GpuBackend("inception_v3", Config(abs_max_bs=8, max_mtl=1)) as be:
+        plain = be.forward(imgs)
+    ref = oracle_mod.forward("inception_v3", imgs, bf16_storage=True)
+    mean = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden",
+                                              "top1_inception_v3.npz"))["mean_32"]
+    dep = np.abs(ref - mean).max(1)
+    assert np.isfinite(swapped).all()
+    assert (np.abs(swapped - ref).max(1) / dep).max() <= 4e-2
+    assert (np.abs(plain - ref).max(1) / dep).max() <= 4e-2
+    assert (np.abs(swapped - plain).max(1) / dep).max() <= 4e-2
