@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int b = 0; b < n_acc; ++b) {
         ptx::mbar_init(&tmem_full[b], 1);
         // one arrival per warp of the owning teams (pairs: of both CTAs' teams)
-        ptx::mbar_init(&tmem_empty[b], 4 * (args.teams > n_acc ? args.teams / n_acc : 1) * (kPair ? 2 : 1));
+        ptx::mbar_init(&tmem_empty[b], 4 * args.tpa * (kPair ? 2 : 1));
       }
       if (kRes && args.res_tma)
         for (int b = 0; b < 2 * epi_warps; ++b) ptx::mbar_init(&res_bar[b], 1);
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int quarter = warp & 3;
     // teams per accumulator: with more teams than accumulators, tpa teams
     // share each tile, team t taking column part t % tpa
-    const int tpa = kTmaA && args.teams > n_acc ? args.teams / n_acc : 1;
+    const int tpa = args.tpa;
     const int team = (warp >> 2) / tpa;
     const int part = (warp >> 2) % tpa;
     const int tile_teams = args.teams / tpa;
@@ -1716,6 +1716,18 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   if (tpa_on && (tmaa || pair_t) && args.BN >= 128 && args.n_acc == 2 &&
       args.BN % (2 * group_cols) == 0)
     args.teams = 4;
+  args.tpa = (tmaa || pair_t) && args.teams > args.n_acc ? args.teams / args.n_acc : 1;
+  // all four teams on one tile (tpa 4: each warp drains a quarter of the
+  // tile's columns, half the per-warp slices of tpa 2); the other accumulator
+  // keeps the MMA busy meanwhile. The epilogue's per-slice chain (TMEM load,
+  // math, staging, fence, store: ~1300 cycles) is latency-bound, so more
+  // warps per tile shorten it — but the sixteen warps' TMA stores then queue
+  // behind each other (pw 28^2 -4 %, 56^2 +3 %): opt-in, DS_CONV_TPA4=1.
+  {
+    const char* e = std::getenv("DS_CONV_TPA4");
+    if (e && e[0] == '1' && args.tpa == 2 && args.teams == 4 && args.BN % (4 * 32) == 0)
+      args.tpa = 4;
+  }
   // sixteen epilogue warps (one staging buffer each at 64-column groups):
   // store 32-column slices through a 64 B-swizzled map instead, two buffers
   // per warp (DS_Y_NARROW=0: off)

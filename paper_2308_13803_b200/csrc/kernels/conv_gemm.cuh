@@ -23,54 +23,55 @@ constexpr int kConvSmemBudget = 200 * 1024;  // operand ring budget per CTA (1 C
 // with m = (image, ho, wo), k = (r, s, c) flattened in that order (KRSC
 // weights), A gathered from the NHWC input on the fly.
 struct ConvGemmArgs {
-  CUtensorMap tmap_b;  // weights [Cout][Kpad] bf16, box {64, BN}, 128 B swizzle
-  CUtensorMap tmap_a;  // input viewed as [rows][C] (1x1 stride-1 convs only)
-  CUtensorMap tmap_y;  // output slice [rows][Cout] at y + c_off, 128 B x 32-row boxes (y_tma)
-  int y_tma;           // epilogue stores through smem + TMA (else direct stores)
-  int y_narrow;        // tmap_y has 32 x 32 boxes, 64 B swizzle (launch_conv_gemm sets it)
-  CUtensorMap tmap_r;  // residual with the same 32 x 32 boxes (res_tma)
-  int res_tma;         // epilogue stages residual slices by TMA (launch_conv_gemm sets it)
-  const __nv_bfloat16* x;
-  int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
-  int R, S, stride_h, stride_w, pad_h, pad_w;
-  int Ho, Wo;
+  // Scalars first, the ones every tile / epilogue slice reads at the front:
+  // kernel parameters live in the constant bank, and with the tensor maps
+  // (1 KB+) between them the hot fields spread over many constant-cache lines
+  // and missed on every epilogue slice.
   int M;       // images * Ho * Wo
-  int num_kb;  // ceil(R*S*C / 64)
-  int taps;    // R*S
-  int Cout, BN, stages;
-  uint32_t tmem_cols;
+  int Cout, BN;
+  int mt;      // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
   // Epilogue teams (4 warps each, one per TMEM lane quarter) and TMEM
   // accumulators: tile j goes to accumulator j % n_acc and team j % teams
   // (n_acc a multiple of teams, so each accumulator has one team). Set by
   // launch_conv_gemm from the mode and BN.
   int teams, n_acc;
+  int tpa;     // teams per tile (sharing its columns); teams / tpa tiles drain at once
+  int y_tma;           // epilogue stores through smem + TMA (else direct stores)
+  int y_narrow;        // tmap_y has 32 x 32 boxes, 64 B swizzle (launch_conv_gemm sets it)
+  int res_tma;         // epilogue stages residual slices by TMA (launch_conv_gemm sets it)
+  int out_f32, relu;
+  int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
+  int ld_res;
+  int nseg;        // fused sibling segments (below; 0: none)
+  int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
+  unsigned long long norelu_g;  // bit g: no ReLU on 64-column group g (from seg_norelu)
+  const float* bias;
+  const __nv_bfloat16* residual;
+  void* y;
+  // bring-up timeline (tools/test_conv_gemm TS=1): per CTA 64 clock64 stamps
+  // relative to kernel entry, see conv_gemm.cu ts_mark(); nullptr in the runtime
+  unsigned long long* ts;
+  int res_prefetch;  // epilogue L2 prefetch of residual rows (launch_conv_gemm sets it)
+  int num_kb;  // ceil(R*S*C / 64)
+  int stages;
+  uint32_t tmem_cols;
   int b_res;  // > 0: all num_kb weight blocks resident in smem (one N tile)
-  int mt;     // 128-row sub-tiles per tile (TMA-A / stem modes; launch_conv_gemm sets it)
   int cluster;  // 2 = CTA pairs (kPairTmaA; launch_conv_gemm sets it): tmap_b box rows
                 // are then BN / 2 (each CTA loads its half of every weight block)
+  const __nv_bfloat16* x;
+  int H, W, C;  // input spatial dims; C = channels per pixel (row stride)
+  int R, S, stride_h, stride_w, pad_h, pad_w;
+  int Ho, Wo;
+  int taps;    // R*S
   // Fused sibling 1x1 convs (model.hpp fuse_sibling_1x1): nseg > 0 splits
   // the N columns into segments [seg_col[s], seg_col[s + 1]) (multiples of
   // 64), each stored through tmap_seg[s] into its own buffer / channel slice
   // (clipped at its real width seg_w[s]); bit s of seg_norelu: no ReLU.
-  int nseg;
   int seg_col[5];
   int seg_norelu;
-  unsigned long long norelu_g;  // bit g: no ReLU on 64-column group g (from seg_norelu)
   uint8_t seg_g[64];            // segment of 64-column group g
-  CUtensorMap tmap_seg[4];
   void* seg_y[4];  // (host: segment bases, widths and row strides for re-encoding)
   int seg_w[4], seg_ld[4];
-  const float* bias;
-  const __nv_bfloat16* residual;
-  int ld_res;
-  int res_prefetch;  // epilogue L2 prefetch of residual rows (launch_conv_gemm sets it)
-  void* y;
-  int ldy, c_off;  // output row stride (channels) and channel offset (concat slices)
-  int out_f32, relu;
-  int debug_flags;  // bring-up experiments only (tools/test_conv_gemm): 1 = no epilogue
-  // bring-up timeline (tools/test_conv_gemm TS=1): per CTA 64 clock64 stamps
-  // relative to kernel entry, see conv_gemm.cu ts_mark(); nullptr in the runtime
-  unsigned long long* ts;
   unsigned long long* span;  // live per-kernel timing slot (pdl.cuh span_mark), or nullptr
   // Pixel-block tiles (kWindow, kS2D, kS2DWide): dw_th x dw_tw output pixels
   // of one image, dw_tiles_y x dw_tiles_x blocks per image; epilogue warp q
@@ -91,6 +92,12 @@ struct ConvGemmArgs {
   // staging normalisation x = bf16((p - 127.5) / 63.75) happens in the
   // producer (C = 4 logical channels, the 4th zero, as in the staged layout).
   const uint8_t* img;
+  // Tensor maps (64 B aligned, read by the TMA unit through their addresses)
+  CUtensorMap tmap_b;  // weights [Cout][Kpad] bf16, box {64, BN}, 128 B swizzle
+  CUtensorMap tmap_a;  // input viewed as [rows][C] (1x1 stride-1 convs only)
+  CUtensorMap tmap_y;  // output slice [rows][Cout] at y + c_off, 128 B x 32-row boxes (y_tma)
+  CUtensorMap tmap_r;  // residual with the same 32 x 32 boxes (res_tma)
+  CUtensorMap tmap_seg[4];
   // kStemU8 tap table (launch_conv_gemm fills it): tap t = r*S + s ->
   // byte offset (r*W + s)*3 | r << 24 | s << 28
   int tap_info[64];
