@@ -89,3 +89,38 @@ def test_null_handles_are_errors():
     lat = ctypes.c_double()
     assert lib.ds_run_batch(None, 1, ctypes.byref(lat)) == _lib.DS_EINVAL
     assert lib.ds_mtl(None) == 0
+
+
+def test_graph_rewrites_keep_the_algorithm(monkeypatch):
+    """Build-time rewrites (model.hpp fuse_sibling_1x1, swap_avgpool_1x1):
+    fewer launches, the same algorithmic FLOPs, no more algorithmic bytes
+    (a fused launch reads its shared input once; the swapped pool runs over
+    the conv's channels instead of its input's)."""
+    from paper_2308_13803_b200 import model_info
+
+    def plan(model, fuse, swap):
+        monkeypatch.setenv("DS_FUSE_1X1", "1" if fuse else "0")
+        monkeypatch.setenv("DS_POOL_SWAP", "1" if swap else "0")
+        ks = kernel_costs(model)
+        return (len(ks), sum(k["flops_per_image"] for k in ks),
+                sum(k["bytes_per_image"] for k in ks), [k["kind"] for k in ks])
+
+    for model in ("resnet50_v1", "inception_v3", "mobilenet_v1"):
+        n0, f0, b0, _ = plan(model, False, False)
+        n1, f1, b1, kinds1 = plan(model, True, True)
+        macs2 = 2 * model_info(model).macs_per_image
+        assert abs(f0 - macs2) < 1 and abs(f1 - macs2) < 1, model
+        assert b1 <= b0 + 1, model
+        if model == "mobilenet_v1":
+            assert n1 == n0  # no siblings, no average pools
+    n_plain = plan("inception_v3", False, False)[0]
+    n_fused = plan("inception_v3", True, False)[0]
+    n_both, _, _, kinds = plan("inception_v3", True, True)
+    # 3 Inception-A blocks: 3 sibling heads -> 1 (2 launches each); B: none;
+    # 4 C blocks: 3 -> 1; D: 2 -> 1; 2 E blocks: 3 -> 1
+    assert n_plain - n_fused == 3 * 2 + 4 * 2 + 1 + 2 * 2
+    # the 9 branch avgpool -> 1x1 pairs: the 1x1 joins its block's fused heads
+    assert n_fused - n_both == 9
+    assert kinds.count("pool") == plan("inception_v3", False, False)[3].count("pool")
+    # ResNet: the first block of each stage fuses conv1 with the projection
+    assert plan("resnet50_v1", False, False)[0] - plan("resnet50_v1", True, True)[0] == 4
