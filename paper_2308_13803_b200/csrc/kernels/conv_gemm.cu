@@ -5,26 +5,28 @@
 // behind GpuSim::run_batch / run_mt_request (reference gpu_sim.cpp:13-24):
 // every dense conv, 1x1 conv and FC layer of the served networks runs here.
 //
-// Persistent CTA (one per SM) walking 128 x BN output tiles, N-tile fastest
-// so the CTAs sharing an A row-block run together and A is read from DRAM
-// once. Eighteen warps, three pipelines (operand ring, two TMEM
-// accumulators, tile loop):
-//   warps 0-7  epilogue (two per TMEM lane quarter, alternating 128 B column
-//              groups): TMEM -> registers (tcgen05.ld), + bias (+ residual),
-//              ReLU, packed into 128 B-swizzled smem rows and written by TMA
-//              bulk tensor stores into the (possibly channel-sliced) NHWC
-//              output; releases the accumulator buffer to the MMA warp, so
-//              tile i's epilogue overlaps tile i+1's main loop.
-//   warps 8-15 A producers: gather the im2col rows of each tile straight from
-//              the NHWC input with zero-filling cp.async (padding, K tail and
-//              M tail become zeros), written in the 128 B-swizzled K-major
-//              layout the UMMA descriptor expects; completion reaches the
-//              stage's full barrier via cp.async.mbarrier.arrive.noinc.
-//              For 1x1 stride-1 layers the A tile is a plain 2D box loaded by
-//              the TMA warp instead (kTmaA) and these warps idle.
-//   warp 16    TMA producer for the weight tile (and A in kTmaA); owns TMEM.
-//   warp 17    one thread issues tcgen05.mma (M=128, N=BN, K=16) into the
-//              current fp32 TMEM accumulator and commits stage releases.
+// Persistent CTA (one per SM) walking 128 x BN output tiles (or 128-row
+// sub-tile groups / pixel blocks per mode), N-tile fastest so the CTAs sharing
+// an A row-block run together and A is read from DRAM once. Eighteen warps,
+// three pipelines (operand ring, up to eight TMEM accumulators, tile loop):
+//   warps 0-7  epilogue teams of four (one warp per TMEM lane quarter):
+//              TMEM -> registers (tcgen05.ld), + bias (+ residual), ReLU,
+//              packed into swizzled smem staging and written by TMA bulk
+//              tensor stores into the (possibly channel-sliced, or per fused
+//              sibling) NHWC output; each releases its accumulator to the MMA
+//              warp, so tile i's epilogue overlaps tile i+1's main loop.
+//   warps 8-15 A producers in the gather modes: the im2col rows of each tile
+//              straight from the NHWC input with zero-filling cp.async
+//              (padding, K tail and M tail become zeros), in the 128 B-swizzled
+//              K-major layout of the UMMA descriptor; completion reaches the
+//              stage's full barrier via cp.async.mbarrier.arrive.noinc. In the
+//              TMA-A / im2col modes (A loaded by the TMA warp) they are
+//              epilogue teams 2-3.
+//   warp 16    TMA producer for the weight tiles (and A / halo boxes); owns TMEM.
+//   warp 17    issues tcgen05.mma (M = 128, or M = 256 cta_group::2 on CTA
+//              pairs, N = BN, K = 16) into the current fp32 TMEM accumulator
+//              and commits stage releases; on a pair's peer CTA it forwards
+//              the gather completion to the leader (kPairGather).
 #include "conv_gemm.cuh"
 #include "pdl.cuh"
 #include "sm100_ptx.cuh"
