@@ -320,6 +320,13 @@ void ds_job_session_free(ds_job_session* s);
 size_t ds_job_result_records(const ds_job_result* r, ds_metrics_record* out, size_t cap);
 ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* out);
 ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* out);
+/* The Profiler alone on one catalog network (reference tools/dnnscaler_main.cpp:88-99,
+ * cmd_profile): sigma < 0 takes the catalog's sigma (else 0.05); the ANALYTIC
+ * seam is GpuSim(bm, mm, pm, Config{}, seed) with the raw seed, as the
+ * reference CLI builds it; DEVICE probes dnn_id on the B200. */
+ds_status ds_profile_dnn(const ds_dnn_profile* catalog, int n_catalog, const char* dnn_id, int m,
+                         int n, int batches, uint64_t seed, double sigma,
+                         const ds_seam_spec* seam, ds_profile_report* out);
 size_t ds_job_result_tape(const ds_job_result* r, double* out, size_t cap);
 /* (mJ, wall ms, W) energy readings of a device run, for ds_seam_spec.energy_tape. */
 size_t ds_job_result_energy_tape(const ds_job_result* r, double* out, size_t cap);

@@ -48,6 +48,9 @@ def lib() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, sz]
         l.ref_render_scenario.argtypes = [ctypes.c_char_p, vp, sz, psz, vp, sz, psz,
                                           ctypes.c_char_p, sz]
+        l.ref_render_profile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                         ctypes.c_double, vp, sz, psz, ctypes.c_char_p, sz]
         _lib = l
     return _lib
 
@@ -123,6 +126,20 @@ def render_scenario(scenario_path: str):
     l.ref_render_scenario(scenario_path.encode(), csv, a.value, ctypes.byref(a), js, b.value,
                           ctypes.byref(b), err, 512)
     return csv.raw[:a.value].decode(), js.raw[:b.value].decode()
+
+
+def render_profile(catalog_path: str, dnn_id: str, m=32, n=8, batches=10, seed=42, sigma=-1.0):
+    """The reference CLI's `profile` JSON (dnnscaler_main.cpp:88-111) on the
+    stock simulator."""
+    l = lib()
+    a = ctypes.c_size_t()
+    err = ctypes.create_string_buffer(512)
+    args = (catalog_path.encode(), dnn_id.encode(), m, n, batches, seed, sigma)
+    if l.ref_render_profile(*args, None, 0, ctypes.byref(a), err, 512) != 0:
+        raise RuntimeError(err.value.decode())
+    js = ctypes.create_string_buffer(a.value + 1)
+    l.ref_render_profile(*args, js, a.value, ctypes.byref(a), err, 512)
+    return js.raw[:a.value].decode()
 
 
 def tempdir():

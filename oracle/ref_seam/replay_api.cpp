@@ -7,7 +7,9 @@
 #include <vector>
 
 #include "dnnscaler/catalog.hpp"
+#include "dnnscaler/gpu_sim.hpp"
 #include "dnnscaler/harness.hpp"
+#include "dnnscaler/perf_model.hpp"
 #include "dnnscaler/profiler.hpp"
 #include "dnnscaler/report.hpp"
 #include "dnnscaler/scenario.hpp"
@@ -180,6 +182,31 @@ int ref_render_scenario(const char* scenario_path, char* csv, size_t csv_cap, si
     *csv_len = c.size();
     *json_len = j.size();
     if (csv && csv_cap >= c.size()) std::memcpy(csv, c.data(), c.size());
+    if (json && json_cap >= j.size()) std::memcpy(json, j.data(), j.size());
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_cap, e.what());
+    return 2;
+  }
+}
+
+// The reference CLI's profile subcommand body (tools/dnnscaler_main.cpp:88-99)
+// on the stock simulator, rendered with render_profile_json (report.cpp).
+int ref_render_profile(const char* catalog_path, const char* dnn_id, int m, int n, int batches,
+                       uint64_t seed, double sigma, char* json, size_t json_cap, size_t* json_len,
+                       char* err, size_t err_cap) {
+  try {
+    set_mode(0, nullptr, 0);
+    const auto catalog = load_catalog(catalog_path);
+    const auto& dnn = find_dnn(catalog, dnn_id);
+    const double used_sigma = sigma >= 0.0 ? sigma : dnn.sigma.value_or(0.05);
+    PowerModel pm;
+    if (dnn.u1) pm.u1 = *dnn.u1;
+    GpuSim gpu(calibrate_batching(dnn.batching_points, used_sigma),
+               calibrate_mt(dnn.mt_points, used_sigma), pm, GpuSim::Config{}, seed);
+    const auto report = profile(gpu, m, n, batches);
+    const std::string j = render_profile_json(report, dnn.id, approach_name(decide(report)));
+    *json_len = j.size();
     if (json && json_cap >= j.size()) std::memcpy(json, j.data(), j.size());
     return 0;
   } catch (const std::exception& e) {

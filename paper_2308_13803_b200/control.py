@@ -106,6 +106,9 @@ _SIGS = {
     "ds_job_result_records": (ctypes.c_size_t, [_vp, _P(_Record), ctypes.c_size_t]),
     "ds_job_result_summary": (ctypes.c_int, [_vp, _P(_Summary)]),
     "ds_job_result_profile": (ctypes.c_int, [_vp, _P(_Report)]),
+    "ds_profile_dnn": (ctypes.c_int, [_P(_DnnProfile), ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                      _P(_SeamSpec), _P(_Report)]),
     "ds_job_result_tape": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
     "ds_job_result_energy_tape": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
     "ds_job_result_latencies": (ctypes.c_size_t, [_vp, _vp, ctypes.c_size_t]),
@@ -334,6 +337,20 @@ def run_job(scenario: Scenario, job: JobSpec, catalog: Sequence[DnnProfile], sea
         return _collect(lib, res)
     finally:
         lib.ds_job_result_free(res)
+
+
+def profile_dnn(catalog: Sequence[DnnProfile], dnn_id: str, m: int = 32, n: int = 8,
+                batches: int = 10, seed: int = 42, sigma: float = -1.0, seam: str = "analytic",
+                backend: Optional[GpuBackend] = None, device: int = 0) -> dict:
+    """The Profiler alone on one catalog network (reference
+    tools/dnnscaler_main.cpp:88-99): the ProfileReport fields as a dict."""
+    lib = _l()
+    mar = _Marshal(Scenario(), JobSpec(0, dnn_id, 1.0, 1.0), catalog)
+    spec = mar.seam(seam, backend, device)
+    rp = _Report()
+    _lib.check(lib.ds_profile_dnn(mar.catalog, mar.n_catalog, dnn_id.encode(), m, n, batches, seed,
+                                  sigma, ctypes.byref(spec), ctypes.byref(rp)))
+    return {name: getattr(rp, name) for name, _ in _Report._fields_}
 
 
 class JobSession:

@@ -1,5 +1,6 @@
 // extern "C" boundary over the control plane (include/dnnscaler_b200.h,
 // "Control plane" section).
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -252,18 +253,50 @@ ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* o) {
   return DS_OK;
 }
 
+namespace {
+ds_profile_report to_report(const ds::ProfileReport& p) {
+  return ds_profile_report{p.tput_base,         p.tput_batching,
+                           p.tput_mt,           p.ti_batching,
+                           p.ti_mt,             p.base_latency_ms,
+                           p.probe_latency_batching_ms, p.probe_latency_mt_ms,
+                           p.m,                 p.n,
+                           p.batches_per_point, p.base_elapsed_ms,
+                           p.batching_elapsed_ms, p.mt_elapsed_ms,
+                           p.transition_ms,     p.profiling_cost_ms,
+                           p.items_served};
+}
+}  // namespace
+
+ds_status ds_profile_dnn(const ds_dnn_profile* catalog, int n_catalog, const char* dnn_id, int m,
+                         int n, int batches, uint64_t seed, double sigma,
+                         const ds_seam_spec* seam, ds_profile_report* out) {
+  if (!dnn_id || !seam || !out || (n_catalog > 0 && !catalog)) return invalid("null argument");
+  return guard([&] {
+    const auto cat = to_catalog(catalog, n_catalog);
+    const ds::DnnProfile& dnn = ds::find_dnn(cat, dnn_id);
+    const double used_sigma = sigma >= 0.0 ? sigma : dnn.sigma.value_or(0.05);
+    const auto bm = ds::calibrate_batching(dnn.batching_points, used_sigma);
+    const auto mm = ds::calibrate_mt(dnn.mt_points, used_sigma);
+    std::unique_ptr<ds::Seam> gpu;
+    if (seam->kind == DS_SEAM_ANALYTIC) {
+      // GpuSim(bm, mm, pm, GpuSim::Config{}, seed): the raw seed, default limits
+      gpu = std::make_unique<ds::AnalyticSeam>(bm, mm, ds::Seam::Config{}, seed);
+    } else {
+      ds::Scenario sc;
+      sc.seed = seed;
+      sc.max_mtl = std::max(sc.max_mtl, n);
+      sc.abs_max_bs = std::max(sc.abs_max_bs, m);
+      ds::JobSpec job;
+      job.dnn_id = dnn_id;
+      gpu = make_factory(*seam)(sc, job, bm, mm);
+    }
+    *out = to_report(ds::profile(*gpu, m, n, batches));
+  });
+}
+
 ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* o) {
   if (!r || !o) return invalid("null argument");
-  const ds::ProfileReport& p = r->trace.report;
-  *o = ds_profile_report{p.tput_base,         p.tput_batching,
-                         p.tput_mt,           p.ti_batching,
-                         p.ti_mt,             p.base_latency_ms,
-                         p.probe_latency_batching_ms, p.probe_latency_mt_ms,
-                         p.m,                 p.n,
-                         p.batches_per_point, p.base_elapsed_ms,
-                         p.batching_elapsed_ms, p.mt_elapsed_ms,
-                         p.transition_ms,     p.profiling_cost_ms,
-                         p.items_served};
+  *o = to_report(r->trace.report);
   return DS_OK;
 }
 

@@ -221,3 +221,72 @@ def test_profile_on_tape_matches_reference():
         ours = C.run_job(sc, job, cat, "replay", tape=full)
         for k, v in ref_report.items():
             assert float(ours.report[k]) == v, k
+
+
+@pytest.mark.skipif(not refo.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name", ["scenario_30jobs.json", "sensitivity_bs_down.json",
+                                  "sensitivity_mt_up.json"])
+@pytest.mark.parametrize("controller", ["dnnscaler", "clipper"])
+def test_report_writers_byte_identical_to_reference(name, controller, tmp_path):
+    """metrics.csv / summary.json from the product's writers (report.py) over
+    the product's own job results equal, byte for byte, what the reference's
+    renderers (report.cpp) write for the reference's run of the same scenario."""
+    from paper_2308_13803_b200 import report as R
+    doc = json.load(open(os.path.join(GOLDEN, name)))
+    doc["controller"] = controller
+    spath = refo.write_scenario(doc, CATALOG_JSON, str(tmp_path))
+    sc, jobs, cat_path = R.load_scenario(spath)
+    catalog = C.load_catalog(cat_path)
+    results = [C.run_job(sc, j, catalog, "analytic") for j in jobs]
+    ref_csv, ref_json = refo.render_scenario(spath)
+    assert R.render_metrics_csv(results) == ref_csv
+    assert R.render_summary_json(sc, jobs, results) == ref_json
+
+
+def test_report_writer_formats():
+    from paper_2308_13803_b200 import report as R
+    cells = [{"bs": 4, "mtl": 2, "mean_ms": 1.25, "p95_ms": 1.5, "throughput": 6400.0}]
+    assert R.render_sweep_csv(cells) == "bs,mtl,mean_ms,p95_ms,throughput\n4,2,1.250000,1.500000,6400.000000\n"
+
+
+@pytest.mark.skipif(not refo.available(), reason="oracle/_ref not built")
+def test_cli_run_and_compare_write_reference_reports(tmp_path):
+    """The CLI (cli.py, the reference CLI's subcommands) on the analytic seam:
+    run writes the reference's metrics.csv / summary.json bytes; compare writes
+    both controllers' reports and the comparison table; a missing config is an
+    error exit."""
+    from paper_2308_13803_b200 import cli
+    doc = json.load(open(os.path.join(GOLDEN, "scenario_30jobs.json")))
+    doc["jobs"] = doc["jobs"][:5]
+    spath = refo.write_scenario(doc, CATALOG_JSON, str(tmp_path))
+    out = tmp_path / "out"
+    assert cli.main(["run", "--config", spath, "--out", str(out)]) == 0
+    ref_csv, ref_json = refo.render_scenario(spath)
+    assert (out / "metrics.csv").read_text() == ref_csv
+    assert (out / "summary.json").read_text() == ref_json
+    assert cli.main(["compare", "--config", spath, "--out", str(out)]) == 0
+    comp = (out / "comparison.csv").read_text().splitlines()
+    assert comp[0].startswith("job_id,dnn_id,approach") and len(comp) == 6
+    assert cli.main(["run", "--config", str(tmp_path / "missing.json"), "--out", str(out)]) != 0
+
+
+@pytest.mark.skipif(not refo.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("dnn,m,n,seed,sigma", [(0, 32, 8, 42, None), (1, 16, 4, 7, 0.1),
+                                                (2, 64, 10, 3, 0.0)])
+def test_cli_profile_byte_identical_to_reference(dnn, m, n, seed, sigma, tmp_path, capsys):
+    """`profile` (cli.py over ds_profile_dnn) prints the reference CLI's
+    render_profile_json bytes for the same catalog, probe sizes, seed and
+    sigma override on the analytic seam."""
+    from paper_2308_13803_b200 import cli
+    cat_path = tmp_path / "catalog.json"
+    cat_path.write_text(json.dumps(CATALOG_JSON))
+    dnn_id = CATALOG_JSON[dnn]["id"]
+    argv = ["profile", "--catalog", str(cat_path), "--dnn", dnn_id, "--m", str(m), "--n", str(n),
+            "--seed", str(seed)]
+    if sigma is not None:
+        argv += ["--sigma", str(sigma)]
+    assert cli.main(argv) == 0
+    out = capsys.readouterr().out
+    ref = refo.render_profile(str(cat_path), dnn_id, m, n, 10, seed, -1.0 if sigma is None else sigma)
+    assert out.endswith(ref) and ("approach: " + json.loads(ref)["approach"]) in out
+    assert cli.main(["profile", "--catalog", str(cat_path), "--dnn", "no_such_net"]) != 0
