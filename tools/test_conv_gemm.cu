@@ -104,6 +104,25 @@ static int run(const Case& cs) {
   a.tmem_cols = conv_gemm_tmem_cols(cs.BN);
   a.y_tma = encode_tmap_out(&a.tmap_y, static_cast<uint8_t*>(dy) + cs.c_off * (cs.f32 ? 4 : 2), M,
                             cs.Cout, ldy, cs.f32) ? 1 : 0;
+  if (getenv("WIN") && cs.sh == 1 && cs.sw == 1 && cs.R * cs.S > 1 && !cs.f32) {
+    // kWindow as the engine sets it up (engine.cu): 16 x 8 pixel blocks, one
+    // halo box per 64-channel K block, 4-D TMA-store epilogue
+    mode = ConvLoadMode::kWindow;
+    a.dw_th = 16; a.dw_tw = 8; a.dw_rw = 4;
+    a.dw_tiles_y = (Ho + 15) / 16; a.dw_tiles_x = (Wo + 7) / 8;
+    a.win_iw = 8 + cs.S - 1; a.win_ih = 16 + cs.R - 1;
+    const int cb = cs.C < 64 ? cs.C : 64;
+    a.win_box_bytes = static_cast<uint32_t>(a.win_iw * a.win_ih * cb * 2);
+    a.win_direct = cs.C % 64 == 0 ? 1 : 0;
+    if (!encode_tmap_nhwc(&a.tmap_a, dx, cs.N, cs.H, cs.W, cs.C, cb, a.win_iw, a.win_ih, 1,
+                          a.win_direct != 0) ||
+        !encode_tmap_out4d(&a.tmap_y, static_cast<uint8_t*>(dy) + cs.c_off * 2, cs.N, Ho, Wo, cs.Cout,
+                           ldy, a.dw_tw, a.dw_rw)) {
+      printf("%s: window maps failed\n", cs.name);
+      return 1;
+    }
+    a.y_tma = 1;
+  }
   if (getenv("NO_TMA_STORE")) a.y_tma = 0;
   if (getenv("STAGES")) a.stages = atoi(getenv("STAGES"));
   if (getenv("DEBUG_FLAGS")) a.debug_flags = atoi(getenv("DEBUG_FLAGS"));
