@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   // (kS2D ring stages are sized for two sub-tiles: a halo box of a 64-row
   // block is still under 32 KiB)
   const SmemLayout L = smem_layout(kPair ? args.BN / 2 : args.BN, args.stages, args.Cout, epi_warps, args.b_res,
-                                   kWin ? 1 : kS2 ? 2 : args.mt,
+                                   kWin ? 0 : kS2 ? 2 : args.mt,
                                    kWin ? static_cast<int>(args.win_box_bytes) : 0, !kBlk && args.y_narrow != 0);
   const uint32_t win_stride = (args.win_box_bytes + 1023) / 1024 * 1024;
   const int mt = args.mt;  // 128-row sub-tiles per tile (one accumulator: mt x BN columns)
@@ -1594,7 +1594,7 @@ bool window_rings(int R, int S, int C, int cout, int BN, int box_bytes, int& b_r
   const int res_bytes = cblocks * taps * BN * 128;
   const int n_tiles = (cout + BN - 1) / BN;
   auto fits = [&](int res_blocks, int tm, int st) {
-    const int total = static_cast<int>(smem_layout(BN, st, cout, 4 * tm, res_blocks, 1, box_bytes).total);
+    const int total = static_cast<int>(smem_layout(BN, st, cout, 4 * tm, res_blocks, 0, box_bytes).total);
     (void)win;
     return total + 1024 <= 227 * 1024;
   };
@@ -1605,8 +1605,11 @@ bool window_rings(int R, int S, int C, int cout, int BN, int box_bytes, int& b_r
       return true;
     }
   }
+  // (window ring stages carry one tap's weight tile only — no A sub-tile —
+  // so the freed space buys ring depth: 28^2 3x3 128->128 at bs 256 95.7 ->
+  // 66.8 us, 35^2 3x3 64->96 41.2 -> 28.2 us going from 2 to 6+ stages)
   for (int tm = 2; tm >= 1; --tm)
-    for (int st = 6; st >= 2; --st)
+    for (int st = 8; st >= 2; --st)
       if (fits(0, tm, st)) {
         b_res = 0, teams = tm, stages = st;
         return true;
@@ -1822,7 +1825,7 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
       return cudaErrorInvalidValue;
   }
   const size_t smem =
-      win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, args.b_res, 1,
+      win ? smem_layout(args.BN, args.stages, args.Cout, 4 * args.teams, args.b_res, 0,
                         static_cast<int>(args.win_box_bytes)).total + 1024
           : conv_gemm_smem_bytes(pair ? args.BN / 2 : args.BN, args.stages, args.Cout, 4 * args.teams,
                                  args.b_res, s2 ? 2 : args.mt, args.y_narrow != 0);
@@ -1832,6 +1835,12 @@ cudaError_t launch_conv_gemm(const ConvGemmArgs& in_args, ConvLoadMode mode, cud
   const int by_smem = static_cast<int>((227 * 1024) / smem);
   const int by_tmem = static_cast<int>(512 / args.tmem_cols);
   const int per_sm = std::max(1, std::min(by_smem, by_tmem));
+  if (std::getenv("DS_CONV_DEBUG"))  // bring-up: the launch's derived configuration
+    std::fprintf(stderr,
+                 "conv_gemm mode %d: BN %d mt %d stages %d b_res %d teams %d tpa %d n_acc %d smem %zu "
+                 "per_sm %d tiles %d\n",
+                 static_cast<int>(mode), args.BN, args.mt, args.stages, args.b_res, args.teams, args.tpa,
+                 args.n_acc, smem, per_sm, tiles);
   if (pair) {  // CTA pairs over (M-block pair, N block) units
     if (args.mt != 1) return cudaErrorInvalidValue;
     const int m_blocks = (args.M + kConvBM - 1) / kConvBM;
