@@ -63,10 +63,11 @@ bool pair_gather_on(int bn) {
 
 // Stride-1 R x S convs as kWindow (shifted-window MMAs, no im2col). Default:
 // only where the halo box is read in place (C % 64 == 0) and the map is at
-// least 56 x 56: ResNet's 56^2 3x3s run in 44 % of the gather's time, but at
-// 28^2 the gather wins (76 vs 88 us: with 128 channels the weights stream per
-// tap, 288 KB per 128-pixel tile, and the 16 x 8 tiles waste a third of the
-// rows); with the transposed (C % 64 != 0) boxes the gather is always faster.
+// least 56 x 56: ResNet's 56^2 3x3s run in half the pair gather's time; at
+// 28^2 / 35^2 the window ties or wins per layer (64.2 vs 64.5 us, 26.6 vs
+// 32.2 us) but the power-capped networks do not move, and below that the
+// 16 x 8 tiles waste too many rows; with the transposed (C % 64 != 0) boxes
+// the gather is always faster.
 // DS_CONV_WINDOW_MIN overrides the map side.
 // DS_CONV_WINDOW=1: every eligible conv; DS_CONV_WINDOW=0: none (A/B).
 int window_mode() {
