@@ -320,6 +320,13 @@ void ds_job_session_free(ds_job_session* s);
 size_t ds_job_result_records(const ds_job_result* r, ds_metrics_record* out, size_t cap);
 ds_status ds_job_result_summary(const ds_job_result* r, ds_job_summary* out);
 ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* out);
+/* The B x MT grid on a catalog network's analytic model (reference
+ * harness.cpp:356-386, CLI cmd_sweep at dnnscaler_main.cpp:186-199; sigma < 0
+ * means 0, as the CLI does): n_bs * n_mtl cells, bs-major, each
+ * (bs, mtl, mean_ms, p95_ms, throughput) written as 5 doubles to cells. */
+ds_status ds_combination_sweep(const ds_dnn_profile* catalog, int n_catalog, const char* dnn_id,
+                               const int* bs_list, int n_bs, const int* mtl_list, int n_mtl,
+                               int samples, uint64_t seed, double sigma, double* cells);
 /* The Profiler alone on one catalog network (reference tools/dnnscaler_main.cpp:88-99,
  * cmd_profile): sigma < 0 takes the catalog's sigma (else 0.05); the ANALYTIC
  * seam is GpuSim(bm, mm, pm, Config{}, seed) with the raw seed, as the

@@ -444,6 +444,18 @@ using SeamFactory = std::function<std::unique_ptr<Seam>(
     const Scenario&, const JobSpec&, const BatchingModel&, const MtModel&)>;
 SeamFactory analytic_seam_factory();
 
+// B x MT grid on the analytic model (reference harness.cpp:356-386): per
+// cell `samples` draws of the instance's mean batch latency x lognormal noise
+// from one RandomStream(seed) in bs-major order.
+struct SweepCell {
+  int bs = 0, mtl = 0;
+  double mean_ms = 0.0, p95_ms = 0.0, throughput = 0.0;
+};
+std::vector<SweepCell> combination_sweep(const BatchingModel& bm, const MtModel& mm,
+                                         const std::vector<int>& bs_list,
+                                         const std::vector<int>& mtl_list, int samples,
+                                         uint64_t seed);
+
 std::vector<std::vector<double>> derive_mt_rows(const std::vector<DnnProfile>& catalog,
                                                 const std::string& exclude_id, int width);
 const DnnProfile& find_dnn(const std::vector<DnnProfile>& catalog, const std::string& id);

@@ -51,6 +51,9 @@ def lib() -> ctypes.CDLL:
         l.ref_render_profile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                          ctypes.c_double, vp, sz, psz, ctypes.c_char_p, sz]
+        l.ref_render_sweep.argtypes = [ctypes.c_char_p, ctypes.c_char_p, vp, ctypes.c_int, vp,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                       vp, sz, psz, ctypes.c_char_p, sz]
         _lib = l
     return _lib
 
@@ -140,6 +143,21 @@ def render_profile(catalog_path: str, dnn_id: str, m=32, n=8, batches=10, seed=4
     js = ctypes.create_string_buffer(a.value + 1)
     l.ref_render_profile(*args, js, a.value, ctypes.byref(a), err, 512)
     return js.raw[:a.value].decode()
+
+
+def render_sweep(catalog_path: str, dnn_id: str, bs, mtl, samples=100, seed=42, sigma=-1.0):
+    """The reference CLI's `sweep` sweep.csv (dnnscaler_main.cpp:186-199)."""
+    l = lib()
+    b = (ctypes.c_int * len(bs))(*bs)
+    m = (ctypes.c_int * len(mtl))(*mtl)
+    a = ctypes.c_size_t()
+    err = ctypes.create_string_buffer(512)
+    args = (catalog_path.encode(), dnn_id.encode(), b, len(bs), m, len(mtl), samples, seed, sigma)
+    if l.ref_render_sweep(*args, None, 0, ctypes.byref(a), err, 512) != 0:
+        raise RuntimeError(err.value.decode())
+    buf = ctypes.create_string_buffer(a.value + 1)
+    l.ref_render_sweep(*args, buf, a.value, ctypes.byref(a), err, 512)
+    return buf.raw[:a.value].decode()
 
 
 def tempdir():

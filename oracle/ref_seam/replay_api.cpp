@@ -215,6 +215,29 @@ int ref_render_profile(const char* catalog_path, const char* dnn_id, int m, int 
   }
 }
 
+// The reference CLI's sweep subcommand body (tools/dnnscaler_main.cpp:186-199)
+// rendered with render_sweep_csv (report.cpp:104-119).
+int ref_render_sweep(const char* catalog_path, const char* dnn_id, const int* bs, int n_bs,
+                     const int* mtl, int n_mtl, int samples, uint64_t seed, double sigma, char* csv,
+                     size_t cap, size_t* len, char* err, size_t err_cap) {
+  try {
+    const auto catalog = load_catalog(catalog_path);
+    const auto& dnn = find_dnn(catalog, dnn_id);
+    const double used_sigma = sigma >= 0.0 ? sigma : 0.0;
+    const auto cells = combination_sweep(calibrate_batching(dnn.batching_points, used_sigma),
+                                         calibrate_mt(dnn.mt_points, used_sigma),
+                                         std::vector<int>(bs, bs + n_bs),
+                                         std::vector<int>(mtl, mtl + n_mtl), samples, seed);
+    const std::string c = render_sweep_csv(cells);
+    *len = c.size();
+    if (csv && cap >= c.size()) std::memcpy(csv, c.data(), c.size());
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, err_cap, e.what());
+    return 2;
+  }
+}
+
 }  // extern "C"
 
 // The reference's generator (random.hpp:10-47), for pinning the oracles'

@@ -93,14 +93,22 @@ def cmd_compare(args) -> int:
 
 
 def cmd_sweep(args) -> int:
-    """B x MT grid on the B200 (GpuBackend.combination_sweep, reference
-    harness.cpp:356-386 on the device)."""
-    from .backend import Config, GpuBackend
+    """== cmd_sweep (reference dnnscaler_main.cpp:186-199): the B x MT grid,
+    on the catalog's analytic model (the reference's combination_sweep) or
+    measured on the B200 (GpuBackend.combination_sweep, --seam device)."""
     bs = [int(x) for x in args.bs.split(",")]
     mtl = [int(x) for x in args.mtl.split(",")]
-    with GpuBackend(args.dnn, Config(max(bs), max(max(mtl), 2)), seed=args.seed or 42,
-                    device=args.device) as be:
-        cells = be.combination_sweep(bs, mtl, args.samples)
+    seed = args.seed if args.seed is not None else 42
+    if args.seam == "analytic":
+        from .serving import B200_CATALOG
+        catalog = C.load_catalog(args.catalog or B200_CATALOG)
+        cells = C.combination_sweep(catalog, args.dnn, bs, mtl, args.samples, seed,
+                                    args.sigma if args.sigma is not None else -1.0)
+    else:
+        from .backend import Config, GpuBackend
+        with GpuBackend(args.dnn, Config(max(bs), max(max(mtl), 2)), seed=seed,
+                        device=args.device) as be:
+            cells = be.combination_sweep(bs, mtl, args.samples)
     text = R.render_sweep_csv(cells)
     _write(args.out, "sweep.csv", text)
     sys.stdout.write(text)
@@ -144,13 +152,16 @@ def main(argv=None) -> int:
     scen(sub.add_parser("run", help="run a scenario, write metrics.csv + summary.json"))
     scen(sub.add_parser("compare", help="DNNScaler and Clipper side by side"), controller=False)
     scen(sub.add_parser("sensitivity", help="jobs that step their SLO mid-run"))
-    sw = sub.add_parser("sweep", help="batch size x instance count grid on the B200")
+    sw = sub.add_parser("sweep", help="batch size x instance count grid")
+    sw.add_argument("--catalog", default="", help="catalog JSON (default: the B200 catalog)")
     sw.add_argument("--dnn", required=True)
     sw.add_argument("--bs", required=True)
     sw.add_argument("--mtl", required=True)
     sw.add_argument("--out", default=".")
     sw.add_argument("--samples", type=int, default=100)
     sw.add_argument("--seed", type=int, default=None)
+    sw.add_argument("--sigma", type=float, default=None, help="latency noise scale (analytic)")
+    sw.add_argument("--seam", default="analytic", choices=["analytic", "device"])
     sw.add_argument("--device", type=int, default=0)
     pr = sub.add_parser("profile", help="probe one network and print the decision")
     pr.add_argument("--dnn", required=True)

@@ -106,6 +106,9 @@ _SIGS = {
     "ds_job_result_records": (ctypes.c_size_t, [_vp, _P(_Record), ctypes.c_size_t]),
     "ds_job_result_summary": (ctypes.c_int, [_vp, _P(_Summary)]),
     "ds_job_result_profile": (ctypes.c_int, [_vp, _P(_Report)]),
+    "ds_combination_sweep": (ctypes.c_int, [_P(_DnnProfile), ctypes.c_int, ctypes.c_char_p, _vp,
+                                            ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_uint64, ctypes.c_double, _vp]),
     "ds_profile_dnn": (ctypes.c_int, [_P(_DnnProfile), ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                       _P(_SeamSpec), _P(_Report)]),
@@ -351,6 +354,22 @@ def profile_dnn(catalog: Sequence[DnnProfile], dnn_id: str, m: int = 32, n: int 
     _lib.check(lib.ds_profile_dnn(mar.catalog, mar.n_catalog, dnn_id.encode(), m, n, batches, seed,
                                   sigma, ctypes.byref(spec), ctypes.byref(rp)))
     return {name: getattr(rp, name) for name, _ in _Report._fields_}
+
+
+def combination_sweep(catalog: Sequence[DnnProfile], dnn_id: str, bs_list, mtl_list,
+                      samples: int = 100, seed: int = 42, sigma: float = -1.0) -> list:
+    """The B x MT grid on a catalog network's analytic model (reference
+    harness.cpp:356-386 via the CLI's cmd_sweep): cells as dicts, bs-major."""
+    lib = _l()
+    mar = _Marshal(Scenario(), JobSpec(0, dnn_id, 1.0, 1.0), catalog)
+    bs = np.ascontiguousarray(bs_list, dtype=np.int32)
+    mt = np.ascontiguousarray(mtl_list, dtype=np.int32)
+    out = np.zeros((max(1, bs.size * mt.size), 5), dtype=np.float64)
+    _lib.check(lib.ds_combination_sweep(mar.catalog, mar.n_catalog, dnn_id.encode(), bs.ctypes.data,
+                                        bs.size, mt.ctypes.data, mt.size, samples, seed, sigma,
+                                        out.ctypes.data))
+    return [{"bs": int(r[0]), "mtl": int(r[1]), "mean_ms": float(r[2]), "p95_ms": float(r[3]),
+             "throughput": float(r[4])} for r in out[:bs.size * mt.size]]
 
 
 class JobSession:

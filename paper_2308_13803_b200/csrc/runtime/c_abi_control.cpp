@@ -294,6 +294,31 @@ ds_status ds_profile_dnn(const ds_dnn_profile* catalog, int n_catalog, const cha
   });
 }
 
+ds_status ds_combination_sweep(const ds_dnn_profile* catalog, int n_catalog, const char* dnn_id,
+                               const int* bs_list, int n_bs, const int* mtl_list, int n_mtl,
+                               int samples, uint64_t seed, double sigma, double* cells) {
+  if (!dnn_id || !cells || n_bs < 0 || n_mtl < 0 || (n_bs > 0 && !bs_list) ||
+      (n_mtl > 0 && !mtl_list) || (n_catalog > 0 && !catalog))
+    return invalid("null argument");
+  return guard([&] {
+    const auto cat = to_catalog(catalog, n_catalog);
+    const ds::DnnProfile& dnn = ds::find_dnn(cat, dnn_id);
+    const double used_sigma = sigma >= 0.0 ? sigma : 0.0;
+    const auto out = ds::combination_sweep(ds::calibrate_batching(dnn.batching_points, used_sigma),
+                                           ds::calibrate_mt(dnn.mt_points, used_sigma),
+                                           std::vector<int>(bs_list, bs_list + n_bs),
+                                           std::vector<int>(mtl_list, mtl_list + n_mtl), samples, seed);
+    for (size_t i = 0; i < out.size(); ++i) {
+      double* c = cells + 5 * i;
+      c[0] = out[i].bs;
+      c[1] = out[i].mtl;
+      c[2] = out[i].mean_ms;
+      c[3] = out[i].p95_ms;
+      c[4] = out[i].throughput;
+    }
+  });
+}
+
 ds_status ds_job_result_profile(const ds_job_result* r, ds_profile_report* o) {
   if (!r || !o) return invalid("null argument");
   *o = to_report(r->trace.report);

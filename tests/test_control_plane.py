@@ -290,3 +290,25 @@ def test_cli_profile_byte_identical_to_reference(dnn, m, n, seed, sigma, tmp_pat
     ref = refo.render_profile(str(cat_path), dnn_id, m, n, 10, seed, -1.0 if sigma is None else sigma)
     assert out.endswith(ref) and ("approach: " + json.loads(ref)["approach"]) in out
     assert cli.main(["profile", "--catalog", str(cat_path), "--dnn", "no_such_net"]) != 0
+
+
+@pytest.mark.skipif(not refo.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("dnn,seed,sigma", [(0, 42, None), (3, 7, 0.08), (5, 1, 0.0)])
+def test_cli_sweep_byte_identical_to_reference(dnn, seed, sigma, tmp_path, capsys):
+    """`sweep` on the analytic seam (ds_combination_sweep) writes the
+    reference CLI's sweep.csv bytes: same grid, noise draws and percentiles."""
+    from paper_2308_13803_b200 import cli
+    cat_path = tmp_path / "catalog.json"
+    cat_path.write_text(json.dumps(CATALOG_JSON))
+    dnn_id = CATALOG_JSON[dnn]["id"]
+    bs, mtl = [1, 4, 16, 64], [1, 2, 3, 8]
+    argv = ["sweep", "--catalog", str(cat_path), "--dnn", dnn_id, "--bs", ",".join(map(str, bs)),
+            "--mtl", ",".join(map(str, mtl)), "--out", str(tmp_path), "--samples", "50",
+            "--seed", str(seed)]
+    if sigma is not None:
+        argv += ["--sigma", str(sigma)]
+    assert cli.main(argv) == 0
+    ref = refo.render_sweep(str(cat_path), dnn_id, bs, mtl, 50, seed, -1.0 if sigma is None else sigma)
+    assert (tmp_path / "sweep.csv").read_text() == ref
+    assert capsys.readouterr().out == ref
+    assert cli.main(argv + ["--samples", "0"]) == 2  # std::invalid_argument -> exit 2, as the reference
