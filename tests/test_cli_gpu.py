@@ -34,6 +34,6 @@ def test_cli_profile_and_sweep_on_device(tmp_path, capsys):
     out = capsys.readouterr().out
     assert "approach:" in out and '"tput_base"' in out
     assert cli.main(["sweep", "--dnn", "synthetic_cnn", "--bs", "1,8", "--mtl", "1,2", "--out",
-                     str(tmp_path), "--samples", "10"]) == 0
+                     str(tmp_path), "--samples", "10", "--seam", "device"]) == 0
     lines = (tmp_path / "sweep.csv").read_text().splitlines()
     assert lines[0] == "bs,mtl,mean_ms,p95_ms,throughput" and len(lines) == 5
