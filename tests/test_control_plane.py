@@ -312,3 +312,24 @@ def test_cli_sweep_byte_identical_to_reference(dnn, seed, sigma, tmp_path, capsy
     assert (tmp_path / "sweep.csv").read_text() == ref
     assert capsys.readouterr().out == ref
     assert cli.main(argv + ["--samples", "0"]) == 2  # std::invalid_argument -> exit 2, as the reference
+
+
+@pytest.mark.skipif(not refo.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name", ["sensitivity_bs_up.json", "sensitivity_mt_down.json"])
+def test_cli_sensitivity_writes_reference_reports(name, tmp_path, capsys):
+    """`sensitivity` (the reference CLI's cmd_sensitivity): the reference's
+    report bytes, one readaptation line per SLO step; a scenario without an
+    slo_schedule is refused with the reference's exit code 2."""
+    from paper_2308_13803_b200 import cli
+    doc = json.load(open(os.path.join(GOLDEN, name)))
+    spath = refo.write_scenario(doc, CATALOG_JSON, str(tmp_path))
+    out = tmp_path / "out"
+    assert cli.main(["sensitivity", "--config", spath, "--out", str(out)]) == 0
+    ref_csv, ref_json = refo.render_scenario(spath)
+    assert (out / "metrics.csv").read_text() == ref_csv
+    assert (out / "summary.json").read_text() == ref_json
+    steps = sum(len(j.get("slo_schedule", [])) for j in doc["jobs"])
+    assert capsys.readouterr().out.count(": slo step at ") == steps
+    plain = dict(doc, jobs=[{k: v for k, v in j.items() if k != "slo_schedule"} for j in doc["jobs"]])
+    ppath = refo.write_scenario(plain, CATALOG_JSON, str(tmp_path / "plain"))
+    assert cli.main(["sensitivity", "--config", ppath, "--out", str(out)]) == 2
