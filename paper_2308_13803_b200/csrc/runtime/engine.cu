@@ -49,6 +49,16 @@ bool pair_on(int bn) {
   return m == 1 && bn >= 128;
 }
 
+// 1x1s with K <= 64 and several N tiles are bound by their output stores,
+// not by weight traffic: single-CTA 128-column tiles (two 128-row sub-tiles
+// per tile, all sixteen epilogue warps) beat CTA-pair 192-column tiles —
+// ResNet's fused 56^2 64 -> 64 + 256 at bs 256: 152 -> 116 us
+// (tools/test_conv_gemm). DS_CONV_K64_BN128=0: off (A/B).
+bool k64_bn128_on(int num_kb, int cout) {
+  const char* e = std::getenv("DS_CONV_K64_BN128");
+  return !(e && e[0] == '0') && num_kb == 1 && cout > 256;
+}
+
 // Gather (and opt-in TMA im2col) convs on CTA pairs: M = 256 pair MMAs, each
 // CTA gathering its own 128 A rows and staging half of every weight block
 // (kPairGather; the peer's gather completion is forwarded to the leader).
@@ -395,10 +405,17 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
     }
     if (op.residual >= 0 && pl.mode != ConvLoadMode::kTmaA)
       throw std::logic_error("residual adds are supported on 1x1 stride-1 convs only");
+    const bool k64 = pl.mode == ConvLoadMode::kTmaA && op.kind == OpKind::kConv &&
+                     k64_bn128_on(a.num_kb, p.cout);
+    if (k64) {
+      a.BN = 128;
+      a.stages = choose_stages(a.BN, p.cout);
+      a.tmem_cols = tmem_cols_for(a.BN);
+    }
     // streamed-weight TMA-A layers run on CTA pairs
     const bool b_resident = (p.cout + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
     a.cluster = 1;
-    if (pl.mode == ConvLoadMode::kTmaA && !b_resident && pair_on(a.BN)) {
+    if (pl.mode == ConvLoadMode::kTmaA && !b_resident && !k64 && pair_on(a.BN)) {
       pl.mode = ConvLoadMode::kPairTmaA;
       a.cluster = 2;  // (tmap_b boxes of BN / 2 rows: each CTA's half)
     } else if (pl.mode == ConvLoadMode::kIm2col && pair_gather_on(a.BN)) {
@@ -465,7 +482,9 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       a.seg_col[a.nseg] = col;
       a.relu = 1;  // (per segment through seg_norelu)
       a.Cout = col;
-      a.BN = choose_bn(col);
+      const bool k64 = (pl.mode == ConvLoadMode::kTmaA || pl.mode == ConvLoadMode::kPairTmaA) &&
+                       k64_bn128_on(a.num_kb, col);
+      a.BN = k64 ? 128 : choose_bn(col);
       a.stages = choose_stages(a.BN, col);
       a.tmem_cols = tmem_cols_for(a.BN);
       a.bias = reinterpret_cast<const float*>(base + fb_off[i]);
@@ -474,7 +493,7 @@ Instance::Instance(const ModelSpec& m, int max_bs, int device)
       if (pl.mode == ConvLoadMode::kPairGather) pl.mode = ConvLoadMode::kGather16;
       if (pl.mode == ConvLoadMode::kPairIm2col) pl.mode = ConvLoadMode::kIm2col;
       const bool b_res = (col + a.BN - 1) / a.BN == 1 && a.num_kb * a.BN * 128 <= 64 * 1024;
-      if (pl.mode == ConvLoadMode::kTmaA && !b_res && pair_on(a.BN)) {
+      if (pl.mode == ConvLoadMode::kTmaA && !b_res && !k64 && pair_on(a.BN)) {
         pl.mode = ConvLoadMode::kPairTmaA;
         a.cluster = 2;
       } else if (pl.mode == ConvLoadMode::kGather16 && pair_gather_on(a.BN)) {

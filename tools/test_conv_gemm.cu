@@ -274,6 +274,8 @@ int main(int argc, char** argv) {
       {"in 35 3x3 c64 bs128", 128, 35, 35, 64, 3, 3, 1, 1, 1, 1, 96, 96, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"in 35 3x3 c64 n64 bs128", 128, 35, 35, 64, 3, 3, 1, 1, 1, 1, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"rn 56 3x3 bs256", 256, 56, 56, 64, 3, 3, 1, 1, 1, 1, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
+      {"rn 56 1x1 64-320 bs256", 256, 56, 56, 64, 1, 1, 1, 1, 0, 0, 320, 192, ConvLoadMode::kTmaA, false, false, true, 0, 0},
+      {"rn 56 1x1 64-256 res bs256", 256, 56, 56, 64, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, true, false, true, 0, 0},
       {"small 5x5 c48 chk", 2, 11, 9, 48, 5, 5, 1, 1, 2, 2, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3 c128 chk", 3, 10, 12, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3s2 c64 chk", 3, 15, 13, 64, 3, 3, 2, 2, 1, 1, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
