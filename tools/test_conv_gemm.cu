@@ -276,6 +276,10 @@ int main(int argc, char** argv) {
       {"rn 56 3x3 bs256", 256, 56, 56, 64, 3, 3, 1, 1, 1, 1, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"rn 56 1x1 64-320 bs256", 256, 56, 56, 64, 1, 1, 1, 1, 0, 0, 320, 192, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"rn 56 1x1 64-256 res bs256", 256, 56, 56, 64, 1, 1, 1, 1, 0, 0, 256, 256, ConvLoadMode::kTmaA, true, false, true, 0, 0},
+      {"rn 28 1x1 128-512 res bs256", 256, 28, 28, 128, 1, 1, 1, 1, 0, 0, 512, 256, ConvLoadMode::kTmaA, true, false, true, 0, 0},
+      {"rn 14 1x1 256-1024 res bs256", 256, 14, 14, 256, 1, 1, 1, 1, 0, 0, 1024, 256, ConvLoadMode::kTmaA, true, false, true, 0, 0},
+      {"rn 7 1x1 512-2048 res bs256", 256, 7, 7, 512, 1, 1, 1, 1, 0, 0, 2048, 256, ConvLoadMode::kTmaA, true, false, true, 0, 0},
+      {"rn 28 1x1 512-128 bs256", 256, 28, 28, 512, 1, 1, 1, 1, 0, 0, 128, 128, ConvLoadMode::kTmaA, false, false, true, 0, 0},
       {"small 5x5 c48 chk", 2, 11, 9, 48, 5, 5, 1, 1, 2, 2, 64, 64, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3 c128 chk", 3, 10, 12, 128, 3, 3, 1, 1, 1, 1, 128, 128, ConvLoadMode::kGather16, false, false, true, 0, 0},
       {"small 3x3s2 c64 chk", 3, 15, 13, 64, 3, 3, 2, 2, 1, 1, 192, 192, ConvLoadMode::kGather16, false, false, true, 0, 0},
